@@ -1,0 +1,870 @@
+// api.cpp — the C ABI (include/fleetplace_b200.h): validation, host-side
+// selection logic, device memory and the search orchestration around the
+// kernels in table_rank_kernels.cu and search_kernels.cu.
+//
+// Host logic kept here is the reference's O(B log B) / O(V) bookkeeping
+// (sorting bases, helipad cap, placement order, pool construction, input
+// validation) and the sequential mt19937_64 permutation stream; everything
+// that touches the M x B table runs on the device.
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <random>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "host_common.hpp"
+
+namespace fpk_host {
+void generate_instance(uint64_t pool_seed, const double* bbox, int aerodromes, int helipads,
+                       int health_sites, int missions, double rotary_only_fraction,
+                       uint64_t seed, int rotary, int fixed_wing, int32_t* base_id,
+                       uint8_t* base_kind, double* base_lat, double* base_lon,
+                       int32_t* vehicle_id, uint8_t* vehicle_kind, int32_t* mission_id,
+                       double* pickup_lat, double* pickup_lon, double* delivery_lat,
+                       double* delivery_lon, uint8_t* rotary_only);
+}
+
+using fpk_host::CudaError;
+using fpk_host::FpError;
+
+struct fp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  double* d_cost = nullptr;
+  size_t cost_cap = 0;  // elements
+  int M = -1, B = -1;
+  uint64_t launches = 0;
+  // pinned staging for permutations (double-buffered)
+  int32_t* h_perm[2] = {nullptr, nullptr};
+  size_t perm_cap = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+fp_status fail(fp_status c, const std::string& m) {
+  g_err = m;
+  return c;
+}
+
+template <typename F>
+fp_status guarded(F&& f) {
+  try {
+    f();
+    return FP_OK;
+  } catch (const FpError& e) {
+    return fail(e.code, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(FP_ERR_OUT_OF_MEMORY, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(FP_ERR_ERROR, e.what());
+  }
+}
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(e, what);
+}
+
+// RAII device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    free_();
+    n = count;
+    if (count) check(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+  }
+  void free_() {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  ~DBuf() { free_(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+};
+
+template <typename T>
+void h2d(T* d, const T* h, size_t n, cudaStream_t st) {
+  if (n) check(cudaMemcpyAsync(d, h, sizeof(T) * n, cudaMemcpyHostToDevice, st), "H2D");
+}
+template <typename T>
+void d2h(T* h, const T* d, size_t n, cudaStream_t st) {
+  if (n) check(cudaMemcpyAsync(h, d, sizeof(T) * n, cudaMemcpyDeviceToHost, st), "D2H");
+}
+
+void ensure_table(const fp_ctx* ctx, int M, int B) {
+  if (ctx->M != M || ctx->B != B || (size_t)M * B > 0 && !ctx->d_cost)
+    throw FpError(FP_ERR_INVALID_ARGUMENT,
+                  "no resident distance table of shape " + std::to_string(M) + "x" +
+                      std::to_string(B) + " (call fp_build_distance_table or fp_table_upload)");
+}
+
+void table_alloc(fp_ctx* ctx, int M, int B) {
+  const size_t need = (size_t)M * (size_t)B;
+  if (need > ctx->cost_cap) {
+    if (ctx->d_cost) cudaFree(ctx->d_cost);
+    ctx->d_cost = nullptr;
+    ctx->cost_cap = 0;
+    check(cudaMalloc(&ctx->d_cost, sizeof(double) * need), "cudaMalloc(table)");
+    ctx->cost_cap = need;
+  }
+  ctx->M = M;
+  ctx->B = B;
+}
+
+bool valid_point(double lat, double lon) {
+  return lat >= -90.0 && lat <= 90.0 && lon >= -180.0 && lon <= 180.0;
+}
+
+// validate_instance, proj/src/model.cpp:46-74 (same checks, same order).
+void validate(const fp_instance* in) {
+  if (in->n_vehicles <= 0) throw FpError(FP_ERR_VALIDATION, "validation failed for fleet: must not be empty");
+  if (in->n_bases <= 0) throw FpError(FP_ERR_VALIDATION, "validation failed for bases: must not be empty");
+  {
+    std::unordered_map<int, int> seen;
+    seen.reserve(in->n_bases * 2);
+    for (int b = 0; b < in->n_bases; ++b) {
+      if (!seen.emplace(in->base_id[b], b).second)
+        throw FpError(FP_ERR_VALIDATION, "validation failed for base " +
+                                             std::to_string(in->base_id[b]) + ": duplicate id");
+      if (!valid_point(in->base_lat[b], in->base_lon[b]))
+        throw FpError(FP_ERR_VALIDATION, "validation failed for base " +
+                                             std::to_string(in->base_id[b]) +
+                                             ": coordinates out of range");
+    }
+  }
+  {
+    std::unordered_map<int, int> seen;
+    for (int v = 0; v < in->n_vehicles; ++v)
+      if (!seen.emplace(in->vehicle_id[v], v).second)
+        throw FpError(FP_ERR_VALIDATION, "validation failed for vehicle " +
+                                             std::to_string(in->vehicle_id[v]) + ": duplicate id");
+  }
+  {
+    std::unordered_map<int, int> seen;
+    seen.reserve((size_t)in->n_missions * 2);
+    for (int m = 0; m < in->n_missions; ++m) {
+      if (!seen.emplace(in->mission_id[m], m).second)
+        throw FpError(FP_ERR_VALIDATION, "validation failed for mission " +
+                                             std::to_string(in->mission_id[m]) + ": duplicate id");
+      if (!valid_point(in->pickup_lat[m], in->pickup_lon[m]) ||
+          !valid_point(in->delivery_lat[m], in->delivery_lon[m]))
+        throw FpError(FP_ERR_VALIDATION, "validation failed for mission " +
+                                             std::to_string(in->mission_id[m]) +
+                                             ": coordinates out of range");
+    }
+  }
+  int aero = 0, fixed = 0;
+  for (int b = 0; b < in->n_bases; ++b) aero += in->base_kind[b] == FP_AERODROME;
+  for (int v = 0; v < in->n_vehicles; ++v) fixed += in->vehicle_kind[v] == FP_FIXED;
+  if (aero < fixed)
+    throw FpError(FP_ERR_VALIDATION,
+                  "validation failed for fleet: needs at least one aerodrome per fixed-wing vehicle");
+}
+
+// ---- permutations (proj/include/fleetplace/rng.hpp:14-42) ------------------
+struct PermStream {
+  std::mt19937_64 rng;
+  explicit PermStream(uint64_t seed) : rng(seed) {}
+  uint64_t below(uint64_t n) {
+    const uint64_t threshold = (0 - n) % n;
+    uint64_t x = rng();
+    while (x < threshold) x = rng();
+    return x % n;
+  }
+  void perm(int n, int32_t* out) {
+    for (int i = 0; i < n; ++i) out[i] = i;
+    for (int64_t i = n; i > 1; --i) {
+      const int64_t j = (int64_t)below((uint64_t)i);
+      std::swap(out[i - 1], out[j]);
+    }
+  }
+};
+
+// ---- search setup -------------------------------------------------------------
+struct HostScenario {
+  const fp_instance* in;
+  std::vector<int32_t> vbase, mv, vcount, bveh, pkind, pidx, vrk, brk;
+  std::vector<uint8_t> vfixed, bheli;
+  int K = 0;
+  int psize = 0;
+};
+
+// tabu_search / local_search preconditions (proj/src/search.cpp:438-460)
+// and SearchState::from (proj/src/search.cpp:14-65), index form.
+HostScenario prepare(const fp_instance* in, const fp_search_start* st) {
+  HostScenario h;
+  h.in = in;
+  const int V = in->n_vehicles, B = in->n_bases, M = in->n_missions;
+  h.vbase.assign(V, -1);
+  h.mv.assign(M, -1);
+  h.bveh.assign(B, -1);
+  h.vcount.assign(V, 0);
+  // placement, iterated in vehicle-id order like std::map<int,int>
+  std::vector<int> vorder(V);
+  std::iota(vorder.begin(), vorder.end(), 0);
+  std::sort(vorder.begin(), vorder.end(),
+            [&](int a, int b) { return in->vehicle_id[a] < in->vehicle_id[b]; });
+  for (int v : vorder) {
+    const int b = st->vehicle_base[v];
+    if (b == -1) continue;
+    if (b < -1 || b >= B) throw FpError(FP_ERR_INFEASIBLE, "assignment references unknown ids");
+    h.vbase[v] = b;
+    h.bveh[b] = v;
+  }
+  for (int m = 0; m < M; ++m) {
+    const int v = st->mission_vehicle[m];
+    if (v == -1) continue;
+    if (v < -1 || v >= V || h.vbase[v] < 0)
+      throw FpError(FP_ERR_INFEASIBLE, "service references unplaced vehicle");
+    h.mv[m] = v;
+    h.vcount[v] += 1;
+  }
+  for (int m = 0; m < M; ++m)
+    if (h.mv[m] < 0) throw FpError(FP_ERR_INFEASIBLE, "search start must serve every mission");
+  for (int k = 0; k < st->pool_size; ++k) {
+    const int x = st->pool_index[k];
+    if (st->pool_kind[k] == FP_POOL_EMPTY_BASE) {
+      if (x < 0 || x >= B || h.bveh[x] >= 0)
+        throw FpError(FP_ERR_INFEASIBLE, "pool lists an occupied or unknown base");
+      h.pkind.push_back(fpk::POOL_EMPTY);
+    } else {
+      if (x < 0 || x >= V || h.vcount[x] != 0)
+        throw FpError(FP_ERR_INFEASIBLE, "pool lists a busy or unknown vehicle");
+      h.pkind.push_back(fpk::POOL_IDLE);
+    }
+    h.pidx.push_back(x);
+  }
+  h.psize = st->pool_size;
+  h.vfixed.resize(V);
+  h.bheli.resize(B);
+  for (int v = 0; v < V; ++v) h.vfixed[v] = in->vehicle_kind[v] == FP_FIXED;
+  for (int b = 0; b < B; ++b) h.bheli[b] = in->base_kind[b] == FP_HELIPAD;
+  // {Relocate, id}: base ids and vehicle ids share one key space
+  // (proj/src/search.cpp:234-245, 256-263).
+  std::unordered_map<int, int> slot;
+  slot.reserve((size_t)(B + V) * 2);
+  h.brk.resize(B);
+  h.vrk.resize(V);
+  for (int b = 0; b < B; ++b) h.brk[b] = slot.emplace(in->base_id[b], (int)slot.size()).first->second;
+  for (int v = 0; v < V; ++v) h.vrk[v] = slot.emplace(in->vehicle_id[v], (int)slot.size()).first->second;
+  h.K = (int)slot.size();
+  return h;
+}
+
+long long resolve_tenure(const fp_search_config* cfg, int M) {
+  if (cfg->mode != FP_MODE_TABU) return 0;
+  if (cfg->tabu_tenure < 0)
+    throw FpError(FP_ERR_INVALID_ARGUMENT, "tabu tenure must be positive (0 = auto)");
+  const long long tenure = cfg->tabu_tenure > 0 ? cfg->tabu_tenure : 2LL * M;
+  if (tenure <= 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "tabu tenure must be positive");
+  return tenure;
+}
+
+// Device arena for n scenarios: one allocation, carved per scenario.
+struct Arena {
+  DBuf<unsigned char> mem;
+  std::vector<fpk::Scenario> scs;
+  size_t per = 0;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
+      invb, exp_take, exp_reas, exp_rel, role_rel, ctr, cost, total;
+};
+
+Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
+  Layout L{};
+  size_t o = 0;
+  auto put = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes);
+    return at;
+  };
+  L.ctr = put(sizeof(fpk::Counters));
+  L.ro = put(M);
+  L.vfixed = put(V);
+  L.bheli = put(B);
+  L.vrk = put(4ull * V);
+  L.brk = put(4ull * B);
+  L.mv = put(4ull * M);
+  L.mc = put(8ull * M);
+  L.vbase = put(4ull * V);
+  L.vcount = put(4ull * V);
+  L.bveh = put(4ull * B);
+  L.pkind = put(4ull * cap);
+  L.pidx = put(4ull * cap);
+  L.mvp = put(4ull * M);
+  L.mcp = put(8ull * M);
+  L.rop = put(M);
+  L.invb = put(4ull * M);
+  L.exp_take = put(8ull * V);
+  L.exp_reas = put(8ull * V);
+  L.exp_rel = put(8ull * K);
+  L.role_rel = put(K);
+  L.cost = own_cost ? put(8ull * M * B) : 0;
+  L.total = o;
+  return L;
+}
+
+struct SearchRun {
+  std::vector<HostScenario> hs;
+  Arena arena;
+  DBuf<fpk::Scenario> d_scs;
+  DBuf<int32_t> d_active;
+  DBuf<int32_t> d_perm;  // [2*M]
+  std::vector<Layout> lay;
+};
+
+// Shared driver for fp_search / fp_search_batch. `tables[s]` is a device
+// pointer to scenario s's table (nullptr = the scenario's arena copy).
+void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_config* cfg,
+                const fp_search_start* starts, fp_search_result* outs,
+                const std::vector<const double*>& dev_tables,
+                const std::vector<const double*>& host_tables) {
+  const int M = insts[0].n_missions;
+  for (int s = 1; s < n; ++s)
+    if (insts[s].n_missions != M)
+      throw FpError(FP_ERR_INVALID_ARGUMENT, "batch scenarios must share the mission count");
+  if (cfg->mode != FP_MODE_LOCAL && cfg->mode != FP_MODE_TABU)
+    throw FpError(FP_ERR_INVALID_ARGUMENT, "unknown search mode");
+  const bool tabu = cfg->mode == FP_MODE_TABU;
+  const long long tenure = resolve_tenure(cfg, M);
+  cudaStream_t st = ctx->stream;
+
+  SearchRun run;
+  run.hs.reserve(n);
+  for (int s = 0; s < n; ++s) run.hs.push_back(prepare(&insts[s], &starts[s]));
+
+  // ---- arena
+  size_t total = 0;
+  run.lay.resize(n);
+  std::vector<size_t> base(n);
+  int maxV = 0;
+  for (int s = 0; s < n; ++s) {
+    const HostScenario& h = run.hs[s];
+    const int V = insts[s].n_vehicles, B = insts[s].n_bases;
+    maxV = std::max(maxV, V);
+    run.lay[s] = layout(M, B, V, h.K, h.psize + V + 1, dev_tables[s] == nullptr);
+    base[s] = total;
+    total += run.lay[s].total;
+  }
+  run.arena.mem.alloc(std::max<size_t>(total, 256));
+  unsigned char* d0 = run.arena.mem.p;
+  std::vector<unsigned char> stage(total, 0);
+  run.arena.scs.resize(n);
+  for (int s = 0; s < n; ++s) {
+    const HostScenario& h = run.hs[s];
+    const Layout& L = run.lay[s];
+    const fp_instance* in = &insts[s];
+    const int V = in->n_vehicles, B = in->n_bases;
+    unsigned char* hb = stage.data() + base[s];
+    unsigned char* db = d0 + base[s];
+    fpk::Counters c{};
+    c.psize = h.psize;
+    std::memcpy(hb + L.ctr, &c, sizeof(c));
+    if (M) std::memcpy(hb + L.ro, in->rotary_only, M);
+    if (V) std::memcpy(hb + L.vfixed, h.vfixed.data(), V);
+    if (B) std::memcpy(hb + L.bheli, h.bheli.data(), B);
+    if (V) std::memcpy(hb + L.vrk, h.vrk.data(), 4ull * V);
+    if (B) std::memcpy(hb + L.brk, h.brk.data(), 4ull * B);
+    if (M) std::memcpy(hb + L.mv, h.mv.data(), 4ull * M);
+    if (V) std::memcpy(hb + L.vbase, h.vbase.data(), 4ull * V);
+    if (V) std::memcpy(hb + L.vcount, h.vcount.data(), 4ull * V);
+    if (B) std::memcpy(hb + L.bveh, h.bveh.data(), 4ull * B);
+    if (h.psize) std::memcpy(hb + L.pkind, h.pkind.data(), 4ull * h.psize);
+    if (h.psize) std::memcpy(hb + L.pidx, h.pidx.data(), 4ull * h.psize);
+    if (!dev_tables[s] && (size_t)M * B)
+      std::memcpy(hb + L.cost, host_tables[s], 8ull * M * B);
+    fpk::Scenario& S = run.arena.scs[s];
+    S.cost = dev_tables[s] ? dev_tables[s] : reinterpret_cast<const double*>(db + L.cost);
+    S.ro = db + L.ro;
+    S.vfixed = db + L.vfixed;
+    S.bheli = db + L.bheli;
+    S.vrk = reinterpret_cast<const int32_t*>(db + L.vrk);
+    S.brk = reinterpret_cast<const int32_t*>(db + L.brk);
+    S.mv = reinterpret_cast<int32_t*>(db + L.mv);
+    S.mc = reinterpret_cast<double*>(db + L.mc);
+    S.vbase = reinterpret_cast<int32_t*>(db + L.vbase);
+    S.vcount = reinterpret_cast<int32_t*>(db + L.vcount);
+    S.bveh = reinterpret_cast<int32_t*>(db + L.bveh);
+    S.pkind = reinterpret_cast<int32_t*>(db + L.pkind);
+    S.pidx = reinterpret_cast<int32_t*>(db + L.pidx);
+    S.mvp = reinterpret_cast<int32_t*>(db + L.mvp);
+    S.mcp = reinterpret_cast<double*>(db + L.mcp);
+    S.rop = db + L.rop;
+    S.invb = reinterpret_cast<int32_t*>(db + L.invb);
+    S.exp_take = reinterpret_cast<long long*>(db + L.exp_take);
+    S.exp_reas = reinterpret_cast<long long*>(db + L.exp_reas);
+    S.exp_rel = reinterpret_cast<long long*>(db + L.exp_rel);
+    S.role_rel = db + L.role_rel;
+    S.ctr = reinterpret_cast<fpk::Counters*>(db + L.ctr);
+    S.M = M;
+    S.B = B;
+    S.V = V;
+    S.K = h.K;
+    S.pool_cap = h.psize + V + 1;
+  }
+  cudaEvent_t ev0, ev1;
+  check(cudaEventCreate(&ev0), "event");
+  check(cudaEventCreate(&ev1), "event");
+  check(cudaEventRecord(ev0, st), "event");
+  h2d(d0, stage.data(), total, st);
+  run.d_scs.alloc(n);
+  h2d(run.d_scs.p, run.arena.scs.data(), n, st);
+  run.d_active.alloc(n);
+  run.d_perm.alloc(2ull * M + 2);
+  std::vector<int32_t> active(n, 1);
+  std::vector<uint64_t> passes(n, 0);
+  std::vector<fpk::Counters> ctrs(n);
+  // pinned perm staging
+  if (ctx->perm_cap < 2ull * M + 2) {
+    for (auto& p : ctx->h_perm)
+      if (p) cudaFreeHost(p), p = nullptr;
+    for (auto& p : ctx->h_perm) check(cudaMallocHost(&p, sizeof(int32_t) * (2ull * M + 2)), "pinned");
+    ctx->perm_cap = 2ull * M + 2;
+  }
+  check(fpk::launch_init(run.d_scs.p, n, st), "init_kernel");
+  ctx->launches += 1;
+  PermStream rng(cfg->seed);
+  int buf = 0;
+  rng.perm(M, ctx->h_perm[buf]);
+  rng.perm(M, ctx->h_perm[buf] + M);
+  const int threads = n == 1 ? 1024 : 256;
+  int n_active = n;
+  while (n_active > 0) {
+    h2d(run.d_active.p, active.data(), n, st);
+    h2d(run.d_perm.p, ctx->h_perm[buf], 2ull * M, st);
+    check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p, run.d_perm.p + M, M, tabu,
+                           tenure, cfg->debug_check_deltas != 0, maxV, st, threads),
+          "pass_kernel");
+    ctx->launches += M > 0 ? 2 : 1;
+    // next pass's permutations while the device works
+    const int nb = buf ^ 1;
+    rng.perm(M, ctx->h_perm[nb]);
+    rng.perm(M, ctx->h_perm[nb] + M);
+    for (int s = 0; s < n; ++s)
+      if (active[s]) d2h(&ctrs[s], run.arena.scs[s].ctr, 1, st);
+    check(cudaStreamSynchronize(st), "pass sync");
+    buf = nb;
+    for (int s = 0; s < n; ++s) {
+      if (!active[s]) continue;
+      passes[s] += 1;
+      const fpk::Counters& c = ctrs[s];
+      const bool keep = c.error == 0 &&
+                        (c.pass_applied > 0 || (tabu && c.pass_skipped)) &&
+                        !(cfg->max_passes >= 0 && passes[s] >= (uint64_t)cfg->max_passes);
+      if (!keep) {
+        active[s] = 0;
+        --n_active;
+      }
+    }
+  }
+  check(fpk::launch_final(run.d_scs.p, n, st), "final_kernel");
+  ctx->launches += 1;
+  check(cudaEventRecord(ev1, st), "event");
+  for (int s = 0; s < n; ++s) {
+    d2h(&ctrs[s], run.arena.scs[s].ctr, 1, st);
+    d2h(outs[s].vehicle_base, run.arena.scs[s].vbase, insts[s].n_vehicles, st);
+    d2h(outs[s].mission_vehicle, run.arena.scs[s].mv, (size_t)M, st);
+  }
+  check(cudaStreamSynchronize(st), "final sync");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev0, ev1);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  for (int s = 0; s < n; ++s) {
+    const fpk::Counters& c = ctrs[s];
+    if (c.error == FP_ERR_INFEASIBLE)
+      throw FpError(FP_ERR_INFEASIBLE, "infeasible assignment during debug_check_deltas");
+    if (c.error == FP_ERR_LOGIC)
+      throw FpError(FP_ERR_LOGIC, "incremental objective drifted from recomputation");
+    if (c.error) throw FpError((fp_status)c.error, "search failed");
+    fp_search_stats& o = outs[s].stats;
+    o.passes = passes[s];
+    o.evaluations = c.evaluations;
+    o.applied_moves = c.applied;
+    o.committed_moves = c.applied;
+    o.tabu_skips_outer = c.skips_outer;
+    o.tabu_skips_inner = c.skips_inner;
+    o.final_objective_km = c.final_total;
+    outs[s].device_ms = ms;
+    outs[s].exact_fallbacks = c.fallbacks;
+    outs[s].kernel_launches = ctx->launches;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t fp_abi_version(void) { return FP_ABI_VERSION; }
+
+const char* fp_last_error(void) { return g_err.c_str(); }
+
+fp_status fp_ctx_create(int32_t device, fp_ctx** out) {
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+      throw FpError(FP_ERR_CUDA, "no CUDA device available (fleetplace_b200 has no CPU path)");
+    if (device < 0 || device >= n) throw FpError(FP_ERR_INVALID_ARGUMENT, "bad device ordinal");
+    check(cudaSetDevice(device), "cudaSetDevice");
+    auto* c = new fp_ctx();
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete c;
+      throw CudaError(e, "cudaStreamCreate");
+    }
+    *out = c;
+  });
+}
+
+void fp_ctx_destroy(fp_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->d_cost) cudaFree(ctx->d_cost);
+  for (auto& p : ctx->h_perm)
+    if (p) cudaFreeHost(p);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+uint64_t fp_ctx_kernel_launches(const fp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+fp_status fp_validate_instance(const fp_instance* inst) {
+  return guarded([&] { validate(inst); });
+}
+
+fp_status fp_generate_instance(uint64_t pool_seed, const double* bbox, int32_t aerodromes,
+                               int32_t helipads, int32_t health_sites, int32_t missions,
+                               double rotary_only_fraction, uint64_t seed, int32_t rotary,
+                               int32_t fixed_wing, int32_t* base_id, uint8_t* base_kind,
+                               double* base_lat, double* base_lon, int32_t* vehicle_id,
+                               uint8_t* vehicle_kind, int32_t* mission_id, double* pickup_lat,
+                               double* pickup_lon, double* delivery_lat, double* delivery_lon,
+                               uint8_t* rotary_only) {
+  return guarded([&] {
+    fpk_host::generate_instance(pool_seed, bbox, aerodromes, helipads, health_sites, missions,
+                                rotary_only_fraction, seed, rotary, fixed_wing, base_id,
+                                base_kind, base_lat, base_lon, vehicle_id, vehicle_kind,
+                                mission_id, pickup_lat, pickup_lon, delivery_lat, delivery_lon,
+                                rotary_only);
+    fp_instance in{aerodromes + helipads, base_id, base_kind, base_lat, base_lon,
+                   rotary + fixed_wing, vehicle_id, vehicle_kind, missions, mission_id,
+                   pickup_lat, pickup_lon, delivery_lat, delivery_lon, rotary_only};
+    validate(&in);
+  });
+}
+
+fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* in, double radius_km,
+                                  double* out_cost) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const int M = in->n_missions, B = in->n_bases;
+    cudaStream_t st = ctx->stream;
+    table_alloc(ctx, M, B);
+    DBuf<double> pts(6ull * M + 3ull * B);
+    double* plat = pts.p;
+    double* plon = plat + M;
+    double* dlat = plon + M;
+    double* dlon = dlat + M;
+    double* blat = dlon + M;
+    double* blon = blat + B;
+    double* cosv = blon + B;  // [B + 2M]: bases, pickups, deliveries
+    h2d(plat, in->pickup_lat, M, st);
+    h2d(plon, in->pickup_lon, M, st);
+    h2d(dlat, in->delivery_lat, M, st);
+    h2d(dlon, in->delivery_lon, M, st);
+    h2d(blat, in->base_lat, B, st);
+    h2d(blon, in->base_lon, B, st);
+    check(fpk::launch_point_cos(blat, B, cosv, st), "cos(bases)");
+    check(fpk::launch_point_cos(plat, M, cosv + B, st), "cos(pickups)");
+    check(fpk::launch_point_cos(dlat, M, cosv + B + M, st), "cos(deliveries)");
+    check(fpk::launch_table(blat, blon, cosv, B, plat, plon, cosv + B, dlat, dlon, cosv + B + M,
+                            M, radius_km, ctx->d_cost, st),
+          "table_kernel");
+    ctx->launches += 4;
+    if (out_cost) d2h(out_cost, ctx->d_cost, (size_t)M * B, st);
+    check(cudaStreamSynchronize(st), "table sync");
+  });
+}
+
+fp_status fp_table_upload(fp_ctx* ctx, int32_t n_missions, int32_t n_bases,
+                          const double* cost_colmajor) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    table_alloc(ctx, n_missions, n_bases);
+    h2d(ctx->d_cost, cost_colmajor, (size_t)n_missions * n_bases, ctx->stream);
+    check(cudaStreamSynchronize(ctx->stream), "upload sync");
+  });
+}
+
+fp_status fp_table_download(fp_ctx* ctx, double* out_cost) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (ctx->M < 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "no resident table");
+    d2h(out_cost, ctx->d_cost, (size_t)ctx->M * ctx->B, ctx->stream);
+    check(cudaStreamSynchronize(ctx->stream), "download sync");
+  });
+}
+
+fp_status fp_column_totals(fp_ctx* ctx, double* out_totals) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (ctx->M < 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "no resident table");
+    DBuf<double> d(ctx->B);
+    check(fpk::launch_column_totals(ctx->d_cost, ctx->M, ctx->B, d.p, ctx->stream), "totals");
+    ctx->launches += 1;
+    d2h(out_totals, d.p, ctx->B, ctx->stream);
+    check(cudaStreamSynchronize(ctx->stream), "totals sync");
+  });
+}
+
+fp_status fp_rank_bases(fp_ctx* ctx, const fp_instance* in, fp_ranked_start* out) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    validate(in);
+    const int M = in->n_missions, B = in->n_bases, V = in->n_vehicles;
+    ensure_table(ctx, M, B);
+    cudaStream_t st = ctx->stream;
+    // (1) fixed-order column totals on the device
+    DBuf<double> d_tot(B);
+    check(fpk::launch_column_totals(ctx->d_cost, M, B, d_tot.p, st), "totals");
+    ctx->launches += 1;
+    d2h(out->base_totals, d_tot.p, B, st);
+    check(cudaStreamSynchronize(st), "totals sync");
+    const double* tot = out->base_totals;
+    // (2) rank order: total ascending, lower id on ties (rank.cpp:35-43)
+    std::vector<int> order(B);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+      if (tot[a] != tot[b]) return tot[a] < tot[b];
+      return in->base_id[a] < in->base_id[b];
+    });
+    int rotary = 0;
+    for (int v = 0; v < V; ++v) rotary += in->vehicle_kind[v] == FP_ROTARY;
+    // (3) top |fleet| with the helipad cap (rank.cpp:47-59)
+    std::vector<int> chosen;
+    int heli = 0;
+    for (int bi : order) {
+      if ((int)chosen.size() == V) break;
+      const bool h = in->base_kind[bi] == FP_HELIPAD;
+      if (h && heli == rotary) continue;
+      chosen.push_back(bi);
+      if (h) ++heli;
+    }
+    if ((int)chosen.size() < V)
+      throw FpError(FP_ERR_VALIDATION,
+                    "validation failed for bases: not enough compatible bases to place the fleet");
+    // (4) placement: helipads first with rotary ids ascending (rank.cpp:61-90)
+    std::vector<int> rot, fix;
+    for (int v = 0; v < V; ++v) (in->vehicle_kind[v] == FP_ROTARY ? rot : fix).push_back(v);
+    auto by_id = [&](int a, int b) { return in->vehicle_id[a] < in->vehicle_id[b]; };
+    std::sort(rot.begin(), rot.end(), by_id);
+    std::sort(fix.begin(), fix.end(), by_id);
+    std::vector<int> base_vehicle(B, -1);
+    for (int v = 0; v < V; ++v) out->vehicle_base[v] = -1;
+    size_t nr = 0, nf = 0;
+    for (int bi : chosen)
+      if (in->base_kind[bi] == FP_HELIPAD) {
+        const int v = rot[nr++];
+        base_vehicle[bi] = v;
+        out->vehicle_base[v] = bi;
+      }
+    for (int bi : chosen)
+      if (in->base_kind[bi] != FP_HELIPAD) {
+        const int v = nr < rot.size() ? rot[nr++] : fix[nf++];
+        base_vehicle[bi] = v;
+        out->vehicle_base[v] = bi;
+      }
+    // (5) per-mission argmin over occupied compatible bases (device)
+    const int n = (int)chosen.size();
+    std::vector<int32_t> cb(n), cbid(n), cv(n);
+    std::vector<uint8_t> cf(n);
+    for (int k = 0; k < n; ++k) {
+      cb[k] = chosen[k];
+      cbid[k] = in->base_id[chosen[k]];
+      cv[k] = base_vehicle[chosen[k]];
+      cf[k] = in->vehicle_kind[cv[k]] == FP_FIXED;
+    }
+    DBuf<int32_t> d_i32(3ull * n + (size_t)M + 1);
+    DBuf<uint8_t> d_u8((size_t)n + M + 1);
+    int32_t* d_cb = d_i32.p;
+    int32_t* d_cbid = d_cb + n;
+    int32_t* d_cv = d_cbid + n;
+    int32_t* d_mv = d_cv + n;
+    int32_t* d_bad = d_mv + M;
+    uint8_t* d_cf = d_u8.p;
+    uint8_t* d_ro = d_cf + n;
+    h2d(d_cb, cb.data(), n, st);
+    h2d(d_cbid, cbid.data(), n, st);
+    h2d(d_cv, cv.data(), n, st);
+    h2d(d_cf, cf.data(), n, st);
+    h2d(d_ro, in->rotary_only, M, st);
+    const int32_t big = 0x7fffffff;
+    h2d(d_bad, &big, 1, st);
+    check(fpk::launch_mission_argmin(ctx->d_cost, M, d_cb, d_cbid, d_cf, d_cv, n, d_ro, d_mv, d_bad,
+                                     st),
+          "mission_argmin");
+    ctx->launches += 1;
+    int32_t bad = 0;
+    d2h(out->mission_vehicle, d_mv, M, st);
+    d2h(&bad, d_bad, 1, st);
+    check(cudaStreamSynchronize(st), "rank sync");
+    if (bad != big)
+      throw FpError(FP_ERR_NO_COMPATIBLE, "mission " + std::to_string(in->mission_id[bad]) +
+                                              " has no compatible placed vehicle");
+    // (6) unused bases in rank order (rank.cpp:118-121)
+    int nu = 0;
+    for (int bi : order)
+      if (base_vehicle[bi] < 0) out->unused_bases[nu++] = bi;
+    out->n_unused = nu;
+  });
+}
+
+fp_status fp_initial_pool(const fp_instance* in, const int32_t* vehicle_base,
+                          const int32_t* mission_vehicle, const int32_t* unused_bases,
+                          int32_t n_unused, int32_t* out_kind, int32_t* out_index,
+                          int32_t* out_size) {
+  return guarded([&] {
+    int k = 0;
+    for (int u = 0; u < n_unused; ++u) {
+      out_kind[k] = FP_POOL_EMPTY_BASE;
+      out_index[k++] = unused_bases[u];
+    }
+    std::vector<int> served(in->n_vehicles, 0);
+    for (int m = 0; m < in->n_missions; ++m)
+      if (mission_vehicle[m] >= 0 && mission_vehicle[m] < in->n_vehicles) served[mission_vehicle[m]]++;
+    std::vector<int> placed;
+    for (int v = 0; v < in->n_vehicles; ++v)
+      if (vehicle_base[v] >= 0) placed.push_back(v);
+    std::sort(placed.begin(), placed.end(),
+              [&](int a, int b) { return in->vehicle_id[a] < in->vehicle_id[b]; });
+    for (int v : placed)
+      if (!served[v]) {
+        out_kind[k] = FP_POOL_IDLE_VEHICLE;
+        out_index[k++] = v;
+      }
+    *out_size = k;
+  });
+}
+
+fp_status fp_search(fp_ctx* ctx, const fp_instance* inst, const fp_search_config* cfg,
+                    const fp_search_start* start, fp_search_result* out) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ensure_table(ctx, inst->n_missions, inst->n_bases);
+    run_search(ctx, 1, inst, cfg, start, out, {ctx->d_cost}, {nullptr});
+  });
+}
+
+fp_status fp_search_batch(fp_ctx* ctx, int32_t n, const fp_instance* insts,
+                          const double* const* tables, const fp_search_config* cfg,
+                          const fp_search_start* starts, fp_search_result* outs) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (n <= 0) return;
+    std::vector<const double*> dev(n, nullptr), host(n, nullptr);
+    std::vector<DBuf<double>> built;
+    for (int s = 0; s < n; ++s) {
+      if (tables && tables[s]) {
+        host[s] = tables[s];
+      } else {
+        // build this scenario's table on the device, keep it in the arena copy
+        fp_status rc = fp_build_distance_table(ctx, &insts[s], 6371.0088, nullptr);
+        if (rc != FP_OK) throw FpError(rc, g_err);
+        built.emplace_back((size_t)insts[s].n_missions * insts[s].n_bases);
+        check(cudaMemcpyAsync(built.back().p, ctx->d_cost,
+                              sizeof(double) * insts[s].n_missions * insts[s].n_bases,
+                              cudaMemcpyDeviceToDevice, ctx->stream),
+              "D2D");
+        dev[s] = built.back().p;
+      }
+    }
+    run_search(ctx, n, insts, cfg, starts, outs, dev, host);
+  });
+}
+
+fp_status fp_enumerate_moves(fp_ctx* ctx, const fp_instance* in, const fp_search_start* state,
+                             int32_t i, int32_t j, int32_t* out_kind, double* out_delta,
+                             int32_t* out_count) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const int M = in->n_missions, V = in->n_vehicles;
+    ensure_table(ctx, M, in->n_bases);
+    HostScenario h = prepare(in, state);
+    if (j < 0 || j >= M) throw FpError(FP_ERR_ERROR, "unknown mission id");
+    cudaStream_t st = ctx->stream;
+    DBuf<int32_t> d_vb(V + 1), d_mv((size_t)M + 1);
+    DBuf<double> d_out(4);
+    h2d(d_vb.p, h.vbase.data(), V, st);
+    h2d(d_mv.p, h.mv.data(), M, st);
+    int n = 0;
+    auto add = [&](int kind, int newcol, int mover) {
+      check(fpk::launch_candidate_delta(ctx->d_cost, M, d_vb.p, d_mv.p, kind, j, newcol, mover,
+                                        d_out.p + n, st),
+            "candidate_delta");
+      ctx->launches += 1;
+      out_kind[n++] = kind;
+    };
+    const bool in_pool = i >= 0 && i < h.psize;
+    // eval_takeover (search.cpp:82-101)
+    if (in_pool && h.pkind[i] == fpk::POOL_IDLE) {
+      const int g = h.pidx[i];
+      if (!(in->rotary_only[j] && h.vfixed[g])) add(FP_MOVE_TAKEOVER, h.vbase[g], -1);
+    }
+    // eval_relocate (search.cpp:103-129)
+    if (in_pool && h.pkind[i] == fpk::POOL_EMPTY) {
+      const int t = h.pidx[i], mover = h.mv[j];
+      if (!(h.vfixed[mover] && h.bheli[t])) add(FP_MOVE_RELOCATE, t, mover);
+    }
+    // eval_reassign (search.cpp:131-148)
+    if (i >= 0 && i < M) {
+      const int g = h.mv[i], l = h.mv[j];
+      if (g != l && !(in->rotary_only[j] && h.vfixed[g])) add(FP_MOVE_REASSIGN, h.vbase[g], -1);
+    }
+    d2h(out_delta, d_out.p, n, st);
+    check(cudaStreamSynchronize(st), "enumerate sync");
+    *out_count = n;
+  });
+}
+
+fp_status fp_objective_km(fp_ctx* ctx, const int32_t* vehicle_base, const int32_t* mission_vehicle,
+                          double* out_km) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (ctx->M < 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "no resident table");
+    const int M = ctx->M;
+    int V = 0;
+    for (int m = 0; m < M; ++m) V = std::max(V, mission_vehicle[m] + 1);
+    cudaStream_t st = ctx->stream;
+    DBuf<int32_t> d_vb(V + 1), d_mv((size_t)M + 1);
+    DBuf<double> d_out(1);
+    h2d(d_vb.p, vehicle_base, V, st);
+    h2d(d_mv.p, mission_vehicle, M, st);
+    check(fpk::launch_objective(ctx->d_cost, M, d_vb.p, d_mv.p, d_out.p, st), "objective");
+    ctx->launches += 1;
+    d2h(out_km, d_out.p, 1, st);
+    check(cudaStreamSynchronize(st), "objective sync");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// common.cuh — device-side types shared by the fleetplace_b200 kernels.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace fpk {
+
+// Tabu roles (proj/include/fleetplace/search.hpp:78-79).
+enum : uint8_t { ROLE_OUTER = 0, ROLE_INNER = 1 };
+// Pool entry kinds (proj/include/fleetplace/search.hpp:30-32).
+enum : int32_t { POOL_EMPTY = 0, POOL_IDLE = 1 };
+
+// Per-scenario counters and block-uniform scalars of the search automaton.
+// Lives in device memory between pass launches; the pass kernel keeps a copy
+// in shared memory and writes it back on exit.
+struct Counters {
+  long long tick;                 // pairs visited so far (tabu clock)
+  unsigned long long evaluations;
+  unsigned long long applied;
+  unsigned long long skips_outer;
+  unsigned long long skips_inner;
+  unsigned long long fallbacks;   // accept decisions settled by exact chains
+  int psize;                      // current pool size
+  int pass_applied;               // moves applied in the current pass
+  int pass_skipped;               // any tabu skip in the current pass
+  int error;                      // 0 = ok, else an fp_status
+  double total_up;                // rigorous upper bound of the current total
+  double final_total;             // exact fixed-order total (written at the end)
+};
+
+// One search scenario: the resident distance table plus the index-based
+// SearchState of proj/src/search_state.hpp:20-31 in structure-of-arrays
+// form, the perm_b-ordered mirrors the scan streams, and the expiry-stamp
+// tabu table.
+struct Scenario {
+  // read-only instance data
+  const double* cost;        // [B*M] column-major, entry (m, b) at b*M + m
+  const uint8_t* ro;         // [M] mission rotary_only
+  const uint8_t* vfixed;     // [V] vehicle is fixed-wing
+  const uint8_t* bheli;      // [B] base is a helipad
+  const int32_t* vrk;        // [V] slot of {Relocate, vehicle id} key
+  const int32_t* brk;        // [B] slot of {Relocate, base id} key
+  // mutable state (natural mission order)
+  int32_t* mv;               // [M] mission -> vehicle index
+  double* mc;                // [M] cost charged per mission
+  int32_t* vbase;            // [V] vehicle -> base index (-1 unplaced)
+  int32_t* vcount;           // [V] missions per vehicle
+  int32_t* bveh;             // [B] base -> vehicle index or -1
+  int32_t* pkind;            // [pool_cap]
+  int32_t* pidx;             // [pool_cap] base index or vehicle index
+  // perm_b-ordered mirrors, rebuilt per pass
+  int32_t* mvp;              // [M] mv[perm_b[p]]
+  double* mcp;               // [M] mc[perm_b[p]]
+  uint8_t* rop;              // [M] ro[perm_b[p]]
+  int32_t* invb;             // [M] position of mission m in perm_b
+  // tabu: expiry stamps; takeover/reassign keys are only ever Outer
+  long long* exp_take;       // [V] {Takeover, vehicle id}
+  long long* exp_reas;       // [V] {Reassign, vehicle id}
+  long long* exp_rel;        // [K] {Relocate, id}, ids of bases and vehicles
+  uint8_t* role_rel;         // [K]
+  Counters* ctr;
+  int32_t M, B, V, K, pool_cap;
+  int32_t active;            // host-managed: scenario still searching
+};
+
+}  // namespace fpk
+
+#define FP_CUDA_CHECK(expr)                                                \
+  do {                                                                     \
+    cudaError_t err__ = (expr);                                            \
+    if (err__ != cudaSuccess) throw ::fpk_host::CudaError(err__, #expr);   \
+  } while (0)

@@ -1,0 +1,50 @@
+// host_common.hpp — host-side error plumbing and kernel launcher prototypes.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "fleetplace_b200.h"
+
+namespace fpk {
+struct Scenario;
+
+cudaError_t launch_point_cos(const double* lat, int n, double* out, cudaStream_t st);
+cudaError_t launch_table(const double* blat, const double* blon, const double* bcos, int B,
+                         const double* plat, const double* plon, const double* pcos,
+                         const double* dlat, const double* dlon, const double* dcos, int M,
+                         double radius_km, double* cost, cudaStream_t st);
+cudaError_t launch_column_totals(const double* cost, int M, int B, double* out, cudaStream_t st);
+cudaError_t launch_mission_argmin(const double* cost, int M, const int32_t* cb, const int32_t* cbid,
+                                  const uint8_t* cf, const int32_t* cv, int n, const uint8_t* ro,
+                                  int32_t* mv, int32_t* first_bad, cudaStream_t st);
+cudaError_t launch_objective(const double* cost, int M, const int32_t* vb, const int32_t* mv,
+                             double* out, cudaStream_t st);
+cudaError_t launch_candidate_delta(const double* cost, int M, const int32_t* vb, const int32_t* mv,
+                                   int kind, int j, int newcol, int mover, double* out,
+                                   cudaStream_t st);
+cudaError_t launch_init(Scenario* d_scs, int n_scn, cudaStream_t stream);
+cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream);
+cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn, const int32_t* d_pa,
+                        const int32_t* d_pb, int M, bool tabu, long long tenure, bool debug, int V,
+                        cudaStream_t stream, int threads);
+}  // namespace fpk
+
+namespace fpk_host {
+
+// An fp_status carried through C++ code up to the C boundary.
+struct FpError : std::runtime_error {
+  FpError(fp_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+  fp_status code;
+};
+
+struct CudaError : FpError {
+  CudaError(cudaError_t e, const char* what)
+      : FpError(e == cudaErrorMemoryAllocation ? FP_ERR_OUT_OF_MEMORY : FP_ERR_CUDA,
+                std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what) {}
+};
+
+}  // namespace fpk_host

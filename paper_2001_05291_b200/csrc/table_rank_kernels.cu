@@ -1,0 +1,213 @@
+// table_rank_kernels.cu — kernel (1) distance table and kernel (2) ranking.
+//
+// Kernel (1) restates haversine_km / mission_cost_km (proj/src/geo.cpp:18-36)
+// operation for operation. The reference is built for baseline x86-64, so
+// none of its multiply-adds are fused; every product/sum here is an explicit
+// __dmul_rn/__dadd_rn so nvcc cannot contract them into FMAs. cos(phi) of
+// every point is hoisted (bit-identical: same argument, same function).
+// The transcendentals are CUDA's fp64 sin/asin; see DESIGN.md for the
+// measured per-entry ULP agreement with glibc.
+//
+// Kernel (2) computes the fixed-order column totals (proj/src/rank.cpp:10-23):
+// each column is ONE sequential fp64 chain in row order, bit-identical to the
+// reference by construction. Warps load 32x32 tiles coalesced and transpose
+// through shared memory so each lane owns one column's chain.
+
+#include <cfloat>
+#include <climits>
+
+#include "common.cuh"
+
+namespace fpk {
+
+namespace {
+constexpr double kDegToRad = 3.14159265358979323846 / 180.0;
+}
+
+__global__ void point_cos_kernel(const double* __restrict__ lat, int n, double* __restrict__ out) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+    out[k] = cos(__dmul_rn(lat[k], kDegToRad));
+}
+
+__device__ __forceinline__ double hav(double lat_a, double lon_a, double cos_a, double lat_b,
+                                      double lon_b, double cos_b, double two_r) {
+  const double half_dphi = __dmul_rn(__dmul_rn(0.5, fabs(__dsub_rn(lat_b, lat_a))), kDegToRad);
+  const double half_dpsi = __dmul_rn(__dmul_rn(0.5, fabs(__dsub_rn(lon_b, lon_a))), kDegToRad);
+  const double s_lat = sin(half_dphi);
+  const double s_lon = sin(half_dpsi);
+  const double h = __dadd_rn(__dmul_rn(s_lat, s_lat),
+                             __dmul_rn(__dmul_rn(__dmul_rn(cos_a, cos_b), s_lon), s_lon));
+  const double r = __dsqrt_rn(h);
+  return __dmul_rn(two_r, asin(fmin(1.0, r)));
+}
+
+// cost[b*M + m] for a tile of bases; threads run along missions so every
+// warp store is 256 contiguous bytes of one column.
+__global__ void __launch_bounds__(256)
+    table_kernel(const double* __restrict__ blat, const double* __restrict__ blon,
+                 const double* __restrict__ bcos, int B, const double* __restrict__ plat,
+                 const double* __restrict__ plon, const double* __restrict__ pcos,
+                 const double* __restrict__ dlat, const double* __restrict__ dlon,
+                 const double* __restrict__ dcos, int M, double two_r, int bases_per_block,
+                 double* __restrict__ cost) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const double pl = plat[m], po = plon[m], pc = pcos[m];
+  const double dl = dlat[m], d_o = dlon[m], dc = dcos[m];
+  const int b0 = blockIdx.y * bases_per_block;
+  const int b1 = min(B, b0 + bases_per_block);
+  for (int b = b0; b < b1; ++b) {
+    const double la = blat[b], lo = blon[b], ca = bcos[b];
+    const double c = __dadd_rn(hav(la, lo, ca, pl, po, pc, two_r), hav(la, lo, ca, dl, d_o, dc, two_r));
+    cost[(long long)b * M + m] = c;
+  }
+}
+
+// Column totals: warp w owns columns [32w, 32w+32). Per 32-row tile, lane l
+// loads row (r0+l) of each of the 32 columns (coalesced within a column),
+// the tile is transposed in shared memory, and lane l adds its column's 32
+// values in row order to its running sum.
+__global__ void __launch_bounds__(128)
+    column_totals_kernel(const double* __restrict__ cost, int M, int B, double* __restrict__ out) {
+  __shared__ double tile[4][32][33];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int c0 = (blockIdx.x * 4 + w) * 32;
+  if (c0 >= B) return;
+  double (*t)[33] = tile[w];
+  double sum = 0.0;
+  for (int r0 = 0; r0 < M; r0 += 32) {
+    const int r = r0 + l;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const int c = c0 + k;
+      t[k][l] = (r < M && c < B) ? cost[(long long)c * M + r] : 0.0;
+    }
+    __syncwarp();
+    const int n = min(32, M - r0);
+    for (int k = 0; k < n; ++k) sum = __dadd_rn(sum, t[l][k]);
+    __syncwarp();
+  }
+  if (c0 + l < B) out[c0 + l] = sum;
+}
+
+// Per-mission argmin over the chosen (occupied) bases whose vehicle may fly
+// the mission; ties fall to the lower base id (proj/src/rank.cpp:92-116).
+// chosen_* are in ranking order; the result does not depend on the order
+// because (cost, base id) is a strict total order.
+__global__ void mission_argmin_kernel(const double* __restrict__ cost, int M,
+                                      const int32_t* __restrict__ chosen_base,
+                                      const int32_t* __restrict__ chosen_bid,
+                                      const uint8_t* __restrict__ chosen_fixed,
+                                      const int32_t* __restrict__ chosen_vehicle, int n_chosen,
+                                      const uint8_t* __restrict__ ro,
+                                      int32_t* __restrict__ mission_vehicle,
+                                      int32_t* __restrict__ first_bad) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const bool rot = ro[m];
+  int best = -1, best_id = 0;
+  double best_c = 0.0;
+  for (int k = 0; k < n_chosen; ++k) {
+    if (rot && chosen_fixed[k]) continue;
+    const double c = cost[(long long)chosen_base[k] * M + m];
+    const int id = chosen_bid[k];
+    if (best < 0 || c < best_c || (c == best_c && id < best_id)) {
+      best = k;
+      best_c = c;
+      best_id = id;
+    }
+  }
+  if (best < 0) {
+    atomicMin(first_bad, m);
+    mission_vehicle[m] = -1;
+  } else {
+    mission_vehicle[m] = chosen_vehicle[best];
+  }
+}
+
+// objective_km's sum (proj/src/model.cpp:186-191): one fixed-order chain.
+__global__ void objective_kernel(const double* __restrict__ cost, int M,
+                                 const int32_t* __restrict__ vehicle_base,
+                                 const int32_t* __restrict__ mission_vehicle, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  for (int m = 0; m < M; ++m)
+    s = __dadd_rn(s, cost[(long long)vehicle_base[mission_vehicle[m]] * M + m]);
+  *out = s;
+}
+
+// enumerate_moves' exact delta: candidate_total - total with both sums in
+// fixed mission order (proj/src/search.cpp:150-167, 379-397). `kind` is the
+// move, `j` the mission index, `newcol` the column charged (gain's base for
+// takeover/reassign, target for relocation), `mover` the relocated vehicle.
+__global__ void candidate_delta_kernel(const double* __restrict__ cost, int M,
+                                       const int32_t* __restrict__ vehicle_base,
+                                       const int32_t* __restrict__ mission_vehicle, int kind,
+                                       int j, int newcol, int mover, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (int m = 0; m < M; ++m) {
+    const double c = cost[(long long)vehicle_base[mission_vehicle[m]] * M + m];
+    a = __dadd_rn(a, c);
+    double nc = c;
+    if (kind == 1) {
+      if (mission_vehicle[m] == mover) nc = cost[(long long)newcol * M + m];
+    } else if (m == j) {
+      nc = cost[(long long)newcol * M + m];
+    }
+    b = __dadd_rn(b, nc);
+  }
+  *out = __dsub_rn(b, a);
+}
+
+// ---- launchers ------------------------------------------------------------
+
+cudaError_t launch_point_cos(const double* lat, int n, double* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int blocks = min(1184, (n + 255) / 256);
+  point_cos_kernel<<<blocks, 256, 0, st>>>(lat, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_table(const double* blat, const double* blon, const double* bcos, int B,
+                         const double* plat, const double* plon, const double* pcos,
+                         const double* dlat, const double* dlon, const double* dcos, int M,
+                         double radius_km, double* cost, cudaStream_t st) {
+  if (B <= 0 || M <= 0) return cudaSuccess;
+  const int bpb = 8;
+  dim3 grid((M + 255) / 256, (B + bpb - 1) / bpb);
+  table_kernel<<<grid, 256, 0, st>>>(blat, blon, bcos, B, plat, plon, pcos, dlat, dlon, dcos, M,
+                                     2.0 * radius_km, bpb, cost);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_column_totals(const double* cost, int M, int B, double* out, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
+  const int blocks = (B + 127) / 128;
+  column_totals_kernel<<<blocks, 128, 0, st>>>(cost, M, B, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mission_argmin(const double* cost, int M, const int32_t* cb, const int32_t* cbid,
+                                  const uint8_t* cf, const int32_t* cv, int n, const uint8_t* ro,
+                                  int32_t* mv, int32_t* first_bad, cudaStream_t st) {
+  if (M <= 0) return cudaSuccess;
+  mission_argmin_kernel<<<(M + 255) / 256, 256, 0, st>>>(cost, M, cb, cbid, cf, cv, n, ro, mv,
+                                                         first_bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_objective(const double* cost, int M, const int32_t* vb, const int32_t* mv,
+                             double* out, cudaStream_t st) {
+  objective_kernel<<<1, 32, 0, st>>>(cost, M, vb, mv, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_candidate_delta(const double* cost, int M, const int32_t* vb, const int32_t* mv,
+                                   int kind, int j, int newcol, int mover, double* out,
+                                   cudaStream_t st) {
+  candidate_delta_kernel<<<1, 32, 0, st>>>(cost, M, vb, mv, kind, j, newcol, mover, out);
+  return cudaGetLastError();
+}
+
+}  // namespace fpk

@@ -122,6 +122,9 @@ typedef struct fp_search_result {
   double device_ms;              /* CUDA-event time of the device search */
   uint64_t kernel_launches;      /* kernels this call launched */
   uint64_t exact_fallbacks;      /* accept decisions settled by exact chains */
+  uint64_t phase_cycles[6];      /* SM cycles per automaton phase (scenario 0):
+                                    row skip, row context, chunk scan, event
+                                    pairs, exact fallbacks, relocation prepass */
 } fp_search_result;
 
 /* RankedStart (proj/include/fleetplace/rank.hpp:10-14) in index form. */

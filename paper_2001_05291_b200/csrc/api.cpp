@@ -506,6 +506,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     o.final_objective_km = c.final_total;
     outs[s].device_ms = ms;
     outs[s].exact_fallbacks = c.fallbacks;
+    for (int k = 0; k < 6; ++k) outs[s].phase_cycles[k] = c.cycles[k];
     outs[s].kernel_launches = ctx->launches;
   }
 }

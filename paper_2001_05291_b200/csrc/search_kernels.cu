@@ -56,6 +56,13 @@ struct Shared {
   double red_d[3][33];
 };
 
+// Phase timing (thread 0's SM clock), accumulated into Counters::cycles.
+__device__ __forceinline__ long long ph_now() { return threadIdx.x == 0 ? clock64() : 0; }
+#define PH_ADD(sh, k, t0) \
+  do {                    \
+    if (threadIdx.x == 0) (sh).c.cycles[k] += clock64() - (t0); \
+  } while (0)
+
 __device__ __forceinline__ double cost_at(const Scenario& s, int col, int m) {
   return s.cost[(long long)col * s.M + m];
 }
@@ -211,7 +218,9 @@ __device__ void reloc_sums(const Scenario& s, int t, double* sumD, double* absD,
 // AMB  sign of the sequential quick_delta not settled
 __device__ __forceinline__ uint8_t reloc_class(double sum, double abs, int n,
                                                double bound_total) {
-  if (n == 0) return CLS_POS;
+  // all terms exactly zero (e.g. a base at the same location): the
+  // sequential sum is exactly 0.0, never < 0
+  if (n == 0 || abs == 0.0) return CLS_POS;
   const double err = (double)(n + 1) * kTwoPowM52 * abs * 1.0001;
   if (sum > err) return CLS_POS;
   if (sum < -(err + bound_total)) return CLS_ACC;
@@ -329,8 +338,10 @@ __device__ void process_pair(const Scenario& s, Shared& sh, int i, int j, bool t
         if (newc - mcj < 0.0) {
           bool acc = mcj - newc > single_bound(s, sh);
           if (!acc) {
+            const long long f0 = ph_now();
             sh.c.fallbacks += 1;
             acc = exact_single_accept(s, j, newc);
+            PH_ADD(sh, 4, f0);
           }
           if (acc) {
             apply_takeover(s, sh, j, g, i);
@@ -373,9 +384,11 @@ __device__ void process_pair(const Scenario& s, Shared& sh, int i, int j, bool t
       const uint8_t cls = reloc_class(a, b, (int)c, bt);
       bool acc = cls == CLS_ACC;
       if (cls == CLS_NEG || cls == CLS_AMB) {
+        const long long f0 = ph_now();
         sh.c.fallbacks += 1;
         const bool neg = cls == CLS_NEG || exact_reloc_quick(s, t, mover) < 0.0;
         acc = neg && exact_reloc_accept(s, t, mover);
+        PH_ADD(sh, 4, f0);
       }
       sh.bi[2] = acc;
     }
@@ -408,8 +421,10 @@ __device__ void process_pair(const Scenario& s, Shared& sh, int i, int j, bool t
       if (newc - mcj < 0.0) {
         bool acc = mcj - newc > single_bound(s, sh);
         if (!acc) {
+          const long long f0 = ph_now();
           sh.c.fallbacks += 1;
           acc = exact_single_accept(s, j, newc);
+          PH_ADD(sh, 4, f0);
         }
         if (acc) {
           apply_reassign(s, sh, j, g);
@@ -485,10 +500,12 @@ __device__ void make_context(const Scenario& s, Shared& sh, int i, bool tabu, in
   }
   const int t = sh.rel_t;
   if (t >= 0) {
+    const long long r0 = ph_now();
     reloc_sums<NT>(s, t, sumD, absD, cnt);
     const double bt = single_bound(s, sh);
     for (int v = threadIdx.x; v < s.V; v += NT)
       cls[v] = (s.vfixed[v] && sh.heli_t) ? CLS_POS : reloc_class(sumD[v], absD[v], cnt[v], bt);
+    PH_ADD(sh, 5, r0);
   }
   __syncthreads();
 }
@@ -501,7 +518,10 @@ __device__ void run_row(const Scenario& s, Shared& sh, int i, const int32_t* __r
   const int M = s.M;
   int p = 0;
   while (p < M) {
+    const long long c0 = ph_now();
     make_context<NT>(s, sh, i, tabu, lim_j, outer_j, cls, sumD, absD, cnt);
+    PH_ADD(sh, 1, c0);
+    const long long c1 = ph_now();
     const int p_seg = p;
     const int gain_r = sh.gain_r, col_r = sh.col_r, fixed_r = sh.fixed_r;
     const int gain_t = sh.gain_t, col_t = sh.col_t, fixed_t = sh.fixed_t;
@@ -565,6 +585,7 @@ __device__ void run_row(const Scenario& s, Shared& sh, int i, const int32_t* __r
       p = stop;
       if (ev != INT_MAX) break;
     }
+    PH_ADD(sh, 2, c1);
     if (ev == INT_MAX) return;  // row exhausted perm_b
     // event at position p
     bool outer_ev = false;
@@ -582,7 +603,10 @@ __device__ void run_row(const Scenario& s, Shared& sh, int i, const int32_t* __r
       __syncthreads();
       return;
     }
+    const long long c2 = ph_now();
     process_pair<NT>(s, sh, i, pb[p], tabu, tenure, debug, sumD, absD, cnt);
+    PH_ADD(sh, 3, c2);
+    __syncthreads();
     if (sh.c.error) return;
     p += 1;
   }
@@ -629,6 +653,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 4)
   const int M = s.M;
   int r = 0;
   while (r < M && !sh.c.error) {
+    const long long b0 = ph_now();
     if (tabu) {
       // rows r .. r+NT-1: outer-blocked at p = 0 if every earlier one was?
       const int d = threadIdx.x, row = r + d;
@@ -659,6 +684,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 4)
       }
       __syncthreads();
       r += nskip;
+      PH_ADD(sh, 0, b0);
       if (found == INT_MAX) continue;
     }
     run_row<NT>(s, sh, pa[r], pb, tabu, tenure, debug, lim_j, outer_j, cls, sumD, absD, cnt);

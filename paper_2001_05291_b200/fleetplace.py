@@ -440,6 +440,7 @@ class SearchStats:
     # B200 extras (not in the reference): device time and exact fallbacks
     device_ms: float = 0.0
     exact_fallbacks: int = 0
+    phase_cycles: tuple = ()
 
 
 @dataclass
@@ -505,7 +506,7 @@ def _stats(r: A.fp_search_result) -> SearchStats:
     s = r.stats
     return SearchStats(int(s.passes), int(s.evaluations), int(s.applied_moves), int(s.committed_moves),
                        int(s.tabu_skips_outer), int(s.tabu_skips_inner), float(s.final_objective_km),
-                       float(r.device_ms), int(r.exact_fallbacks))
+                       float(r.device_ms), int(r.exact_fallbacks), tuple(int(x) for x in r.phase_cycles))
 
 
 def search_arrays(inst: Instance, t: DistanceTable, cfg: SearchConfig, vehicle_base: np.ndarray,
@@ -713,3 +714,43 @@ def small_generated(seed: int, missions: int = 10, aerodromes: int = 12, helipad
     """helpers::small_generated (proj/tests/test_helpers.hpp:42-50)."""
     return generate_instance(seed, aerodromes, helipads, 30, missions, 0.3, seed, rotary, fixed,
                              bbox=(43.0, 49.0, -82.0, -74.0))
+
+
+# ------------------------------------------------------------------ batch ----
+def search_batch(insts: Sequence[Instance], starts: Sequence[tuple], cfg: SearchConfig,
+                 tables: Optional[Sequence[Optional[np.ndarray]]] = None,
+                 device: int = 0) -> list:
+    """Independent scenarios of one mission count searched concurrently, one
+    thread block per scenario (C ABI fp_search_batch). `starts[s]` is the
+    index-form start (vehicle_base, mission_vehicle, pool_kind, pool_index);
+    `tables[s]` a flat column-major host table or None to build it on the
+    device. Returns one SearchResult per scenario."""
+    n = len(insts)
+    ctx = _Ctx(device)
+    ci = (A.fp_instance * n)(*[x.c() for x in insts])
+    keep = []
+    tp = (C.POINTER(C.c_double) * n)()
+    for s in range(n):
+        t = None if tables is None else tables[s]
+        if t is not None:
+            t = np.ascontiguousarray(t, np.float64).reshape(-1)
+            keep.append(t)
+            tp[s] = A.ptr(t, C.c_double)
+        else:
+            tp[s] = C.cast(None, C.POINTER(C.c_double))
+    st = (A.fp_search_start * n)()
+    res = (A.fp_search_result * n)()
+    outs = []
+    for s in range(n):
+        vb, mv, pk, px = (np.ascontiguousarray(a, np.int32) for a in starts[s])
+        keep += [vb, mv, pk, px]
+        st[s] = A.fp_search_start(A.ptr(vb, C.c_int32), A.ptr(mv, C.c_int32), len(pk),
+                                  A.ptr(pk, C.c_int32), A.ptr(px, C.c_int32))
+        ovb = np.empty(insts[s].n_vehicles, np.int32)
+        omv = np.empty(insts[s].n_missions, np.int32)
+        outs.append((ovb, omv))
+        res[s].vehicle_base, res[s].mission_vehicle = A.ptr(ovb, C.c_int32), A.ptr(omv, C.c_int32)
+    c = _cfg_c(cfg)
+    _check(lib().fp_search_batch(ctx.p, n, ci, tp, C.byref(c), st, res))
+    return [SearchResult(outs[s][0], outs[s][1], _stats(res[s]), int(res[s].kernel_launches))
+            for s in range(n)]

@@ -1,0 +1,184 @@
+"""GPU: kernel (1) table, kernel (2) ranking, objective, enumerate_moves and
+the scenario batch, each against the compiled reference."""
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_harness as H
+from paper_2001_05291_b200 import fleetplace as F
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def _ulps(a, b):
+    ai = a.view(np.int64)
+    bi = b.view(np.int64)
+    return np.abs(ai - bi)
+
+
+@pytest.mark.parametrize("shape", [(50, 200, 10), (200, 5000, 20), (500, 10000, 40)])
+def test_table_matches_reference_within_2ulp(shape):
+    """Kernel (1) vs glibc: same operation order, no FMA contraction; the only
+    difference is CUDA's vs glibc's sin/asin (each <= 1-2 ulp). Tolerance: 2
+    ulp per entry, and the vast majority bit-identical (reported)."""
+    inst = F.survey_instance(*shape, seed=1)
+    t = F.build_distance_table(inst)
+    got = np.ascontiguousarray(t.cost.T).reshape(-1)
+    ref = H.ref_table(inst)
+    u = _ulps(got, ref)
+    assert u.max() <= 2, int(u.max())
+    assert (u == 0).mean() > 0.95, float((u == 0).mean())
+
+
+def test_table_geo_known_answers():
+    """proj/tests/test_geo.cpp:15-55 through the table kernel: identical
+    points -> 0, analytic antipode/quarter circle to 1e-6, fixed pair to 1e-12."""
+    kat = json.loads((GOLD / "kats.json").read_text())
+    inst = F.Instance(
+        bases=[(0, 0, (0.0, 0.0)), (1, 0, (45.0, -75.0)), (2, 0, (43.7, -79.4))],
+        fleet=[(0, 0)],
+        missions=[(0, (0.0, 180.0), (0.0, 0.0), False), (1, (90.0, 0.0), (0.0, 0.0), False),
+                  (2, (50.0, -85.0), (45.0, -75.0), False), (3, (43.7, -79.4), (43.7, -79.4), False)])
+    c = F.build_distance_table(inst).cost
+    assert abs(c[0, 0] - kat["test_geo_antipodal_literal"]) <= 1e-6 * c[0, 0]
+    assert abs(c[1, 0] - kat["test_geo_quarter_literal"]) <= 1e-6 * c[1, 0]
+    assert abs(c[2, 1] - kat["test_geo_fixed_pair_literal"]) <= 1e-12 * c[2, 1]
+    assert c[3, 2] == 0.0
+    assert (c >= 0).all()
+
+
+@pytest.mark.parametrize("shape", [(50, 200, 10), (500, 10000, 40), (2000, 20000, 100)])
+def test_column_totals_bit_exact(shape):
+    inst = F.survey_instance(*shape, seed=1)
+    cost = H.ref_table(inst)
+    t = F.DistanceTable.from_host(cost.reshape(inst.n_bases, inst.n_missions).T)
+    got = F.column_totals(t)
+    ref = np.empty(inst.n_bases)
+    H.REF.ref_column_totals(inst.n_missions, inst.n_bases, H.P(cost, H.C.c_double), 0,
+                            H.P(ref, H.C.c_double))
+    assert np.array_equal(got, ref)
+    assert np.array_equal(F.parallel_rank_totals(t, F.ParallelConfig(4)), ref)
+
+
+@pytest.mark.parametrize("name,shape", [("c1", (50, 200, 10)), ("c5", (200, 5000, 20)),
+                                        ("c2", (500, 10000, 40))])
+def test_rank_bases_matches_reference(name, shape):
+    inst = F.survey_instance(*shape, seed=1)
+    cost = H.ref_table(inst)
+    t = F.DistanceTable.from_host(cost.reshape(inst.n_bases, inst.n_missions).T)
+    start = F.rank_bases(inst, t)
+    r = H.ref_rank(inst, cost)
+    assert np.array_equal(start.base_totals, r.totals)
+    assert np.array_equal(start.vehicle_base, r.vehicle_base)
+    assert np.array_equal(start.mission_vehicle, r.mission_vehicle)
+    assert np.array_equal(start.unused_index, r.unused)
+    # end to end on the GPU-built table: same ranking (reported)
+    t2 = F.build_distance_table(inst)
+    s2 = F.rank_bases(inst, t2)
+    assert np.array_equal(s2.vehicle_base, r.vehicle_base)
+
+
+def test_rank_errors():
+    inst = F.Instance(bases=[(0, 0, (45.0, -75.0)), (1, 0, (46.0, -76.0))], fleet=[(0, 1)],
+                      missions=[(0, (45.1, -75.1), (44.9, -74.9), True)])
+    t = F.build_distance_table(inst)
+    with pytest.raises(F.NoCompatibleVehicleError):
+        F.rank_bases(inst, t)
+    # fewer bases than vehicles: "not enough compatible bases" (rank.cpp:57-59)
+    inst = F.Instance(bases=[(0, 1, (45.0, -75.0)), (1, 0, (46.0, -76.0))],
+                      fleet=[(0, 0), (1, 0), (2, 0)],
+                      missions=[(0, (45.1, -75.1), (44.9, -74.9), False)])
+    with pytest.raises(F.ValidationError, match="not enough compatible bases"):
+        F.rank_bases(inst, F.build_distance_table(inst))
+
+
+def test_objective_and_enumerate_moves_match_reference():
+    inst = F.small_generated(16000, 15, 12, 8)
+    cost = H.ref_table(inst)
+    t = F.DistanceTable.from_host(cost.reshape(inst.n_bases, inst.n_missions).T)
+    start = F.rank_bases(inst, t)
+    ref_obj = H.C.c_double(0)
+    H.REF.ref_objective_km(H.C.byref(inst.c()), H.P(cost, H.C.c_double),
+                           H.P(start.vehicle_base, H.C.c_int32),
+                           H.P(start.mission_vehicle, H.C.c_int32), H.C.byref(ref_obj))
+    assert F.objective_km(start.assignment, inst, t) == ref_obj.value
+    pool = F.initial_pool(start, inst)
+    vb, mv, pk, px = F._state_arrays(start.assignment, pool, inst)
+    st = H._start(vb, mv, pk, px)
+    for i in range(inst.n_missions):
+        for j in range(inst.n_missions):
+            got = F.enumerate_moves(start.assignment, pool, i, int(inst.mission_id[j]), inst, t)
+            k = np.empty(3, np.int32)
+            d = np.empty(3)
+            n = H.C.c_int32(0)
+            H.REF.ref_enumerate_moves(H.C.byref(inst.c()), H.P(cost, H.C.c_double), H.C.byref(st),
+                                      i, j, H.P(k, H.C.c_int32), H.P(d, H.C.c_double), H.C.byref(n))
+            assert [(int(m.kind), m.delta_km) for m in got] == \
+                [(int(k[q]), float(d[q])) for q in range(n.value)]
+
+
+def test_batch_equals_individual_searches():
+    """fp_search_batch: scenario s of the batch == the single search of s."""
+    insts, starts, tables = [], [], []
+    for k in range(6):
+        inst = F.survey_instance(60, 600, 8, seed=1 + k)
+        cost = H.ref_table(inst)
+        r = H.ref_rank(inst, cost)
+        pk, px = H.initial_pool_idx(inst, r.vehicle_base, r.mission_vehicle, r.unused)
+        insts.append(inst)
+        starts.append((r.vehicle_base, r.mission_vehicle, pk, px))
+        tables.append(cost)
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu)
+    batch = F.search_batch(insts, starts, cfg, tables)
+    for k in range(6):
+        ref = H.ref_search(insts[k], tables[k], 1, 7, *starts[k])
+        got = batch[k]
+        gs = tuple(getattr(got.stats, f) for f in H.A.STATS_FIELDS)
+        assert gs == ref.stats, k
+        assert np.array_equal(got.mission_vehicle, ref.mission_vehicle)
+        assert np.array_equal(got.vehicle_base, ref.vehicle_base)
+
+
+def test_golden_c1_on_device():
+    g = np.load(GOLD / "c1.npz")
+    inst = F.survey_instance(50, 200, 10, seed=1)
+    t = F.DistanceTable.from_host(g["cost"].reshape(inst.n_bases, inst.n_missions).T)
+    start = F.rank_bases(inst, t)
+    assert np.array_equal(start.base_totals, g["totals"])
+    assert np.array_equal(start.mission_vehicle, g["rank_mv"])
+    pool = F.initial_pool(start, inst)
+    vb, mv, pk, px = F._state_arrays(start.assignment, pool, inst)
+    for mode, seed in [(1, 1), (1, 2), (1, 3), (1, 7), (0, 1), (0, 7)]:
+        key = f"m{mode}_s{seed}_t0"
+        r = F.search_arrays(inst, t, F.SearchConfig(seed=seed, mode=F.SearchMode(mode)),
+                            vb, mv, pk, px)
+        s = r.stats
+        assert [s.passes, s.evaluations, s.applied_moves, s.committed_moves, s.tabu_skips_outer,
+                s.tabu_skips_inner] == g[key + "_stats"].tolist()
+        assert s.final_objective_km == g[key + "_obj"][0]
+        assert np.array_equal(r.mission_vehicle, g[key + "_mv"])
+
+
+def test_golden_shapes_on_device():
+    kat = json.loads((GOLD / "kats.json").read_text())
+    for name, sh in kat["shapes"].items():
+        inst = F.survey_instance(sh["bases"], sh["missions"], sh["vehicles"], seed=1)
+        cost = H.ref_table(inst)
+        assert hashlib.sha256(cost.tobytes()).hexdigest() == sh["table_sha256"]
+        t = F.DistanceTable.from_host(cost.reshape(inst.n_bases, inst.n_missions).T)
+        start = F.rank_bases(inst, t)
+        assert hashlib.sha256(start.base_totals.tobytes()).hexdigest() == sh["totals_sha256"]
+        pool = F.initial_pool(start, inst)
+        vb, mv, pk, px = F._state_arrays(start.assignment, pool, inst)
+        r = F.search_arrays(inst, t, F.SearchConfig(seed=sh["seed"], mode=F.SearchMode.Tabu,
+                                                    max_passes=sh["max_passes"]), vb, mv, pk, px)
+        s = r.stats
+        assert [s.passes, s.evaluations, s.applied_moves, s.committed_moves, s.tabu_skips_outer,
+                s.tabu_skips_inner] == sh["stats"], name
+        assert s.final_objective_km == sh["final_objective_km"]
+        assert hashlib.sha256(r.vehicle_base.tobytes() + r.mission_vehicle.tobytes()).hexdigest() \
+            == sh["assignment_sha256"]

@@ -1,0 +1,80 @@
+"""GPU parity: the B200 path against the compiled reference (oracle/_ref).
+
+Every comparison is bit-exact: same Assignment (index form), all seven
+SearchStats fields equal (final objective bit-equal), same ranking. The
+search runs on the reference's own distance table (uploaded), so the move
+sequence is compared independently of kernel (1)'s transcendental ULPs;
+kernel (1) is checked separately.
+"""
+import numpy as np
+import pytest
+
+from oracle_harness import (initial_pool_idx, orc_search, ref_rank, ref_search,
+                            ref_small_generated, ref_survey_instance, ref_table, ref_generate)
+from paper_2001_05291_b200 import fleetplace as F
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_search(inst, cost, mode, seed, vb, mv, pk, px, tenure=0, max_passes=None):
+    t = F.DistanceTable.from_host(cost.reshape(inst.n_bases, inst.n_missions).T)
+    cfg = F.SearchConfig(seed=seed, mode=F.SearchMode(mode), tabu_tenure=tenure, max_passes=max_passes)
+    return F.search_arrays(inst, t, cfg, vb, mv, pk, px)
+
+
+def _check_search(inst, mode, seeds, tenure=0, max_passes=None):
+    cost = ref_table(inst)
+    r = ref_rank(inst, cost)
+    pk, px = initial_pool_idx(inst, r.vehicle_base, r.mission_vehicle, r.unused)
+    for seed in seeds:
+        ref = ref_search(inst, cost, mode, seed, r.vehicle_base, r.mission_vehicle, pk, px,
+                         tenure=tenure, max_passes=max_passes)
+        got = _gpu_search(inst, cost, mode, seed, r.vehicle_base, r.mission_vehicle, pk, px,
+                          tenure=tenure, max_passes=max_passes)
+        gs = tuple(getattr(got.stats, f) for f in
+                   ("passes", "evaluations", "applied_moves", "committed_moves",
+                    "tabu_skips_outer", "tabu_skips_inner", "final_objective_km"))
+        assert gs == ref.stats, (seed, gs, ref.stats)
+        assert np.array_equal(got.vehicle_base, ref.vehicle_base), seed
+        assert np.array_equal(got.mission_vehicle, ref.mission_vehicle), seed
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_c1_all_seeds(mode):
+    inst = ref_survey_instance(50, 200, 10)
+    _check_search(inst, mode, seeds=[0, 1, 2, 3, 7, 11])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_small_generated_tabu(seed):
+    inst = ref_small_generated(16000 + seed, 15, 12, 8)
+    _check_search(inst, 1, seeds=[seed])
+    _check_search(inst, 0, seeds=[seed])
+
+
+@pytest.mark.parametrize("tenure", [1, 2, 5, 17, 100])
+def test_tenures(tenure):
+    inst = ref_small_generated(14500, 40, 12, 8, 4, 2)
+    _check_search(inst, 1, seeds=[0, 1], tenure=tenure)
+
+
+def test_trap_instance():
+    inst = ref_small_generated(17010, 6, 5, 3, 2, 1)
+    _check_search(inst, 1, seeds=[6])
+    _check_search(inst, 0, seeds=[6])
+
+
+def test_full_census_80():
+    inst = ref_generate(900, 274, 104, 200, 80, 0.3, 900, 8, 4)
+    _check_search(inst, 1, seeds=[0, 1, 2])
+    _check_search(inst, 0, seeds=[0, 1])
+
+
+def test_c5_shape_prefix():
+    inst = ref_survey_instance(200, 5000, 20, seed=1)
+    _check_search(inst, 1, seeds=[7], max_passes=2)
+
+
+def test_c2_first_pass():
+    inst = ref_survey_instance(500, 10000, 40, seed=1)
+    _check_search(inst, 1, seeds=[7], max_passes=1)

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -286,7 +287,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
-      invb, exp_take, exp_reas, exp_rel, role_rel, ctr, cost, total;
+      invb, exp_take, exp_reas, exp_rel, role_rel, cls_cache, cls_ver, ctr, cost, total;
 };
 
 Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
@@ -318,6 +319,8 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   L.exp_reas = put(8ull * V);
   L.exp_rel = put(8ull * K);
   L.role_rel = put(K);
+  L.cls_cache = put((size_t)B * V);
+  L.cls_ver = put(8ull * B);
   L.cost = own_cost ? put(8ull * M * B) : 0;
   L.total = o;
   return L;
@@ -356,11 +359,13 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   size_t total = 0;
   run.lay.resize(n);
   std::vector<size_t> base(n);
-  int maxV = 0;
+  int maxV = 0, maxB = 0, maxK = 0;
   for (int s = 0; s < n; ++s) {
     const HostScenario& h = run.hs[s];
     const int V = insts[s].n_vehicles, B = insts[s].n_bases;
     maxV = std::max(maxV, V);
+    maxB = std::max(maxB, B);
+    maxK = std::max(maxK, h.K);
     run.lay[s] = layout(M, B, V, h.K, h.psize + V + 1, dev_tables[s] == nullptr);
     base[s] = total;
     total += run.lay[s].total;
@@ -390,6 +395,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     if (B) std::memcpy(hb + L.bveh, h.bveh.data(), 4ull * B);
     if (h.psize) std::memcpy(hb + L.pkind, h.pkind.data(), 4ull * h.psize);
     if (h.psize) std::memcpy(hb + L.pidx, h.pidx.data(), 4ull * h.psize);
+    std::memset(hb + L.cls_ver, 0xff, 8ull * B);  // -1: no cached classes
     if (!dev_tables[s] && (size_t)M * B)
       std::memcpy(hb + L.cost, host_tables[s], 8ull * M * B);
     fpk::Scenario& S = run.arena.scs[s];
@@ -414,6 +420,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.exp_reas = reinterpret_cast<long long*>(db + L.exp_reas);
     S.exp_rel = reinterpret_cast<long long*>(db + L.exp_rel);
     S.role_rel = db + L.role_rel;
+    S.cls_cache = db + L.cls_cache;
+    S.cls_ver = reinterpret_cast<long long*>(db + L.cls_ver);
     S.ctr = reinterpret_cast<fpk::Counters*>(db + L.ctr);
     S.M = M;
     S.B = B;
@@ -446,13 +454,14 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   int buf = 0;
   rng.perm(M, ctx->h_perm[buf]);
   rng.perm(M, ctx->h_perm[buf] + M);
-  const int threads = n == 1 ? 1024 : 256;
+  int threads = n == 1 ? 1024 : 256;
+  if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
   int n_active = n;
   while (n_active > 0) {
     h2d(run.d_active.p, active.data(), n, st);
     h2d(run.d_perm.p, ctx->h_perm[buf], 2ull * M, st);
     check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p, run.d_perm.p + M, M, tabu,
-                           tenure, cfg->debug_check_deltas != 0, maxV, st, threads),
+                           tenure, cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads),
           "pass_kernel");
     ctx->launches += M > 0 ? 2 : 1;
     // next pass's permutations while the device works
@@ -507,6 +516,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     outs[s].device_ms = ms;
     outs[s].exact_fallbacks = c.fallbacks;
     for (int k = 0; k < 6; ++k) outs[s].phase_cycles[k] = c.cycles[k];
+    for (int k = 0; k < 4; ++k) outs[s].event_counts[k] = c.counts[k];
     outs[s].kernel_launches = ctx->launches;
   }
 }

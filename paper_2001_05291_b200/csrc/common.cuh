@@ -32,6 +32,9 @@ struct Counters {
   // launches): 0 row skipping, 1 row context, 2 chunk scans, 3 event pairs,
   // 4 exact fallbacks, 5 relocation prepasses
   unsigned long long cycles[6];
+  // event counts: 0 interesting rows, 1 chunk iterations, 2 row contexts,
+  // 3 relocation prepasses
+  unsigned long long counts[4];
 };
 
 // One search scenario: the resident distance table plus the index-based
@@ -64,9 +67,12 @@ struct Scenario {
   long long* exp_reas;       // [V] {Reassign, vehicle id}
   long long* exp_rel;        // [K] {Relocate, id}, ids of bases and vehicles
   uint8_t* role_rel;         // [K]
+  // relocation-class cache: per target base t, the per-vehicle classes of
+  // the relocation delta, valid while no move has been applied since
+  uint8_t* cls_cache;        // [B*V]
+  long long* cls_ver;        // [B] applied-move count the entry was built at
   Counters* ctr;
   int32_t M, B, V, K, pool_cap;
-  int32_t active;            // host-managed: scenario still searching
 };
 
 }  // namespace fpk

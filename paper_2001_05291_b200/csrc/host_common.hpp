@@ -30,7 +30,7 @@ cudaError_t launch_init(Scenario* d_scs, int n_scn, cudaStream_t stream);
 cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream);
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn, const int32_t* d_pa,
                         const int32_t* d_pb, int M, bool tabu, long long tenure, bool debug, int V,
-                        cudaStream_t stream, int threads);
+                        int B, int K, cudaStream_t stream, int threads);
 }  // namespace fpk
 
 namespace fpk_host {

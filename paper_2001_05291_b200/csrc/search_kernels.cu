@@ -16,8 +16,9 @@
 //    inner-blocked (tick + skip), or evaluated (3 evaluations); an evaluated
 //    pair is an event when one of its three moves MAY be accepted
 //    (takeover/reassign: new cost < current cost; relocation: the per-vehicle
-//    delta class is not certainly >= 0). A block argmin over the position
-//    finds the first event; counts before it give the SearchStats increments.
+//    delta class is not certainly >= 0). All loads of a chunk are issued
+//    before any is consumed; one ballot-based block reduction yields the
+//    first event and the SearchStats increments before it.
 //  * Event pairs are processed exactly as the reference does (takeover, then
 //    relocation, then reassignment, each on the state the previous one left)
 //    with the exact accept rule quick_delta < 0 && candidate_total < total.
@@ -27,7 +28,8 @@
 //
 // The tabu list is the expiry-stamp form (live iff tick < expiry), held in
 // dense per-key arrays; the {Relocate, id} key space is shared by base and
-// vehicle ids exactly like the reference's std::map<TabuKey, Entry>.
+// vehicle ids exactly like the reference's std::map<TabuKey, Entry>. The
+// per-vehicle / per-key state lives in shared memory for the whole pass.
 
 #include <cfloat>
 #include <climits>
@@ -41,6 +43,7 @@ namespace {
 constexpr int U = 4;  // positions per thread per chunk
 enum : uint8_t { CLS_POS = 0, CLS_NEG = 1, CLS_ACC = 2, CLS_AMB = 3 };
 constexpr double kTwoPowM52 = 2.220446049250313e-16;  // 2^-52
+constexpr unsigned FULL = 0xffffffffu;
 
 struct Shared {
   Counters c;                 // block copy of the counters
@@ -51,15 +54,26 @@ struct Shared {
   int lim_ro, lim_ra;                   // row keys: live-positions (outer / any)
   long long t0;                         // tick at the start of the scan segment
   int bi[8];
-  double bd[4];
+  int ev;                               // chunk result broadcast
   int red_i[2][33];
   double red_d[3][33];
 };
 
+// Dynamic shared memory carve-up (see pass_smem_bytes()).
+struct Smem {
+  int* lim_j;          // [V] positions from the segment start a j-key stays live
+  uint8_t* outer_j;    // [V] that key's role is Outer
+  uint8_t* cls;        // [V] relocation class towards the row's empty base
+  double* acc_sum;     // [NW*V] warp-private relocation partial sums
+  double* acc_abs;     // [NW*V]
+  double* stage;       // [NW*32]
+  unsigned* masks;     // [U*NW*3] per-chunk ballots
+};
+
 // Phase timing (thread 0's SM clock), accumulated into Counters::cycles.
 __device__ __forceinline__ long long ph_now() { return threadIdx.x == 0 ? clock64() : 0; }
-#define PH_ADD(sh, k, t0) \
-  do {                    \
+#define PH_ADD(sh, k, t0)                                        \
+  do {                                                           \
     if (threadIdx.x == 0) (sh).c.cycles[k] += clock64() - (t0); \
   } while (0)
 
@@ -67,83 +81,25 @@ __device__ __forceinline__ double cost_at(const Scenario& s, int col, int m) {
   return s.cost[(long long)col * s.M + m];
 }
 
+__device__ __forceinline__ int clamp_lim(long long e, int M) {
+  return e <= 0 ? 0 : (e > M + 1 ? M + 1 : (int)e);
+}
+
 template <int NT>
 __device__ int block_min(int v, Shared& sh) {
-  v = __reduce_min_sync(0xffffffffu, v);
+  v = __reduce_min_sync(FULL, v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) sh.red_i[0][w] = v;
   __syncthreads();
   if (w == 0) {
     int x = l < NT / 32 ? sh.red_i[0][l] : INT_MAX;
-    x = __reduce_min_sync(0xffffffffu, x);
+    x = __reduce_min_sync(FULL, x);
     if (l == 0) sh.red_i[0][32] = x;
   }
   __syncthreads();
   const int r = sh.red_i[0][32];
   __syncthreads();
   return r;
-}
-
-template <int NT>
-__device__ void block_sum2(int& a, int& b, Shared& sh) {
-  a = (int)__reduce_add_sync(0xffffffffu, (unsigned)a);
-  b = (int)__reduce_add_sync(0xffffffffu, (unsigned)b);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    sh.red_i[0][w] = a;
-    sh.red_i[1][w] = b;
-  }
-  __syncthreads();
-  if (w == 0) {
-    int x = l < NT / 32 ? sh.red_i[0][l] : 0;
-    int y = l < NT / 32 ? sh.red_i[1][l] : 0;
-    x = (int)__reduce_add_sync(0xffffffffu, (unsigned)x);
-    y = (int)__reduce_add_sync(0xffffffffu, (unsigned)y);
-    if (l == 0) {
-      sh.red_i[0][32] = x;
-      sh.red_i[1][32] = y;
-    }
-  }
-  __syncthreads();
-  a = sh.red_i[0][32];
-  b = sh.red_i[1][32];
-  __syncthreads();
-}
-
-template <int NT>
-__device__ void block_sum3d(double& a, double& b, double& c, Shared& sh) {
-  for (int o = 16; o > 0; o >>= 1) {
-    a += __shfl_down_sync(0xffffffffu, a, o);
-    b += __shfl_down_sync(0xffffffffu, b, o);
-    c += __shfl_down_sync(0xffffffffu, c, o);
-  }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    sh.red_d[0][w] = a;
-    sh.red_d[1][w] = b;
-    sh.red_d[2][w] = c;
-  }
-  __syncthreads();
-  if (w == 0) {
-    double x = l < NT / 32 ? sh.red_d[0][l] : 0.0;
-    double y = l < NT / 32 ? sh.red_d[1][l] : 0.0;
-    double z = l < NT / 32 ? sh.red_d[2][l] : 0.0;
-    for (int o = 16; o > 0; o >>= 1) {
-      x += __shfl_down_sync(0xffffffffu, x, o);
-      y += __shfl_down_sync(0xffffffffu, y, o);
-      z += __shfl_down_sync(0xffffffffu, z, o);
-    }
-    if (l == 0) {
-      sh.red_d[0][32] = x;
-      sh.red_d[1][32] = y;
-      sh.red_d[2][32] = z;
-    }
-  }
-  __syncthreads();
-  a = sh.red_d[0][32];
-  b = sh.red_d[1][32];
-  c = sh.red_d[2][32];
-  __syncthreads();
 }
 
 // Rigorous bound for a single-substitution candidate (takeover/reassign):
@@ -189,29 +145,8 @@ __device__ bool exact_reloc_accept(const Scenario& s, int t, int mover) {
   return b < a;
 }
 
-// Per-vehicle relocation deltas towards target base t, in any order, with
-// the data needed for a rigorous sign/accept classification.
-template <int NT>
-__device__ void reloc_sums(const Scenario& s, int t, double* sumD, double* absD,
-                           int* cnt) {
-  for (int v = threadIdx.x; v < s.V; v += NT) {
-    sumD[v] = 0.0;
-    absD[v] = 0.0;
-    cnt[v] = 0;
-  }
-  __syncthreads();
-  const double* col = s.cost + (long long)t * s.M;
-  for (int m = threadIdx.x; m < s.M; m += NT) {
-    const int v = s.mv[m];
-    const double d = col[m] - s.mc[m];
-    atomicAdd(&sumD[v], d);
-    atomicAdd(&absD[v], fabs(d));
-    atomicAdd(&cnt[v], 1);
-  }
-  __syncthreads();
-}
-
-// Classification of one vehicle's relocation (see header comment):
+// Classification of one vehicle's relocation from its (any-order) delta sum,
+// absolute sum and term count:
 // POS  quick_delta >= 0 for sure (never accepted)
 // NEG  quick_delta < 0 for sure, the total comparison is not yet settled
 // ACC  accepted for sure
@@ -230,6 +165,74 @@ __device__ __forceinline__ uint8_t reloc_class(double sum, double abs, int n,
 
 __device__ __forceinline__ bool compat_vm(bool vehicle_fixed, bool rotary_only) {
   return !(vehicle_fixed && rotary_only);
+}
+
+// Relocation classes of every vehicle towards empty base t, into sm.cls,
+// through the (t, version) cache. The per-vehicle sums use warp-private
+// accumulators: lanes of a warp holding the same vehicle are grouped with
+// __match_any_sync and their leader adds the group's terms, so no shared
+// memory atomics are needed (fp64 shared atomics are CAS loops).
+template <int NT>
+__device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm, int t) {
+  const long long ver = (long long)sh.c.applied;
+  const int V = s.V;
+  if (s.cls_ver[t] == ver) {  // uniform: all threads read the same word
+    for (int v = threadIdx.x; v < V; v += NT) sm.cls[v] = s.cls_cache[(long long)t * V + v];
+    __syncthreads();
+    return;
+  }
+  const long long r0 = ph_now();
+  if (threadIdx.x == 0) sh.c.counts[3] += 1;
+  constexpr int NW = NT / 32;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  double* as = sm.acc_sum + (long long)w * V;
+  double* aa = sm.acc_abs + (long long)w * V;
+  for (int v = l; v < V; v += 32) {
+    as[v] = 0.0;
+    aa[v] = 0.0;
+  }
+  double* st = sm.stage + w * 32;
+  __syncwarp();
+  const double* col = s.cost + (long long)t * s.M;
+  for (int base = w * 32; base < s.M; base += NT) {
+    const int m = base + l;
+    int v = -1;
+    double d = 0.0;
+    if (m < s.M) {
+      v = s.mv[m];
+      d = col[m] - s.mc[m];
+    }
+    const unsigned peers = __match_any_sync(FULL, v);
+    st[l] = d;
+    __syncwarp();
+    if (v >= 0 && l == __ffs(peers) - 1) {
+      double sum = 0.0, abs = 0.0;
+      for (unsigned b = peers; b; b &= b - 1) {
+        const double x = st[__ffs(b) - 1];
+        sum += x;
+        abs += fabs(x);
+      }
+      as[v] += sum;
+      aa[v] += abs;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  const double bt = single_bound(s, sh);
+  const bool heli = s.bheli[t];
+  for (int v = threadIdx.x; v < V; v += NT) {
+    double sum = 0.0, abs = 0.0;
+    for (int k = 0; k < NW; ++k) {
+      sum += sm.acc_sum[(long long)k * V + v];
+      abs += sm.acc_abs[(long long)k * V + v];
+    }
+    const uint8_t c = (s.vfixed[v] && heli) ? CLS_POS : reloc_class(sum, abs, s.vcount[v], bt);
+    sm.cls[v] = c;
+    s.cls_cache[(long long)t * V + v] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s.cls_ver[t] = ver;
+  PH_ADD(sh, 5, r0);
 }
 
 // ---- moves (proj/src/search.cpp:169-220) ---------------------------------
@@ -316,16 +319,11 @@ __device__ void debug_check(const Scenario& s, Shared& sh) {
   }
 }
 
-__device__ void insert_outer(const Scenario& s, long long* arr, int idx, long long exp) {
-  arr[idx] = exp;
-}
-
 // Processes the pair (i, j) exactly as try_move x3 (proj/src/search.cpp:277-303,
 // 333-341). Block-cooperative; returns with the block synchronised.
 template <int NT>
-__device__ void process_pair(const Scenario& s, Shared& sh, int i, int j, bool tabu,
-                             long long tenure, bool debug, double* sumD, double* absD,
-                             int* cnt) {
+__device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int i, int j,
+                             bool tabu, long long tenure, bool debug) {
   const long long exp = sh.c.tick + tenure;
   // ---- takeover
   if (threadIdx.x == 0) {
@@ -347,7 +345,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, int i, int j, bool t
             apply_takeover(s, sh, j, g, i);
             sh.c.applied += 1;
             sh.c.pass_applied += 1;
-            if (tabu) insert_outer(s, s.exp_take, g, exp);
+            if (tabu) s.exp_take[g] = exp;
             if (debug) debug_check(s, sh);
           }
         }
@@ -368,20 +366,9 @@ __device__ void process_pair(const Scenario& s, Shared& sh, int i, int j, bool t
   // ---- relocation
   const int t = sh.bi[0], mover = sh.bi[1];
   if (t >= 0) {
-    // sums for the mover only
-    double a = 0.0, b = 0.0, c = 0.0;
-    const double* col = s.cost + (long long)t * s.M;
-    for (int m = threadIdx.x; m < s.M; m += NT)
-      if (s.mv[m] == mover) {
-        const double d = col[m] - s.mc[m];
-        a += d;
-        b += fabs(d);
-        c += 1.0;
-      }
-    block_sum3d<NT>(a, b, c, sh);
+    relocation_classes<NT>(s, sh, sm, t);
     if (threadIdx.x == 0) {
-      const double bt = single_bound(s, sh);
-      const uint8_t cls = reloc_class(a, b, (int)c, bt);
+      const uint8_t cls = sm.cls[mover];
       bool acc = cls == CLS_ACC;
       if (cls == CLS_NEG || cls == CLS_AMB) {
         const long long f0 = ph_now();
@@ -430,7 +417,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, int i, int j, bool t
           apply_reassign(s, sh, j, g);
           sh.c.applied += 1;
           sh.c.pass_applied += 1;
-          if (tabu) insert_outer(s, s.exp_reas, g, exp);
+          if (tabu) s.exp_reas[g] = exp;
           if (debug) debug_check(s, sh);
         }
       }
@@ -442,10 +429,9 @@ __device__ void process_pair(const Scenario& s, Shared& sh, int i, int j, bool t
 
 // Row context after any state change (thread 0 writes, all read after sync).
 template <int NT>
-__device__ void make_context(const Scenario& s, Shared& sh, int i, bool tabu, int* lim_j,
-                             uint8_t* outer_j, uint8_t* cls, double* sumD, double* absD,
-                             int* cnt) {
+__device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int i, bool tabu) {
   if (threadIdx.x == 0) {
+    sh.c.counts[2] += 1;
     const int g = s.mv[i];
     sh.gain_r = g;
     sh.col_r = s.vbase[g];
@@ -462,8 +448,7 @@ __device__ void make_context(const Scenario& s, Shared& sh, int i, bool tabu, in
         sh.col_t = s.vbase[x];
         sh.fixed_t = s.vfixed[x];
         if (tabu) {
-          const long long e = s.exp_take[x] - T;
-          const int lim = e <= 0 ? 0 : (e > s.M + 1 ? s.M + 1 : (int)e);
+          const int lim = clamp_lim(s.exp_take[x] - T, s.M);
           lim_ro = lim;
           lim_ra = lim;
         }
@@ -472,16 +457,14 @@ __device__ void make_context(const Scenario& s, Shared& sh, int i, bool tabu, in
         sh.heli_t = s.bheli[x];
         if (tabu) {
           const int kk = s.brk[x];
-          const long long e = s.exp_rel[kk] - T;
-          const int lim = e <= 0 ? 0 : (e > s.M + 1 ? s.M + 1 : (int)e);
+          const int lim = clamp_lim(s.exp_rel[kk] - T, s.M);
           if (s.role_rel[kk] == ROLE_OUTER) lim_ro = lim;
           lim_ra = lim;
         }
       }
     }
     if (tabu) {
-      const long long e = s.exp_reas[g] - T;
-      const int lim = e <= 0 ? 0 : (e > s.M + 1 ? s.M + 1 : (int)e);
+      const int lim = clamp_lim(s.exp_reas[g] - T, s.M);
       lim_ro = max(lim_ro, lim);
       lim_ra = max(lim_ra, lim);
     }
@@ -493,33 +476,27 @@ __device__ void make_context(const Scenario& s, Shared& sh, int i, bool tabu, in
     const long long T = sh.t0;
     for (int v = threadIdx.x; v < s.V; v += NT) {
       const int k = s.vrk[v];
-      const long long e = s.exp_rel[k] - T;
-      lim_j[v] = e <= 0 ? 0 : (e > s.M + 1 ? s.M + 1 : (int)e);
-      outer_j[v] = s.role_rel[k] == ROLE_OUTER;
+      sm.lim_j[v] = clamp_lim(s.exp_rel[k] - T, s.M);
+      sm.outer_j[v] = s.role_rel[k] == ROLE_OUTER;
     }
   }
   const int t = sh.rel_t;
-  if (t >= 0) {
-    const long long r0 = ph_now();
-    reloc_sums<NT>(s, t, sumD, absD, cnt);
-    const double bt = single_bound(s, sh);
-    for (int v = threadIdx.x; v < s.V; v += NT)
-      cls[v] = (s.vfixed[v] && sh.heli_t) ? CLS_POS : reloc_class(sumD[v], absD[v], cnt[v], bt);
-    PH_ADD(sh, 5, r0);
-  }
+  if (t >= 0) relocation_classes<NT>(s, sh, sm, t);
   __syncthreads();
 }
 
 // One outer-index row, proj/src/search.cpp:307-346.
 template <int NT>
-__device__ void run_row(const Scenario& s, Shared& sh, int i, const int32_t* __restrict__ pb,
-                        bool tabu, long long tenure, bool debug, int* lim_j, uint8_t* outer_j,
-                        uint8_t* cls, double* sumD, double* absD, int* cnt) {
+__device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i,
+                        const int32_t* __restrict__ pb, bool tabu, long long tenure, bool debug) {
+  constexpr int NW = NT / 32;
   const int M = s.M;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   int p = 0;
+  if (threadIdx.x == 0) sh.c.counts[0] += 1;
   while (p < M) {
     const long long c0 = ph_now();
-    make_context<NT>(s, sh, i, tabu, lim_j, outer_j, cls, sumD, absD, cnt);
+    make_context<NT>(s, sh, sm, i, tabu);
     PH_ADD(sh, 1, c0);
     const long long c1 = ph_now();
     const int p_seg = p;
@@ -527,62 +504,126 @@ __device__ void run_row(const Scenario& s, Shared& sh, int i, const int32_t* __r
     const int gain_t = sh.gain_t, col_t = sh.col_t, fixed_t = sh.fixed_t;
     const int rel_t = sh.rel_t;
     const int lim_ro = sh.lim_ro, lim_ra = sh.lim_ra;
+    const double* colr = s.cost + (long long)col_r * M;
+    const double* colt = s.cost + (long long)(gain_t >= 0 ? col_t : 0) * M;
     int ev = INT_MAX;
     while (p < M) {
-      // classify U positions per thread; bit k of `inner`/`unb` marks status
-      unsigned inner = 0, unb = 0;
-      int first = INT_MAX;
+      // ---- issue every load of the chunk first
+      int vq[U], jq[U];
+      double mq[U];
+      bool rq[U];
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         const int q = p + k * NT + threadIdx.x;
-        if (q >= M) break;
-        const int v = s.mvp[q];
+        vq[k] = 0;
+        jq[k] = 0;
+        mq[k] = 0.0;
+        rq[k] = false;
+        if (q < M) {
+          vq[k] = s.mvp[q];
+          jq[k] = pb[q];
+          mq[k] = s.mcp[q];
+          rq[k] = s.rop[q];
+        }
+      }
+      double cr[U], ct[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int q = p + k * NT + threadIdx.x;
+        cr[k] = q < M ? colr[jq[k]] : 0.0;
+        ct[k] = (q < M && gain_t >= 0) ? colt[jq[k]] : 0.0;
+      }
+      // ---- classify: bit k of ev/in/un
+      unsigned evb = 0, inb = 0, unb = 0;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int q = p + k * NT + threadIdx.x;
+        if (q >= M) continue;
+        const int v = vq[k];
         if (tabu) {
           const int off = q - p_seg;
-          const int lj = lim_j[v];
-          const bool oj = outer_j[v];
-          if (off < lim_ro || (off < lj && oj)) {
-            first = min(first, q);
-            break;
+          const int lj = sm.lim_j[v];
+          if (off < lim_ro || (off < lj && sm.outer_j[v])) {
+            evb |= 1u << k;
+            continue;
           }
           if (off < lim_ra || off < lj) {
-            inner |= 1u << k;
+            inb |= 1u << k;
             continue;
           }
         }
-        const int j = pb[q];
-        const double mcj = s.mcp[q];
-        const bool roj = s.rop[q];
         bool e = false;
-        if (gain_t >= 0 && compat_vm(fixed_t, roj)) e |= cost_at(s, col_t, j) < mcj;
-        if (rel_t >= 0) e |= cls[v] != CLS_POS;
-        if (v != gain_r && compat_vm(fixed_r, roj)) e |= cost_at(s, col_r, j) < mcj;
-        if (e) {
-          first = min(first, q);
-          break;
-        }
-        unb |= 1u << k;
+        if (gain_t >= 0 && compat_vm(fixed_t, rq[k])) e |= ct[k] < mq[k];
+        if (rel_t >= 0) e |= sm.cls[v] != CLS_POS;
+        if (v != gain_r && compat_vm(fixed_r, rq[k])) e |= cr[k] < mq[k];
+        if (e)
+          evb |= 1u << k;
+        else
+          unb |= 1u << k;
       }
-      ev = block_min<NT>(first, sh);
-      int n_in = 0, n_unb = 0;
+      // ---- one block reduction: first event + counts before it
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        const int q = p + k * NT + threadIdx.x;
-        if (q >= ev || q >= M) break;
-        n_in += (inner >> k) & 1u;
-        n_unb += (unb >> k) & 1u;
-      }
-      block_sum2<NT>(n_in, n_unb, sh);
-      const int chunk_end = min(p + NT * U, M);
-      const int stop = min(ev, chunk_end);
-      if (threadIdx.x == 0) {
-        sh.c.skips_inner += (unsigned long long)n_in;
-        sh.c.evaluations += 3ull * (unsigned long long)n_unb;
-        if (tabu) sh.c.tick += stop - p;
-        if (n_in > 0) sh.c.pass_skipped = 1;
+        const unsigned a = __ballot_sync(FULL, (evb >> k) & 1u);
+        const unsigned b = __ballot_sync(FULL, (inb >> k) & 1u);
+        const unsigned c = __ballot_sync(FULL, (unb >> k) & 1u);
+        if (l == 0) {
+          sm.masks[(k * NW + w) * 3 + 0] = a;
+          sm.masks[(k * NW + w) * 3 + 1] = b;
+          sm.masks[(k * NW + w) * 3 + 2] = c;
+        }
       }
       __syncthreads();
-      p = stop;
+      if (w == 0) {
+        // lane l summarises warp l's masks
+        unsigned me[U], mi[U], mu[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          me[k] = l < NW ? sm.masks[(k * NW + l) * 3 + 0] : 0u;
+          mi[k] = l < NW ? sm.masks[(k * NW + l) * 3 + 1] : 0u;
+          mu[k] = l < NW ? sm.masks[(k * NW + l) * 3 + 2] : 0u;
+        }
+        int kstar = U, wstar = 32;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const unsigned any = __ballot_sync(FULL, me[k] != 0u);
+          if (kstar == U && any) {
+            kstar = k;
+            wstar = __ffs(any) - 1;
+          }
+        }
+        int n_in = 0, n_un = 0;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          unsigned keep = 0u;
+          if (k < kstar) keep = FULL;
+          else if (k == kstar) {
+            if (l < wstar) keep = FULL;
+            else if (l == wstar) keep = (1u << (__ffs(me[k]) - 1)) - 1u;
+          }
+          n_in += __popc(mi[k] & keep);
+          n_un += __popc(mu[k] & keep);
+        }
+        n_in = (int)__reduce_add_sync(FULL, (unsigned)n_in);
+        n_un = (int)__reduce_add_sync(FULL, (unsigned)n_un);
+        int evp = INT_MAX;
+        if (kstar < U) {
+          const unsigned wm = __shfl_sync(FULL, me[kstar < U ? kstar : 0], wstar);
+          evp = p + kstar * NT + wstar * 32 + (__ffs(wm) - 1);
+        }
+        if (l == 0) {
+          const int stop = min(evp, min(p + NT * U, M));
+          sh.ev = evp;
+          sh.c.counts[1] += 1;
+          sh.c.skips_inner += (unsigned long long)n_in;
+          sh.c.evaluations += 3ull * (unsigned long long)n_un;
+          if (tabu) sh.c.tick += stop - p;
+          if (n_in > 0) sh.c.pass_skipped = 1;
+        }
+      }
+      __syncthreads();
+      ev = sh.ev;
+      p = min(ev, min(p + NT * U, M));
       if (ev != INT_MAX) break;
     }
     PH_ADD(sh, 2, c1);
@@ -592,7 +633,7 @@ __device__ void run_row(const Scenario& s, Shared& sh, int i, const int32_t* __r
     if (tabu) {
       const int v = s.mvp[p];
       const int off = p - p_seg;
-      outer_ev = off < lim_ro || (off < lim_j[v] && outer_j[v]);
+      outer_ev = off < lim_ro || (off < sm.lim_j[v] && sm.outer_j[v]);
     }
     if (outer_ev) {
       if (threadIdx.x == 0) {
@@ -604,13 +645,14 @@ __device__ void run_row(const Scenario& s, Shared& sh, int i, const int32_t* __r
       return;
     }
     const long long c2 = ph_now();
-    process_pair<NT>(s, sh, i, pb[p], tabu, tenure, debug, sumD, absD, cnt);
+    process_pair<NT>(s, sh, sm, i, pb[p], tabu, tenure, debug);
     PH_ADD(sh, 3, c2);
-    __syncthreads();
     if (sh.c.error) return;
     p += 1;
   }
 }
+
+__host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 }  // namespace
 
@@ -628,22 +670,79 @@ __global__ void mirror_kernel(Scenario* scs, const int32_t* __restrict__ active,
   }
 }
 
+// Shared-memory bytes of the always-resident part and of the optional copy
+// of the small per-vehicle / per-key state.
+size_t pass_smem_core(int V, int NT) {
+  const int NW = NT / 32;
+  return align16(4ull * V) + align16(V) + align16(V) + 2 * align16(8ull * NW * V) +
+         align16(8ull * NW * 32) + align16(4ull * U * NW * 3) + 64;
+}
+size_t pass_smem_state(int V, int B, int K) {
+  return align16(8ull * V) * 2 + align16(8ull * K) + align16(K) + align16(4ull * V) * 3 +
+         align16(V) + align16(4ull * B) + align16(B) + 64;
+}
+
 // One pass over perm_a for every active scenario (blockIdx.x = scenario).
 template <int NT>
-__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 4)
+__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ pa,
-                const int32_t* __restrict__ pb, int tabu_i, long long tenure, int debug_i) {
+                const int32_t* __restrict__ pb, int tabu_i, long long tenure, int debug_i,
+                int state_in_smem) {
   if (!active[blockIdx.x]) return;
-  const Scenario s = scs[blockIdx.x];
+  const Scenario g = scs[blockIdx.x];
+  Scenario s = g;
   const bool tabu = tabu_i != 0, debug = debug_i != 0;
   __shared__ Shared sh;
   extern __shared__ __align__(16) unsigned char dyn[];
-  double* sumD = reinterpret_cast<double*>(dyn);
-  double* absD = sumD + s.V;
-  int* lim_j = reinterpret_cast<int*>(absD + s.V);
-  int* cnt = lim_j + s.V;
-  uint8_t* outer_j = reinterpret_cast<uint8_t*>(cnt + s.V);
-  uint8_t* cls = outer_j + s.V;
+  constexpr int NW = NT / 32;
+  const int V = s.V, B = s.B, K = s.K;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char* p = dyn + off;
+    off = align16(off + bytes);
+    return p;
+  };
+  Smem sm;
+  sm.lim_j = reinterpret_cast<int*>(take(4ull * V));
+  sm.outer_j = take(V);
+  sm.cls = take(V);
+  sm.acc_sum = reinterpret_cast<double*>(take(8ull * NW * V));
+  sm.acc_abs = reinterpret_cast<double*>(take(8ull * NW * V));
+  sm.stage = reinterpret_cast<double*>(take(8ull * NW * 32));
+  sm.masks = reinterpret_cast<unsigned*>(take(4ull * U * NW * 3));
+  if (state_in_smem) {
+    // the small mutable state lives in shared memory for the whole pass
+    s.exp_take = reinterpret_cast<long long*>(take(8ull * V));
+    s.exp_reas = reinterpret_cast<long long*>(take(8ull * V));
+    s.exp_rel = reinterpret_cast<long long*>(take(8ull * K));
+    s.role_rel = take(K);
+    s.vbase = reinterpret_cast<int32_t*>(take(4ull * V));
+    s.vcount = reinterpret_cast<int32_t*>(take(4ull * V));
+    int32_t* vrk = reinterpret_cast<int32_t*>(take(4ull * V));
+    uint8_t* vfixed = take(V);
+    int32_t* brk = reinterpret_cast<int32_t*>(take(4ull * B));
+    uint8_t* bheli = take(B);
+    for (int v = threadIdx.x; v < V; v += NT) {
+      s.exp_take[v] = g.exp_take[v];
+      s.exp_reas[v] = g.exp_reas[v];
+      s.vbase[v] = g.vbase[v];
+      s.vcount[v] = g.vcount[v];
+      vrk[v] = g.vrk[v];
+      vfixed[v] = g.vfixed[v];
+    }
+    for (int k = threadIdx.x; k < K; k += NT) {
+      s.exp_rel[k] = g.exp_rel[k];
+      s.role_rel[k] = g.role_rel[k];
+    }
+    for (int b = threadIdx.x; b < B; b += NT) {
+      brk[b] = g.brk[b];
+      bheli[b] = g.bheli[b];
+    }
+    s.vrk = vrk;
+    s.vfixed = vfixed;
+    s.brk = brk;
+    s.bheli = bheli;
+  }
   if (threadIdx.x == 0) {
     sh.c = *s.ctr;
     sh.c.pass_applied = 0;
@@ -687,11 +786,23 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : 4)
       PH_ADD(sh, 0, b0);
       if (found == INT_MAX) continue;
     }
-    run_row<NT>(s, sh, pa[r], pb, tabu, tenure, debug, lim_j, outer_j, cls, sumD, absD, cnt);
+    run_row<NT>(s, sh, sm, pa[r], pb, tabu, tenure, debug);
     __syncthreads();
     r += 1;
   }
-  if (threadIdx.x == 0) *s.ctr = sh.c;
+  if (state_in_smem) {
+    for (int v = threadIdx.x; v < V; v += NT) {
+      g.exp_take[v] = s.exp_take[v];
+      g.exp_reas[v] = s.exp_reas[v];
+      g.vbase[v] = s.vbase[v];
+      g.vcount[v] = s.vcount[v];
+    }
+    for (int k = threadIdx.x; k < K; k += NT) {
+      g.exp_rel[k] = s.exp_rel[k];
+      g.role_rel[k] = s.role_rel[k];
+    }
+  }
+  if (threadIdx.x == 0) *g.ctr = sh.c;
 }
 
 // Search start: per-mission costs, per-vehicle counts and the exact initial
@@ -720,24 +831,36 @@ __global__ void final_kernel(Scenario* scs) {
   }
 }
 
-size_t pass_dyn_smem(int V) { return (size_t)V * (8 + 8 + 4 + 4 + 1 + 1) + 16; }
+template <int NT>
+static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int n_scn,
+                                  const int32_t* d_pa, const int32_t* d_pb, bool tabu,
+                                  long long tenure, bool debug, int V, int B, int K,
+                                  cudaStream_t stream) {
+  const size_t core = pass_smem_core(V, NT);
+  const size_t state = pass_smem_state(V, B, K);
+  const size_t limit = 200 * 1024;
+  if (core > limit) return cudaErrorInvalidConfiguration;
+  const int in_smem = core + state <= limit ? 1 : 0;
+  const size_t smem = core + (in_smem ? state : 0);
+  cudaFuncSetAttribute(pass_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  pass_kernel<NT><<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_pa, d_pb, tabu, tenure, debug,
+                                               in_smem);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn, const int32_t* d_pa,
                         const int32_t* d_pb, int M, bool tabu, long long tenure, bool debug, int V,
-                        cudaStream_t stream, int threads) {
-  const size_t smem = pass_dyn_smem(V);
+                        int B, int K, cudaStream_t stream, int threads) {
   dim3 mg((M + 255) / 256 < 64 ? (M + 255) / 256 : 64, n_scn);
   if (M > 0) mirror_kernel<<<mg, 256, 0, stream>>>(d_scs, d_active, d_pb);
-  if (threads == 1024) {
-    cudaFuncSetAttribute(pass_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    pass_kernel<1024><<<n_scn, 1024, smem, stream>>>(d_scs, d_active, d_pa, d_pb, tabu, tenure,
-                                                    debug);
-  } else {
-    cudaFuncSetAttribute(pass_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    pass_kernel<256><<<n_scn, 256, smem, stream>>>(d_scs, d_active, d_pa, d_pb, tabu, tenure,
-                                                  debug);
-  }
-  return cudaGetLastError();
+  if (threads == 1024)
+    return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_pa, d_pb, tabu, tenure, debug, V, B, K,
+                                stream);
+  if (threads == 512)
+    return launch_pass_nt<512>(d_scs, d_active, n_scn, d_pa, d_pb, tabu, tenure, debug, V, B, K,
+                               stream);
+  return launch_pass_nt<256>(d_scs, d_active, n_scn, d_pa, d_pb, tabu, tenure, debug, V, B, K,
+                             stream);
 }
 
 cudaError_t launch_init(Scenario* d_scs, int n_scn, cudaStream_t stream) {

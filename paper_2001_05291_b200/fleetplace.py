@@ -441,6 +441,7 @@ class SearchStats:
     device_ms: float = 0.0
     exact_fallbacks: int = 0
     phase_cycles: tuple = ()
+    event_counts: tuple = ()
 
 
 @dataclass
@@ -506,7 +507,8 @@ def _stats(r: A.fp_search_result) -> SearchStats:
     s = r.stats
     return SearchStats(int(s.passes), int(s.evaluations), int(s.applied_moves), int(s.committed_moves),
                        int(s.tabu_skips_outer), int(s.tabu_skips_inner), float(s.final_objective_km),
-                       float(r.device_ms), int(r.exact_fallbacks), tuple(int(x) for x in r.phase_cycles))
+                       float(r.device_ms), int(r.exact_fallbacks), tuple(int(x) for x in r.phase_cycles),
+                       tuple(int(x) for x in r.event_counts))
 
 
 def search_arrays(inst: Instance, t: DistanceTable, cfg: SearchConfig, vehicle_base: np.ndarray,

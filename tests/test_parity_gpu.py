@@ -78,3 +78,38 @@ def test_c5_shape_prefix():
 def test_c2_first_pass():
     inst = ref_survey_instance(500, 10000, 40, seed=1)
     _check_search(inst, 1, seeds=[7], max_passes=1)
+
+
+@pytest.mark.parametrize("shape,seeds,passes", [((50, 200, 10), (1, 2, 3, 7), None),
+                                                ((200, 5000, 20), (7,), 2),
+                                                ((500, 10000, 40), (7,), 1)])
+def test_end_to_end_pipeline_matches_reference(shape, seeds, passes):
+    """The whole hot path on the device — table (kernel 1), ranking (kernel 2),
+    tabu search (kernels 3+4) — against the reference's whole pipeline on the
+    same instance: same base set, same move sequence (all SearchStats) and
+    objective within 1e-9 relative (BASELINE.json north star)."""
+    inst = F.survey_instance(*shape, seed=1)
+    t = F.build_distance_table(inst)
+    start = F.rank_bases(inst, t)
+    cost = ref_table(inst)
+    r = ref_rank(inst, cost)
+    assert np.array_equal(start.vehicle_base, r.vehicle_base)
+    assert np.array_equal(start.mission_vehicle, r.mission_vehicle)
+    assert np.array_equal(start.unused_index, r.unused)
+    pk, px = initial_pool_idx(inst, r.vehicle_base, r.mission_vehicle, r.unused)
+    for seed in seeds:
+        ref = ref_search(inst, cost, 1, seed, r.vehicle_base, r.mission_vehicle, pk, px,
+                         max_passes=passes)
+        cfg = F.SearchConfig(seed=seed, mode=F.SearchMode.Tabu, max_passes=passes)
+        got = F.search_arrays(inst, t, cfg, start.vehicle_base, start.mission_vehicle, pk, px)
+        s = got.stats
+        assert (s.passes, s.evaluations, s.applied_moves, s.tabu_skips_outer,
+                s.tabu_skips_inner) == (ref.stats[0], ref.stats[1], ref.stats[2], ref.stats[4],
+                                        ref.stats[5])
+        assert np.array_equal(got.vehicle_base, ref.vehicle_base)
+        assert np.array_equal(got.mission_vehicle, ref.mission_vehicle)
+        assert abs(s.final_objective_km - ref.stats[6]) <= 1e-9 * ref.stats[6]
+        # coverage: every mission served by a compatible placed vehicle
+        assert (got.mission_vehicle >= 0).all()
+        fixed = inst.vehicle_kind[got.mission_vehicle] == 1
+        assert not (fixed & (inst.rotary_only == 1)).any()

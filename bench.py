@@ -176,8 +176,8 @@ def run_ours(args) -> None:
         "phase_ms": dict(zip(("row_skip", "row_context", "chunk_scan", "event_pairs",
                               "exact_fallbacks", "reloc_prepass"),
                              [c / (clocks["sm_mhz"] or 1965.0) / 1e3 for c in st.phase_cycles])),
-        "event_counts": dict(zip(("interesting_rows", "chunk_scans", "row_contexts",
-                                  "reloc_prepasses"), st.event_counts)),
+        "event_counts": dict(zip(("scanned_rows", "scan_steps", "row_contexts",
+                                  "reloc_prepasses", "eventless_rows_o1"), st.event_counts)),
         "e2e": {"value": ws * evals / e2e_mean, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_mean * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -125,8 +125,9 @@ typedef struct fp_search_result {
   uint64_t phase_cycles[6];      /* SM cycles per automaton phase (scenario 0):
                                     row skip, row context, chunk scan, event
                                     pairs, exact fallbacks, relocation prepass */
-  uint64_t event_counts[4];      /* scenario 0: interesting rows, chunk scans,
-                                    row contexts, relocation prepasses */
+  uint64_t event_counts[5];      /* scenario 0: scanned rows, scan steps, row
+                                    contexts, relocation prepasses, rows settled
+                                    by the O(1) eventless test */
 } fp_search_result;
 
 /* RankedStart (proj/include/fleetplace/rank.hpp:10-14) in index form. */

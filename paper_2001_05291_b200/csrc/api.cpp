@@ -287,7 +287,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
-      invb, exp_take, exp_reas, exp_rel, role_rel, cls_cache, cls_ver, ctr, cost, total;
+      invb, exp_take, exp_reas, exp_rel, role_rel, cls_cache, cls_ver, cls_any, imp, mem, ctr, cost, total;
 };
 
 Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
@@ -321,6 +321,10 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   L.role_rel = put(K);
   L.cls_cache = put((size_t)B * V);
   L.cls_ver = put(8ull * B);
+  L.cls_any = put(B);
+  const size_t nwd = ((size_t)M + 31) / 32;
+  L.imp = put(4ull * V * nwd);
+  L.mem = put(4ull * V * nwd);
   L.cost = own_cost ? put(8ull * M * B) : 0;
   L.total = o;
   return L;
@@ -422,6 +426,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.role_rel = db + L.role_rel;
     S.cls_cache = db + L.cls_cache;
     S.cls_ver = reinterpret_cast<long long*>(db + L.cls_ver);
+    S.cls_any = db + L.cls_any;
+    S.imp = reinterpret_cast<uint32_t*>(db + L.imp);
+    S.mem = reinterpret_cast<uint32_t*>(db + L.mem);
+    S.nwd = (M + 31) / 32;
     S.ctr = reinterpret_cast<fpk::Counters*>(db + L.ctr);
     S.M = M;
     S.B = B;
@@ -454,7 +462,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   int buf = 0;
   rng.perm(M, ctx->h_perm[buf]);
   rng.perm(M, ctx->h_perm[buf] + M);
-  int threads = n == 1 ? 1024 : 256;
+  int threads = n == 1 ? 512 : 256;
   if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
   int n_active = n;
   while (n_active > 0) {
@@ -516,7 +524,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     outs[s].device_ms = ms;
     outs[s].exact_fallbacks = c.fallbacks;
     for (int k = 0; k < 6; ++k) outs[s].phase_cycles[k] = c.cycles[k];
-    for (int k = 0; k < 4; ++k) outs[s].event_counts[k] = c.counts[k];
+    for (int k = 0; k < 5; ++k) outs[s].event_counts[k] = c.counts[k];
     outs[s].kernel_launches = ctx->launches;
   }
 }

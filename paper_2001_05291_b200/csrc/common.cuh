@@ -34,7 +34,7 @@ struct Counters {
   unsigned long long cycles[6];
   // event counts: 0 interesting rows, 1 chunk iterations, 2 row contexts,
   // 3 relocation prepasses
-  unsigned long long counts[4];
+  unsigned long long counts[5];   // ... 4 rows resolved by the O(1) eventless test
 };
 
 // One search scenario: the resident distance table plus the index-based
@@ -71,8 +71,15 @@ struct Scenario {
   // the relocation delta, valid while no move has been applied since
   uint8_t* cls_cache;        // [B*V]
   long long* cls_ver;        // [B] applied-move count the entry was built at
+  uint8_t* cls_any;          // [B] some compatible vehicle's class is not POS
+  // perm_b-position bitsets, word w covers positions [32w, 32w+32):
+  //  imp[g]: reassigning / taking over that position's mission to vehicle g
+  //          would lower its cost (mv != g, compatible, cost(j, base(g)) < mc[j])
+  //  mem[v]: the position's mission is served by vehicle v
+  uint32_t* imp;             // [V*NWD]
+  uint32_t* mem;             // [V*NWD]
   Counters* ctr;
-  int32_t M, B, V, K, pool_cap;
+  int32_t M, B, V, K, pool_cap, nwd;
 };
 
 }  // namespace fpk

@@ -40,7 +40,6 @@ namespace fpk {
 
 namespace {
 
-constexpr int U = 4;  // positions per thread per chunk
 enum : uint8_t { CLS_POS = 0, CLS_NEG = 1, CLS_ACC = 2, CLS_AMB = 3 };
 constexpr double kTwoPowM52 = 2.220446049250313e-16;  // 2^-52
 constexpr unsigned FULL = 0xffffffffu;
@@ -54,7 +53,10 @@ struct Shared {
   int lim_ro, lim_ra;                   // row keys: live-positions (outer / any)
   long long t0;                         // tick at the start of the scan segment
   int bi[8];
-  int ev;                               // chunk result broadcast
+  int ev;                               // scan step result broadcast
+  int nj;                               // live j-keys in sm.jl_*
+  long long jexp_max;                   // latest expiry of any vehicle's {Relocate, id} key
+  int tmp;
   int red_i[2][33];
   double red_d[3][33];
 };
@@ -67,7 +69,12 @@ struct Smem {
   double* acc_sum;     // [NW*V] warp-private relocation partial sums
   double* acc_abs;     // [NW*V]
   double* stage;       // [NW*32]
-  unsigned* masks;     // [U*NW*3] per-chunk ballots
+  int* wsum;           // [NW*3] per-warp scan summaries
+  int* impc;           // [V] set bits of imp[g] (0 = no reassign/takeover to g improves)
+  int* jl_v;           // [V] vehicles whose {Relocate, id} j-key is live
+  int* jl_lim;         // [V] its live window (positions from the segment start)
+  uint8_t* jl_outer;   // [V] its role is Outer
+  const int32_t* pb;   // perm_b
 };
 
 // Phase timing (thread 0's SM clock), accumulated into Counters::cycles.
@@ -167,6 +174,88 @@ __device__ __forceinline__ bool compat_vm(bool vehicle_fixed, bool rotary_only) 
   return !(vehicle_fixed && rotary_only);
 }
 
+// bits [0, n) of a word, n clamped to [0, 32]
+__device__ __forceinline__ uint32_t prefix_bits(long long n) {
+  return n <= 0 ? 0u : (n >= 32 ? FULL : ((1u << n) - 1u));
+}
+
+// imp[g] bit of position q (mission j): reassigning / taking it over to g
+// lowers its cost (proj/src/search.cpp:82-101, 131-148 preconditions + sign).
+__device__ __forceinline__ bool imp_bit(const Scenario& s, int g, int q, int j) {
+  return s.mvp[q] != g && compat_vm(s.vfixed[g], s.rop[q]) &&
+         cost_at(s, s.vbase[g], j) < s.mcp[q];
+}
+
+__device__ __forceinline__ void put_bit(uint32_t* w, uint32_t bit, bool on) {
+  *w = on ? (*w | bit) : (*w & ~bit);
+}
+
+// After mission j at position q moved from `loser` to `gain` (new cost in
+// mcp[q]): refresh bit q of every imp row, move its mem bit. Block-wide.
+template <int NT>
+__device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Smem& sm, int q,
+                                        int j, int loser, int gain) {
+  const int wd = q >> 5;
+  const uint32_t bit = 1u << (q & 31);
+  for (int g = threadIdx.x; g < s.V; g += NT) {
+    uint32_t* wp = s.imp + (long long)g * s.nwd + wd;
+    const bool was = (*wp & bit) != 0u, now = imp_bit(s, g, q, j);
+    put_bit(wp, bit, now);
+    sm.impc[g] += (int)now - (int)was;
+  }
+  if (threadIdx.x == 0 && loser != gain) {
+    s.mem[(long long)loser * s.nwd + wd] &= ~bit;
+    s.mem[(long long)gain * s.nwd + wd] |= bit;
+  }
+  __syncthreads();
+}
+
+// After vehicle x moved to a new base (its missions' costs already updated):
+// its own imp row in full (warp per word, lane per position), and the bits of
+// the positions it serves in every other row (thread per word). Block-wide.
+template <int NT>
+__device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem& sm, int x) {
+  constexpr int NW = NT / 32;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nwd = s.nwd, M = s.M;
+  const double* colx = s.cost + (long long)s.vbase[x] * M;
+  const bool fx = s.vfixed[x];
+  if (threadIdx.x == 0) sh.tmp = 0;
+  __syncthreads();
+  for (int wd = w; wd < nwd; wd += NW) {
+    const int q = wd * 32 + l;
+    bool b = false;
+    if (q < M) b = s.mvp[q] != x && compat_vm(fx, s.rop[q]) && colx[sm.pb[q]] < s.mcp[q];
+    const unsigned m = __ballot_sync(FULL, b);
+    if (l == 0) {
+      s.imp[(long long)x * nwd + wd] = m;
+      atomicAdd(&sh.tmp, __popc(m));
+    }
+  }
+  for (int wd = threadIdx.x; wd < nwd; wd += NT) {
+    uint32_t mx = s.mem[(long long)x * nwd + wd];
+    while (mx) {
+      const int bn = __ffs(mx) - 1;
+      mx &= mx - 1;
+      const int q = wd * 32 + bn;
+      const int j = sm.pb[q];
+      const double mcq = s.mcp[q];
+      const bool ro = s.rop[q];
+      for (int g = 0; g < s.V; ++g) {
+        if (g == x) continue;
+        uint32_t* wp = s.imp + (long long)g * nwd + wd;
+        const bool was = (*wp & (1u << bn)) != 0u;
+        const bool now = compat_vm(s.vfixed[g], ro) && cost_at(s, s.vbase[g], j) < mcq;
+        put_bit(wp, 1u << bn, now);
+        if (now != was) atomicAdd(&sm.impc[g], now ? 1 : -1);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sm.impc[x] = sh.tmp;
+  __syncthreads();
+}
+
 // Relocation classes of every vehicle towards empty base t, into sm.cls,
 // through the (t, version) cache. The per-vehicle sums use warp-private
 // accumulators: lanes of a warp holding the same vehicle are grouped with
@@ -220,6 +309,7 @@ __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm
   __syncthreads();
   const double bt = single_bound(s, sh);
   const bool heli = s.bheli[t];
+  int any = 0;
   for (int v = threadIdx.x; v < V; v += NT) {
     double sum = 0.0, abs = 0.0;
     for (int k = 0; k < NW; ++k) {
@@ -229,9 +319,13 @@ __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm
     const uint8_t c = (s.vfixed[v] && heli) ? CLS_POS : reloc_class(sum, abs, s.vcount[v], bt);
     sm.cls[v] = c;
     s.cls_cache[(long long)t * V + v] = c;
+    any |= c != CLS_POS;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) s.cls_ver[t] = ver;
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) {
+    s.cls_ver[t] = ver;
+    s.cls_any[t] = any ? 1 : 0;
+  }
   PH_ADD(sh, 5, r0);
 }
 
@@ -322,12 +416,14 @@ __device__ void debug_check(const Scenario& s, Shared& sh) {
 // Processes the pair (i, j) exactly as try_move x3 (proj/src/search.cpp:277-303,
 // 333-341). Block-cooperative; returns with the block synchronised.
 template <int NT>
-__device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int i, int j,
+__device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int i, int q,
                              bool tabu, long long tenure, bool debug) {
+  const int j = sm.pb[q];
   const long long exp = sh.c.tick + tenure;
-  // ---- takeover
+  // ---- takeover (thread 0 decides and applies)
   if (threadIdx.x == 0) {
     sh.c.evaluations += 1;
+    sh.bi[4] = 0;
     if (i < sh.c.psize && s.pkind[i] == POOL_IDLE) {
       const int g = s.pidx[i];
       if (compat_vm(s.vfixed[g], s.ro[j])) {
@@ -342,6 +438,9 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
             PH_ADD(sh, 4, f0);
           }
           if (acc) {
+            sh.bi[4] = 1;
+            sh.bi[5] = s.mv[j];
+            sh.bi[6] = g;
             apply_takeover(s, sh, j, g, i);
             sh.c.applied += 1;
             sh.c.pass_applied += 1;
@@ -351,7 +450,11 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         }
       }
     }
-    // relocation preconditions (on the state the takeover left)
+  }
+  __syncthreads();
+  if (sh.bi[4]) bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
+  // relocation preconditions (on the state the takeover left)
+  if (threadIdx.x == 0) {
     sh.c.evaluations += 1;
     int t = -1, mover = -1;
     if (i < sh.c.psize && s.pkind[i] == POOL_EMPTY) {
@@ -382,6 +485,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
     __syncthreads();
     if (sh.bi[2]) {
       apply_relocate<NT>(s, sh, mover, t, i);
+      bits_after_relocation<NT>(s, sh, sm, mover);
       if (threadIdx.x == 0) {
         sh.c.applied += 1;
         sh.c.pass_applied += 1;
@@ -393,6 +497,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           s.role_rel[ko] = ROLE_OUTER;
           s.exp_rel[ki] = exp;
           s.role_rel[ki] = ROLE_INNER;
+          sh.jexp_max = max(sh.jexp_max, exp);
         }
         if (debug) debug_check(s, sh);
       }
@@ -401,6 +506,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
   // ---- reassignment
   if (threadIdx.x == 0) {
     sh.c.evaluations += 1;
+    sh.bi[4] = 0;
     const int g = s.mv[i], l = s.mv[j];
     if (g != l && compat_vm(s.vfixed[g], s.ro[j])) {
       const double newc = cost_at(s, s.vbase[g], j);
@@ -414,6 +520,9 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           PH_ADD(sh, 4, f0);
         }
         if (acc) {
+          sh.bi[4] = 1;
+          sh.bi[5] = l;
+          sh.bi[6] = g;
           apply_reassign(s, sh, j, g);
           sh.c.applied += 1;
           sh.c.pass_applied += 1;
@@ -425,6 +534,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
     sh.c.tick += 1;
   }
   __syncthreads();
+  if (sh.bi[4]) bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
 }
 
 // Row context after any state change (thread 0 writes, all read after sync).
@@ -479,6 +589,27 @@ __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int 
       sm.lim_j[v] = clamp_lim(s.exp_rel[k] - T, s.M);
       sm.outer_j[v] = s.role_rel[k] == ROLE_OUTER;
     }
+    __syncthreads();
+    // compact the vehicles whose j-key is live (usually none or a few)
+    if (threadIdx.x < 32) {
+      const int l = threadIdx.x;
+      int n = 0;
+      for (int v0 = 0; v0 < s.V; v0 += 32) {
+        const int v = v0 + l;
+        const bool live = v < s.V && sm.lim_j[v] > 0;
+        const unsigned m = __ballot_sync(FULL, live);
+        if (live) {
+          const int k = n + __popc(m & ((1u << l) - 1u));
+          sm.jl_v[k] = v;
+          sm.jl_lim[k] = sm.lim_j[v];
+          sm.jl_outer[k] = sm.outer_j[v];
+        }
+        n += __popc(m);
+      }
+      if (l == 0) sh.nj = n;
+    }
+  } else if (threadIdx.x == 0) {
+    sh.nj = 0;
   }
   const int t = sh.rel_t;
   if (t >= 0) relocation_classes<NT>(s, sh, sm, t);
@@ -486,11 +617,20 @@ __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int 
 }
 
 // One outer-index row, proj/src/search.cpp:307-346.
+//
+// Scan step: the block covers 32*NW words (32 positions each) from the
+// current position. Per word (one lane): candidates = imp[gain of the row]
+// | imp[idle pool vehicle] | relocation mask; blocked = row-key prefix |
+// the positions of vehicles whose j-key is live (mem rows, within their live
+// windows); outer = row outer prefix | outer j-key positions. The first event
+// is the first set bit of outer | (candidates & ~blocked); the positions
+// before it are either inner-blocked (tick + skip) or evaluated (3
+// evaluations each), counted with popc.
 template <int NT>
-__device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i,
-                        const int32_t* __restrict__ pb, bool tabu, long long tenure, bool debug) {
+__device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bool tabu,
+                        long long tenure, bool debug) {
   constexpr int NW = NT / 32;
-  const int M = s.M;
+  const int M = s.M, nwd = s.nwd;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   int p = 0;
   if (threadIdx.x == 0) sh.c.counts[0] += 1;
@@ -500,130 +640,103 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i,
     PH_ADD(sh, 1, c0);
     const long long c1 = ph_now();
     const int p_seg = p;
-    const int gain_r = sh.gain_r, col_r = sh.col_r, fixed_r = sh.fixed_r;
-    const int gain_t = sh.gain_t, col_t = sh.col_t, fixed_t = sh.fixed_t;
-    const int rel_t = sh.rel_t;
-    const int lim_ro = sh.lim_ro, lim_ra = sh.lim_ra;
-    const double* colr = s.cost + (long long)col_r * M;
-    const double* colt = s.cost + (long long)(gain_t >= 0 ? col_t : 0) * M;
+    const int gain_r = sh.gain_r, gain_t = sh.gain_t, rel_t = sh.rel_t;
+    const int lim_ro = sh.lim_ro, lim_ra = sh.lim_ra, nj = sh.nj;
+    const uint32_t* imp_r = s.imp + (long long)gain_r * nwd;
+    const uint32_t* imp_t = s.imp + (long long)(gain_t >= 0 ? gain_t : 0) * nwd;
     int ev = INT_MAX;
     while (p < M) {
-      // ---- issue every load of the chunk first
-      int vq[U], jq[U];
-      double mq[U];
-      bool rq[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int q = p + k * NT + threadIdx.x;
-        vq[k] = 0;
-        jq[k] = 0;
-        mq[k] = 0.0;
-        rq[k] = false;
-        if (q < M) {
-          vq[k] = s.mvp[q];
-          jq[k] = pb[q];
-          mq[k] = s.mcp[q];
-          rq[k] = s.rop[q];
+      const int w0 = p >> 5;
+      const int wd = w0 + w * 32 + l;
+      const long long base = (long long)wd * 32;
+      uint32_t relw = 0;
+      if (rel_t >= 0) {
+        // relocation candidates need the vehicle of every position: one
+        // coalesced pass over the warp's 32 words, lane = position
+        for (int k = 0; k < 32; ++k) {
+          const long long q = (long long)(w0 + w * 32 + k) * 32 + l;
+          bool b = false;
+          if (q < M && q >= p) b = sm.cls[s.mvp[q]] != CLS_POS;
+          const unsigned m = __ballot_sync(FULL, b);
+          if (l == k) relw = m;
         }
       }
-      double cr[U], ct[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int q = p + k * NT + threadIdx.x;
-        cr[k] = q < M ? colr[jq[k]] : 0.0;
-        ct[k] = (q < M && gain_t >= 0) ? colt[jq[k]] : 0.0;
-      }
-      // ---- classify: bit k of ev/in/un
-      unsigned evb = 0, inb = 0, unb = 0;
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const int q = p + k * NT + threadIdx.x;
-        if (q >= M) continue;
-        const int v = vq[k];
+      uint32_t valid = 0, evw = 0, blk = 0;
+      if (wd < nwd) {
+        valid = prefix_bits(M - base) & ~prefix_bits(p - base);
+        uint32_t cand = imp_r[wd] | relw;
+        if (gain_t >= 0) cand |= imp_t[wd];
+        uint32_t outer = 0;
         if (tabu) {
-          const int off = q - p_seg;
-          const int lj = sm.lim_j[v];
-          if (off < lim_ro || (off < lj && sm.outer_j[v])) {
-            evb |= 1u << k;
-            continue;
+          outer = prefix_bits(p_seg + lim_ro - base);
+          blk = prefix_bits(p_seg + lim_ra - base);
+          for (int k = 0; k < nj; ++k) {
+            const uint32_t m =
+                s.mem[(long long)sm.jl_v[k] * nwd + wd] & prefix_bits(p_seg + sm.jl_lim[k] - base);
+            blk |= m;
+            if (sm.jl_outer[k]) outer |= m;
           }
-          if (off < lim_ra || off < lj) {
-            inb |= 1u << k;
-            continue;
-          }
+          outer &= valid;
+          blk = (blk | outer) & valid;
         }
-        bool e = false;
-        if (gain_t >= 0 && compat_vm(fixed_t, rq[k])) e |= ct[k] < mq[k];
-        if (rel_t >= 0) e |= sm.cls[v] != CLS_POS;
-        if (v != gain_r && compat_vm(fixed_r, rq[k])) e |= cr[k] < mq[k];
-        if (e)
-          evb |= 1u << k;
-        else
-          unb |= 1u << k;
+        evw = outer | (cand & ~blk & valid);
       }
-      // ---- one block reduction: first event + counts before it
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const unsigned a = __ballot_sync(FULL, (evb >> k) & 1u);
-        const unsigned b = __ballot_sync(FULL, (inb >> k) & 1u);
-        const unsigned c = __ballot_sync(FULL, (unb >> k) & 1u);
-        if (l == 0) {
-          sm.masks[(k * NW + w) * 3 + 0] = a;
-          sm.masks[(k * NW + w) * 3 + 1] = b;
-          sm.masks[(k * NW + w) * 3 + 2] = c;
+      // warp: first event and the counts before it
+      const unsigned evl = __ballot_sync(FULL, evw != 0u);
+      int n_valid, n_blk, evpos = INT_MAX;
+      if (evl) {
+        const int f = __ffs(evl) - 1;
+        if (l < f) {
+          n_valid = __popc(valid);
+          n_blk = __popc(blk);
+        } else if (l == f) {
+          const int bn = __ffs(evw) - 1;
+          const uint32_t below = (1u << bn) - 1u;
+          n_valid = __popc(valid & below);
+          n_blk = __popc(blk & below);
+          evpos = (int)(base + bn);
+        } else {
+          n_valid = 0;
+          n_blk = 0;
         }
+      } else {
+        n_valid = __popc(valid);
+        n_blk = __popc(blk);
+      }
+      n_valid = (int)__reduce_add_sync(FULL, (unsigned)n_valid);
+      n_blk = (int)__reduce_add_sync(FULL, (unsigned)n_blk);
+      evpos = __reduce_min_sync(FULL, evpos);
+      if (l == 0) {
+        sm.wsum[w * 3 + 0] = evpos;
+        sm.wsum[w * 3 + 1] = n_valid;
+        sm.wsum[w * 3 + 2] = n_blk;
       }
       __syncthreads();
       if (w == 0) {
-        // lane l summarises warp l's masks
-        unsigned me[U], mi[U], mu[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          me[k] = l < NW ? sm.masks[(k * NW + l) * 3 + 0] : 0u;
-          mi[k] = l < NW ? sm.masks[(k * NW + l) * 3 + 1] : 0u;
-          mu[k] = l < NW ? sm.masks[(k * NW + l) * 3 + 2] : 0u;
+        const int e = l < NW ? sm.wsum[l * 3 + 0] : INT_MAX;
+        int nv = l < NW ? sm.wsum[l * 3 + 1] : 0;
+        int nb = l < NW ? sm.wsum[l * 3 + 2] : 0;
+        const unsigned any = __ballot_sync(FULL, e != INT_MAX);
+        const int wstar = any ? __ffs(any) - 1 : 32;
+        if (l > wstar) {
+          nv = 0;
+          nb = 0;
         }
-        int kstar = U, wstar = 32;
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const unsigned any = __ballot_sync(FULL, me[k] != 0u);
-          if (kstar == U && any) {
-            kstar = k;
-            wstar = __ffs(any) - 1;
-          }
-        }
-        int n_in = 0, n_un = 0;
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          unsigned keep = 0u;
-          if (k < kstar) keep = FULL;
-          else if (k == kstar) {
-            if (l < wstar) keep = FULL;
-            else if (l == wstar) keep = (1u << (__ffs(me[k]) - 1)) - 1u;
-          }
-          n_in += __popc(mi[k] & keep);
-          n_un += __popc(mu[k] & keep);
-        }
-        n_in = (int)__reduce_add_sync(FULL, (unsigned)n_in);
-        n_un = (int)__reduce_add_sync(FULL, (unsigned)n_un);
-        int evp = INT_MAX;
-        if (kstar < U) {
-          const unsigned wm = __shfl_sync(FULL, me[kstar < U ? kstar : 0], wstar);
-          evp = p + kstar * NT + wstar * 32 + (__ffs(wm) - 1);
-        }
+        nv = (int)__reduce_add_sync(FULL, (unsigned)nv);
+        nb = (int)__reduce_add_sync(FULL, (unsigned)nb);
+        const int evp = any ? __shfl_sync(FULL, e, wstar) : INT_MAX;
         if (l == 0) {
-          const int stop = min(evp, min(p + NT * U, M));
           sh.ev = evp;
           sh.c.counts[1] += 1;
-          sh.c.skips_inner += (unsigned long long)n_in;
-          sh.c.evaluations += 3ull * (unsigned long long)n_un;
-          if (tabu) sh.c.tick += stop - p;
-          if (n_in > 0) sh.c.pass_skipped = 1;
+          sh.c.skips_inner += (unsigned long long)nb;
+          sh.c.evaluations += 3ull * (unsigned long long)(nv - nb);
+          if (tabu) sh.c.tick += nv;  // every position before the event is one pair
+          if (nb > 0) sh.c.pass_skipped = 1;
         }
       }
       __syncthreads();
       ev = sh.ev;
-      p = min(ev, min(p + NT * U, M));
+      p = ev != INT_MAX ? ev : (int)min((long long)M, (long long)(w0 + 32 * NW) * 32);
       if (ev != INT_MAX) break;
     }
     PH_ADD(sh, 2, c1);
@@ -645,7 +758,7 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i,
       return;
     }
     const long long c2 = ph_now();
-    process_pair<NT>(s, sh, sm, i, pb[p], tabu, tenure, debug);
+    process_pair<NT>(s, sh, sm, i, p, tabu, tenure, debug);
     PH_ADD(sh, 3, c2);
     if (sh.c.error) return;
     p += 1;
@@ -656,17 +769,41 @@ __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) &
 
 }  // namespace
 
-// Rebuild the perm_b-ordered mirrors for a new pass.
-__global__ void mirror_kernel(Scenario* scs, const int32_t* __restrict__ active,
-                              const int32_t* __restrict__ pb) {
+// Per pass: the perm_b-ordered mirrors and the imp/mem bitsets, warp per
+// word, lane per position (the neighbourhood sweep: every occupied vehicle's
+// base column is gathered once, V*M table reads). grid = (words, scenarios).
+__global__ void __launch_bounds__(256) prep_kernel(Scenario* scs, const int32_t* __restrict__ active,
+                                                   const int32_t* __restrict__ pb) {
   if (!active[blockIdx.y]) return;
   const Scenario s = scs[blockIdx.y];
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < s.M; q += gridDim.x * blockDim.x) {
-    const int j = pb[q];
-    s.mvp[q] = s.mv[j];
-    s.mcp[q] = s.mc[j];
-    s.rop[q] = s.ro[j];
-    s.invb[j] = q;
+  const int l = threadIdx.x & 31;
+  const int warps = blockDim.x >> 5;
+  for (int wd = blockIdx.x * warps + (threadIdx.x >> 5); wd < s.nwd; wd += gridDim.x * warps) {
+    const int q = wd * 32 + l;
+    const bool valid = q < s.M;
+    int j = 0, v = -1;
+    double mcq = 0.0;
+    bool ro = false;
+    if (valid) {
+      j = pb[q];
+      v = s.mv[j];
+      mcq = s.mc[j];
+      ro = s.ro[j];
+      s.mvp[q] = v;
+      s.mcp[q] = mcq;
+      s.rop[q] = ro;
+      s.invb[j] = q;
+    }
+    for (int g = 0; g < s.V; ++g) {
+      const bool b = valid && v != g && compat_vm(s.vfixed[g], ro) &&
+                     s.cost[(long long)s.vbase[g] * s.M + j] < mcq;
+      const unsigned m = __ballot_sync(FULL, b);
+      const unsigned mm = __ballot_sync(FULL, v == g);
+      if (l == 0) {
+        s.imp[(long long)g * s.nwd + wd] = m;
+        s.mem[(long long)g * s.nwd + wd] = mm;
+      }
+    }
   }
 }
 
@@ -675,7 +812,8 @@ __global__ void mirror_kernel(Scenario* scs, const int32_t* __restrict__ active,
 size_t pass_smem_core(int V, int NT) {
   const int NW = NT / 32;
   return align16(4ull * V) + align16(V) + align16(V) + 2 * align16(8ull * NW * V) +
-         align16(8ull * NW * 32) + align16(4ull * U * NW * 3) + 64;
+         align16(8ull * NW * 32) + align16(4ull * NW * 3) + 3 * align16(4ull * V) + align16(V) +
+         64;
 }
 size_t pass_smem_state(int V, int B, int K) {
   return align16(8ull * V) * 2 + align16(8ull * K) + align16(K) + align16(4ull * V) * 3 +
@@ -709,7 +847,12 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
   sm.acc_sum = reinterpret_cast<double*>(take(8ull * NW * V));
   sm.acc_abs = reinterpret_cast<double*>(take(8ull * NW * V));
   sm.stage = reinterpret_cast<double*>(take(8ull * NW * 32));
-  sm.masks = reinterpret_cast<unsigned*>(take(4ull * U * NW * 3));
+  sm.wsum = reinterpret_cast<int*>(take(4ull * NW * 3));
+  sm.jl_v = reinterpret_cast<int*>(take(4ull * V));
+  sm.jl_lim = reinterpret_cast<int*>(take(4ull * V));
+  sm.jl_outer = take(V);
+  sm.impc = reinterpret_cast<int*>(take(4ull * V));
+  sm.pb = pb;
   if (state_in_smem) {
     // the small mutable state lives in shared memory for the whole pass
     s.exp_take = reinterpret_cast<long long*>(take(8ull * V));
@@ -747,6 +890,22 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
     sh.c = *s.ctr;
     sh.c.pass_applied = 0;
     sh.c.pass_skipped = 0;
+    sh.jexp_max = LLONG_MIN;
+  }
+  __syncthreads();
+  {
+    // imp row popcounts (warp per vehicle) and the latest vehicle j-key expiry
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    for (int v = w; v < V; v += NW) {
+      int c = 0;
+      for (int wd = l; wd < s.nwd; wd += 32) c += __popc(s.imp[(long long)v * s.nwd + wd]);
+      c = (int)__reduce_add_sync(FULL, (unsigned)c);
+      if (l == 0) sm.impc[v] = c;
+    }
+    long long e = LLONG_MIN;
+    for (int v = threadIdx.x; v < V; v += NT) e = max(e, s.exp_rel[s.vrk[v]]);
+    for (int o = 16; o > 0; o >>= 1) e = max(e, __shfl_xor_sync(FULL, e, o));
+    if (l == 0) atomicMax(&sh.jexp_max, e);
   }
   __syncthreads();
   const int M = s.M;
@@ -786,7 +945,36 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
       PH_ADD(sh, 0, b0);
       if (found == INT_MAX) continue;
     }
-    run_row<NT>(s, sh, sm, pa[r], pb, tabu, tenure, debug);
+    // O(1) eventless row: no live key can block or end it and no move from
+    // its outer index improves any mission, so all M pairs are evaluated
+    // and nothing else happens (3 evaluations and one tick per pair).
+    if (threadIdx.x == 0) {
+      const int i = pa[r];
+      const long long T = sh.c.tick;
+      const int g0 = s.mv[i];
+      bool ok = sm.impc[g0] == 0 && (!tabu || (s.exp_reas[g0] <= T && sh.jexp_max <= T));
+      if (ok && i < sh.c.psize) {
+        const int x = s.pidx[i];
+        if (s.pkind[i] == POOL_IDLE) {
+          ok = sm.impc[x] == 0 && (!tabu || s.exp_take[x] <= T);
+        } else {
+          ok = s.cls_ver[x] == (long long)sh.c.applied && s.cls_any[x] == 0 &&
+               (!tabu || s.exp_rel[s.brk[x]] <= T);
+        }
+      }
+      if (ok) {
+        sh.c.evaluations += 3ull * (unsigned long long)M;
+        if (tabu) sh.c.tick += M;
+        sh.c.counts[4] += 1;
+      }
+      sh.bi[7] = ok;
+    }
+    __syncthreads();
+    if (sh.bi[7]) {
+      r += 1;
+      continue;
+    }
+    run_row<NT>(s, sh, sm, pa[r], tabu, tenure, debug);
     __syncthreads();
     r += 1;
   }
@@ -851,8 +1039,9 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn, const int32_t* d_pa,
                         const int32_t* d_pb, int M, bool tabu, long long tenure, bool debug, int V,
                         int B, int K, cudaStream_t stream, int threads) {
-  dim3 mg((M + 255) / 256 < 64 ? (M + 255) / 256 : 64, n_scn);
-  if (M > 0) mirror_kernel<<<mg, 256, 0, stream>>>(d_scs, d_active, d_pb);
+  const int nwd = (M + 31) / 32;
+  dim3 mg((nwd + 7) / 8 < 1184 ? (nwd + 7) / 8 : 1184, n_scn);
+  if (M > 0) prep_kernel<<<mg, 256, 0, stream>>>(d_scs, d_active, d_pb);
   if (threads == 1024)
     return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_pa, d_pb, tabu, tenure, debug, V, B, K,
                                 stream);

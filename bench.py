@@ -126,7 +126,9 @@ def run_ours(args) -> None:
         dist.barrier()
     torch.cuda.synchronize()
     clk = Clocks(local)
+    launches0 = t._ctx.launches()
     results = [step() for _ in range(args.steps)]
+    launches = t._ctx.launches() - launches0
     torch.cuda.synchronize()
     clocks = clk.stop()
     dev_ms = [r.stats.device_ms for r in results]
@@ -184,8 +186,8 @@ def run_ours(args) -> None:
                      "frac": achieved / peak, "traffic": None, "kernel": "pass_kernel<1024>",
                      "peak_source": peak_kind,
                      "note": "serial first-improvement automaton: latency-bound, see DESIGN.md"},
-        # init + (mirror + pass) per pass + final, per timed step
-        "gpu_launches": int(args.steps * (2 * st.passes + 2)),
+        # our kernels launched inside the timed region (library counter)
+        "gpu_launches": int(launches),
         "clocks": clocks,
     }
     if rank == 0 and not args.no_cpu_baseline:

@@ -298,7 +298,6 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
     o = align_up(o + bytes);
     return at;
   };
-  L.ctr = put(sizeof(fpk::Counters));
   L.ro = put(M);
   L.vfixed = put(V);
   L.bheli = put(B);
@@ -336,6 +335,7 @@ struct SearchRun {
   DBuf<fpk::Scenario> d_scs;
   DBuf<int32_t> d_active;
   DBuf<int32_t> d_perm;  // [2*M]
+  DBuf<fpk::Counters> d_ctr;  // [n], contiguous: one copy per pass
   std::vector<Layout> lay;
 };
 
@@ -375,6 +375,12 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     total += run.lay[s].total;
   }
   run.arena.mem.alloc(std::max<size_t>(total, 256));
+  run.d_ctr.alloc(n);
+  std::vector<fpk::Counters> ctrs(n);
+  for (int s = 0; s < n; ++s) {
+    ctrs[s] = fpk::Counters{};
+    ctrs[s].psize = run.hs[s].psize;
+  }
   unsigned char* d0 = run.arena.mem.p;
   std::vector<unsigned char> stage(total, 0);
   run.arena.scs.resize(n);
@@ -385,9 +391,6 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     const int V = in->n_vehicles, B = in->n_bases;
     unsigned char* hb = stage.data() + base[s];
     unsigned char* db = d0 + base[s];
-    fpk::Counters c{};
-    c.psize = h.psize;
-    std::memcpy(hb + L.ctr, &c, sizeof(c));
     if (M) std::memcpy(hb + L.ro, in->rotary_only, M);
     if (V) std::memcpy(hb + L.vfixed, h.vfixed.data(), V);
     if (B) std::memcpy(hb + L.bheli, h.bheli.data(), B);
@@ -430,7 +433,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.imp = reinterpret_cast<uint32_t*>(db + L.imp);
     S.mem = reinterpret_cast<uint32_t*>(db + L.mem);
     S.nwd = (M + 31) / 32;
-    S.ctr = reinterpret_cast<fpk::Counters*>(db + L.ctr);
+    S.ctr = run.d_ctr.p + s;
     S.M = M;
     S.B = B;
     S.V = V;
@@ -445,49 +448,55 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   run.d_scs.alloc(n);
   h2d(run.d_scs.p, run.arena.scs.data(), n, st);
   run.d_active.alloc(n);
-  run.d_perm.alloc(2ull * M + 2);
   std::vector<int32_t> active(n, 1);
-  std::vector<uint64_t> passes(n, 0);
-  std::vector<fpk::Counters> ctrs(n);
-  // pinned perm staging
-  if (ctx->perm_cap < 2ull * M + 2) {
+  h2d(run.d_ctr.p, ctrs.data(), n, st);
+  // Small scenarios run many passes per launch, each block rebuilding its
+  // own mirrors/bitsets between passes (scenarios of a batch progress
+  // independently); large ones run one pass per launch after the grid-wide
+  // sweep. Permutations for a chunk of passes are generated on the host
+  // while the device runs the previous chunk.
+  const bool inkernel = n > 1 || (long long)maxV * M <= (64ll << 10);
+  int kchunk = inkernel ? (int)std::max<long long>(1, std::min<long long>(64, (16ll << 20) / (8ll * std::max(M, 1)))) : 1;
+  if (const char* e = std::getenv("FLEETPLACE_KPASSES")) kchunk = std::max(1, std::atoi(e));
+  const size_t chunk_ints = 2ull * kchunk * M + 2;
+  if (ctx->perm_cap < chunk_ints) {
     for (auto& p : ctx->h_perm)
       if (p) cudaFreeHost(p), p = nullptr;
-    for (auto& p : ctx->h_perm) check(cudaMallocHost(&p, sizeof(int32_t) * (2ull * M + 2)), "pinned");
-    ctx->perm_cap = 2ull * M + 2;
+    for (auto& p : ctx->h_perm) check(cudaMallocHost(&p, sizeof(int32_t) * chunk_ints), "pinned");
+    ctx->perm_cap = chunk_ints;
   }
+  run.d_perm.alloc(chunk_ints);
   check(fpk::launch_init(run.d_scs.p, n, st), "init_kernel");
   ctx->launches += 1;
   PermStream rng(cfg->seed);
+  auto gen_chunk = [&](int32_t* buf) {
+    for (int k = 0; k < kchunk; ++k) {
+      rng.perm(M, buf + 2ll * k * M);
+      rng.perm(M, buf + (2ll * k + 1) * M);
+    }
+  };
   int buf = 0;
-  rng.perm(M, ctx->h_perm[buf]);
-  rng.perm(M, ctx->h_perm[buf] + M);
+  gen_chunk(ctx->h_perm[buf]);
   int threads = n == 1 ? 512 : 256;
   if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
   int n_active = n;
   while (n_active > 0) {
     h2d(run.d_active.p, active.data(), n, st);
-    h2d(run.d_perm.p, ctx->h_perm[buf], 2ull * M, st);
-    check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p, run.d_perm.p + M, M, tabu,
-                           tenure, cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads),
+    h2d(run.d_perm.p, ctx->h_perm[buf], 2ull * kchunk * M, st);
+    check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p, kchunk, inkernel,
+                           cfg->max_passes, M, tabu, tenure, cfg->debug_check_deltas != 0, maxV,
+                           maxB, maxK, st, threads),
           "pass_kernel");
-    ctx->launches += M > 0 ? 2 : 1;
-    // next pass's permutations while the device works
+    ctx->launches += (M > 0 && !inkernel) ? 2 : 1;
+    // next chunk's permutations while the device works
     const int nb = buf ^ 1;
-    rng.perm(M, ctx->h_perm[nb]);
-    rng.perm(M, ctx->h_perm[nb] + M);
-    for (int s = 0; s < n; ++s)
-      if (active[s]) d2h(&ctrs[s], run.arena.scs[s].ctr, 1, st);
+    gen_chunk(ctx->h_perm[nb]);
+    d2h(ctrs.data(), run.d_ctr.p, n, st);
     check(cudaStreamSynchronize(st), "pass sync");
     buf = nb;
     for (int s = 0; s < n; ++s) {
       if (!active[s]) continue;
-      passes[s] += 1;
-      const fpk::Counters& c = ctrs[s];
-      const bool keep = c.error == 0 &&
-                        (c.pass_applied > 0 || (tabu && c.pass_skipped)) &&
-                        !(cfg->max_passes >= 0 && passes[s] >= (uint64_t)cfg->max_passes);
-      if (!keep) {
+      if (ctrs[s].done || ctrs[s].error) {
         active[s] = 0;
         --n_active;
       }
@@ -496,8 +505,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   check(fpk::launch_final(run.d_scs.p, n, st), "final_kernel");
   ctx->launches += 1;
   check(cudaEventRecord(ev1, st), "event");
+  d2h(ctrs.data(), run.d_ctr.p, n, st);
   for (int s = 0; s < n; ++s) {
-    d2h(&ctrs[s], run.arena.scs[s].ctr, 1, st);
     d2h(outs[s].vehicle_base, run.arena.scs[s].vbase, insts[s].n_vehicles, st);
     d2h(outs[s].mission_vehicle, run.arena.scs[s].mv, (size_t)M, st);
   }
@@ -514,7 +523,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       throw FpError(FP_ERR_LOGIC, "incremental objective drifted from recomputation");
     if (c.error) throw FpError((fp_status)c.error, "search failed");
     fp_search_stats& o = outs[s].stats;
-    o.passes = passes[s];
+    o.passes = (uint64_t)c.passes;
     o.evaluations = c.evaluations;
     o.applied_moves = c.applied;
     o.committed_moves = c.applied;

@@ -22,6 +22,8 @@ struct Counters {
   unsigned long long skips_outer;
   unsigned long long skips_inner;
   unsigned long long fallbacks;   // accept decisions settled by exact chains
+  long long passes;               // passes completed
+  int done;                       // search finished (quiescent, max_passes or error)
   int psize;                      // current pool size
   int pass_applied;               // moves applied in the current pass
   int pass_skipped;               // any tabu skip in the current pass

@@ -260,7 +260,8 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
 // through the (t, version) cache. The per-vehicle sums use warp-private
 // accumulators: lanes of a warp holding the same vehicle are grouped with
 // __match_any_sync and their leader adds the group's terms, so no shared
-// memory atomics are needed (fp64 shared atomics are CAS loops).
+// memory atomics are needed (fp64 shared atomics are CAS loops). Any
+// summation order is fine: the class uses a rigorous error bound.
 template <int NT>
 __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm, int t) {
   const long long ver = (long long)sh.c.applied;
@@ -283,28 +284,38 @@ __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm
   double* st = sm.stage + w * 32;
   __syncwarp();
   const double* col = s.cost + (long long)t * s.M;
-  for (int base = w * 32; base < s.M; base += NT) {
-    const int m = base + l;
-    int v = -1;
-    double d = 0.0;
-    if (m < s.M) {
-      v = s.mv[m];
-      d = col[m] - s.mc[m];
-    }
-    const unsigned peers = __match_any_sync(FULL, v);
-    st[l] = d;
-    __syncwarp();
-    if (v >= 0 && l == __ffs(peers) - 1) {
-      double sum = 0.0, abs = 0.0;
-      for (unsigned b = peers; b; b &= b - 1) {
-        const double x = st[__ffs(b) - 1];
-        sum += x;
-        abs += fabs(x);
+  constexpr int UR = 4;  // independent 32-mission groups in flight per warp
+  for (int base = w * 32; base < s.M; base += UR * NT) {
+    int vv[UR];
+    double dd[UR];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const int m = base + u * NT + l;
+      vv[u] = -1;
+      dd[u] = 0.0;
+      if (m < s.M) {
+        vv[u] = s.mv[m];
+        dd[u] = col[m] - s.mc[m];
       }
-      as[v] += sum;
-      aa[v] += abs;
     }
-    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const int v = vv[u];
+      const unsigned peers = __match_any_sync(FULL, v);
+      st[l] = dd[u];
+      __syncwarp();
+      if (v >= 0 && l == __ffs(peers) - 1) {
+        double sum = 0.0, abs = 0.0;
+        for (unsigned b = peers; b; b &= b - 1) {
+          const double x = st[__ffs(b) - 1];
+          sum += x;
+          abs += fabs(x);
+        }
+        as[v] += sum;
+        aa[v] += abs;
+      }
+      __syncwarp();
+    }
   }
   __syncthreads();
   const double bt = single_bound(s, sh);
@@ -771,14 +782,11 @@ __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) &
 
 // Per pass: the perm_b-ordered mirrors and the imp/mem bitsets, warp per
 // word, lane per position (the neighbourhood sweep: every occupied vehicle's
-// base column is gathered once, V*M table reads). grid = (words, scenarios).
-__global__ void __launch_bounds__(256) prep_kernel(Scenario* scs, const int32_t* __restrict__ active,
-                                                   const int32_t* __restrict__ pb) {
-  if (!active[blockIdx.y]) return;
-  const Scenario s = scs[blockIdx.y];
+// base column is gathered once, V*M table reads). Four vehicles' gathers are
+// kept in flight per lane.
+__device__ void prep_words(const Scenario& s, const int32_t* __restrict__ pb, int wd0, int wstride) {
   const int l = threadIdx.x & 31;
-  const int warps = blockDim.x >> 5;
-  for (int wd = blockIdx.x * warps + (threadIdx.x >> 5); wd < s.nwd; wd += gridDim.x * warps) {
+  for (int wd = wd0; wd < s.nwd; wd += wstride) {
     const int q = wd * 32 + l;
     const bool valid = q < s.M;
     int j = 0, v = -1;
@@ -794,17 +802,36 @@ __global__ void __launch_bounds__(256) prep_kernel(Scenario* scs, const int32_t*
       s.rop[q] = ro;
       s.invb[j] = q;
     }
-    for (int g = 0; g < s.V; ++g) {
-      const bool b = valid && v != g && compat_vm(s.vfixed[g], ro) &&
-                     s.cost[(long long)s.vbase[g] * s.M + j] < mcq;
-      const unsigned m = __ballot_sync(FULL, b);
-      const unsigned mm = __ballot_sync(FULL, v == g);
-      if (l == 0) {
-        s.imp[(long long)g * s.nwd + wd] = m;
-        s.mem[(long long)g * s.nwd + wd] = mm;
+    for (int g0 = 0; g0 < s.V; g0 += 4) {
+      double c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int g = g0 + u;
+        c[u] = (valid && g < s.V) ? s.cost[(long long)s.vbase[g] * s.M + j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int g = g0 + u;
+        if (g >= s.V) break;
+        const bool b = valid && v != g && compat_vm(s.vfixed[g], ro) && c[u] < mcq;
+        const unsigned m = __ballot_sync(FULL, b);
+        const unsigned mm = __ballot_sync(FULL, v == g);
+        if (l == 0) {
+          s.imp[(long long)g * s.nwd + wd] = m;
+          s.mem[(long long)g * s.nwd + wd] = mm;
+        }
       }
     }
   }
+}
+
+// grid = (words, scenarios): the sweep for large scenarios, one launch per pass.
+__global__ void __launch_bounds__(256) prep_kernel(Scenario* scs, const int32_t* __restrict__ active,
+                                                   const int32_t* __restrict__ pb) {
+  if (!active[blockIdx.y]) return;
+  const Scenario s = scs[blockIdx.y];
+  const int warps = blockDim.x >> 5;
+  prep_words(s, pb, blockIdx.x * warps + (threadIdx.x >> 5), gridDim.x * warps);
 }
 
 // Shared-memory bytes of the always-resident part and of the optional copy
@@ -823,9 +850,9 @@ size_t pass_smem_state(int V, int B, int K) {
 // One pass over perm_a for every active scenario (blockIdx.x = scenario).
 template <int NT>
 __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
-    pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ pa,
-                const int32_t* __restrict__ pb, int tabu_i, long long tenure, int debug_i,
-                int state_in_smem) {
+    pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
+                int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
+                int debug_i, int state_in_smem) {
   if (!active[blockIdx.x]) return;
   const Scenario g = scs[blockIdx.x];
   Scenario s = g;
@@ -852,7 +879,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
   sm.jl_lim = reinterpret_cast<int*>(take(4ull * V));
   sm.jl_outer = take(V);
   sm.impc = reinterpret_cast<int*>(take(4ull * V));
-  sm.pb = pb;
+  sm.pb = perms + s.M;
   if (state_in_smem) {
     // the small mutable state lives in shared memory for the whole pass
     s.exp_take = reinterpret_cast<long long*>(take(8ull * V));
@@ -888,20 +915,12 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
   }
   if (threadIdx.x == 0) {
     sh.c = *s.ctr;
-    sh.c.pass_applied = 0;
-    sh.c.pass_skipped = 0;
     sh.jexp_max = LLONG_MIN;
   }
   __syncthreads();
   {
-    // imp row popcounts (warp per vehicle) and the latest vehicle j-key expiry
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    for (int v = w; v < V; v += NW) {
-      int c = 0;
-      for (int wd = l; wd < s.nwd; wd += 32) c += __popc(s.imp[(long long)v * s.nwd + wd]);
-      c = (int)__reduce_add_sync(FULL, (unsigned)c);
-      if (l == 0) sm.impc[v] = c;
-    }
+    // latest vehicle j-key expiry (maintained on inserts afterwards)
+    const int l = threadIdx.x & 31;
     long long e = LLONG_MIN;
     for (int v = threadIdx.x; v < V; v += NT) e = max(e, s.exp_rel[s.vrk[v]]);
     for (int o = 16; o > 0; o >>= 1) e = max(e, __shfl_xor_sync(FULL, e, o));
@@ -909,74 +928,113 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
   }
   __syncthreads();
   const int M = s.M;
-  int r = 0;
-  while (r < M && !sh.c.error) {
-    const long long b0 = ph_now();
-    if (tabu) {
-      // rows r .. r+NT-1: outer-blocked at p = 0 if every earlier one was?
+  for (int kp = 0; kp < kpasses && !sh.c.done; ++kp) {
+    const int32_t* pa = perms + 2ll * kp * M;
+    sm.pb = pa + M;
+    if (inkernel_prep) {
+      prep_words(s, sm.pb, threadIdx.x >> 5, NW);
+      __syncthreads();
+    }
+    {
+      // imp row popcounts (warp per vehicle)
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+      for (int v = w; v < V; v += NW) {
+        int c = 0;
+        for (int wd = l; wd < s.nwd; wd += 32) c += __popc(s.imp[(long long)v * s.nwd + wd]);
+        c = (int)__reduce_add_sync(FULL, (unsigned)c);
+        if (l == 0) sm.impc[v] = c;
+      }
+    }
+    if (threadIdx.x == 0) {
+      sh.c.pass_applied = 0;
+      sh.c.pass_skipped = 0;
+    }
+    __syncthreads();
+      int r = 0;
+    while (r < M && !sh.c.error) {
+      const long long b0 = ph_now();
+      // Classify the next NT rows at the current tick T (thread d: row r+d):
+      //  S: no move from its outer index can improve any mission (imp rows
+      //     empty, relocation classes all POS) -- tick independent;
+      //  F: latest expiry of any key that could touch the row (row keys and
+      //     every vehicle's {Relocate, id} j-key); F <= T: none ever live again;
+      //  E: expiry of its keys that block pair 0 with the Outer role.
+      // A row with S and F <= T is eventless at any later tick: all M pairs
+      // are evaluated (M ticks, 3M evaluations). A row with T_d < E is
+      // outer-blocked at its first pair (1 tick).
+      const long long T = sh.c.tick;
       const int d = threadIdx.x, row = r + d;
-      int cand = INT_MAX;
+      int first_nontrivial = INT_MAX, first_nonouter = INT_MAX;
       if (row < M) {
         const int i = pa[row];
-        const long long T = sh.c.tick + d;
-        bool outer = T < s.exp_reas[s.mv[i]];
+        const int g0 = s.mv[i];
+        bool st = sm.impc[g0] == 0;
+        long long F = tabu ? max(s.exp_reas[g0], sh.jexp_max) : LLONG_MIN;
+        long long E = tabu ? s.exp_reas[g0] : LLONG_MIN;
         if (i < sh.c.psize) {
           const int x = s.pidx[i];
           if (s.pkind[i] == POOL_IDLE) {
-            outer |= T < s.exp_take[x];
+            st = st && sm.impc[x] == 0;
+            if (tabu) {
+              F = max(F, s.exp_take[x]);
+              E = max(E, s.exp_take[x]);
+            }
           } else {
-            const int k = s.brk[x];
-            outer |= T < s.exp_rel[k] && s.role_rel[k] == ROLE_OUTER;
+            st = st && s.cls_ver[x] == (long long)sh.c.applied && s.cls_any[x] == 0;
+            if (tabu) {
+              const int k = s.brk[x];
+              F = max(F, s.exp_rel[k]);
+              if (s.role_rel[k] == ROLE_OUTER) E = max(E, s.exp_rel[k]);
+            }
           }
         }
-        const int k = s.vrk[s.mvp[0]];
-        outer |= T < s.exp_rel[k] && s.role_rel[k] == ROLE_OUTER;
-        if (!outer) cand = d;
-      }
-      const int found = block_min<NT>(cand, sh);
-      const int nskip = found == INT_MAX ? min(NT, M - r) : found;
-      if (threadIdx.x == 0 && nskip > 0) {
-        sh.c.tick += nskip;
-        sh.c.skips_outer += (unsigned long long)nskip;
-        sh.c.pass_skipped = 1;
-      }
-      __syncthreads();
-      r += nskip;
-      PH_ADD(sh, 0, b0);
-      if (found == INT_MAX) continue;
-    }
-    // O(1) eventless row: no live key can block or end it and no move from
-    // its outer index improves any mission, so all M pairs are evaluated
-    // and nothing else happens (3 evaluations and one tick per pair).
-    if (threadIdx.x == 0) {
-      const int i = pa[r];
-      const long long T = sh.c.tick;
-      const int g0 = s.mv[i];
-      bool ok = sm.impc[g0] == 0 && (!tabu || (s.exp_reas[g0] <= T && sh.jexp_max <= T));
-      if (ok && i < sh.c.psize) {
-        const int x = s.pidx[i];
-        if (s.pkind[i] == POOL_IDLE) {
-          ok = sm.impc[x] == 0 && (!tabu || s.exp_take[x] <= T);
-        } else {
-          ok = s.cls_ver[x] == (long long)sh.c.applied && s.cls_any[x] == 0 &&
-               (!tabu || s.exp_rel[s.brk[x]] <= T);
+        if (tabu) {
+          const int k = s.vrk[s.mvp[0]];
+          if (s.role_rel[k] == ROLE_OUTER) E = max(E, s.exp_rel[k]);
         }
+        if (!(st && F <= T)) first_nontrivial = d;
+        if (!(T + d < E)) first_nonouter = d;
       }
-      if (ok) {
-        sh.c.evaluations += 3ull * (unsigned long long)M;
-        if (tabu) sh.c.tick += M;
-        sh.c.counts[4] += 1;
+      const int A = block_min<NT>(first_nontrivial, sh);
+      if (A > 0) {
+        // a run of eventless rows
+        const int n = A == INT_MAX ? min(NT, M - r) : A;
+        if (threadIdx.x == 0) {
+          sh.c.evaluations += 3ull * (unsigned long long)M * (unsigned long long)n;
+          if (tabu) sh.c.tick += (long long)M * n;
+          sh.c.counts[4] += (unsigned long long)n;
+        }
+        __syncthreads();
+        r += n;
+        PH_ADD(sh, 0, b0);
+        continue;
       }
-      sh.bi[7] = ok;
-    }
-    __syncthreads();
-    if (sh.bi[7]) {
+      if (tabu) {
+        // a run of rows outer-blocked at their first pair (one tick each)
+        const int found = block_min<NT>(first_nonouter, sh);
+        const int nskip = found == INT_MAX ? min(NT, M - r) : found;
+        if (threadIdx.x == 0 && nskip > 0) {
+          sh.c.tick += nskip;
+          sh.c.skips_outer += (unsigned long long)nskip;
+          sh.c.pass_skipped = 1;
+        }
+        __syncthreads();
+        r += nskip;
+        PH_ADD(sh, 0, b0);
+        if (nskip > 0) continue;
+      }
+      run_row<NT>(s, sh, sm, pa[r], tabu, tenure, debug);
+      __syncthreads();
       r += 1;
-      continue;
     }
-    run_row<NT>(s, sh, sm, pa[r], tabu, tenure, debug);
+    // end of pass: run_search's keep_going / max_passes (search.cpp:420-428)
+    if (threadIdx.x == 0) {
+      sh.c.passes += 1;
+      const bool keep = sh.c.error == 0 &&
+                        (sh.c.pass_applied > 0 || (tabu && sh.c.pass_skipped));
+      if (!keep || (max_passes >= 0 && sh.c.passes >= max_passes)) sh.c.done = 1;
+    }
     __syncthreads();
-    r += 1;
   }
   if (state_in_smem) {
     for (int v = threadIdx.x; v < V; v += NT) {
@@ -1021,9 +1079,9 @@ __global__ void final_kernel(Scenario* scs) {
 
 template <int NT>
 static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int n_scn,
-                                  const int32_t* d_pa, const int32_t* d_pb, bool tabu,
-                                  long long tenure, bool debug, int V, int B, int K,
-                                  cudaStream_t stream) {
+                                  const int32_t* d_perms, int kpasses, bool inkernel,
+                                  int max_passes, bool tabu, long long tenure, bool debug, int V,
+                                  int B, int K, cudaStream_t stream) {
   const size_t core = pass_smem_core(V, NT);
   const size_t state = pass_smem_state(V, B, K);
   const size_t limit = 200 * 1024;
@@ -1031,25 +1089,32 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   const int in_smem = core + state <= limit ? 1 : 0;
   const size_t smem = core + (in_smem ? state : 0);
   cudaFuncSetAttribute(pass_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  pass_kernel<NT><<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_pa, d_pb, tabu, tenure, debug,
-                                               in_smem);
+  pass_kernel<NT><<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
+                                               max_passes, tabu, tenure, debug, in_smem);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn, const int32_t* d_pa,
-                        const int32_t* d_pb, int M, bool tabu, long long tenure, bool debug, int V,
-                        int B, int K, cudaStream_t stream, int threads) {
-  const int nwd = (M + 31) / 32;
-  dim3 mg((nwd + 7) / 8 < 1184 ? (nwd + 7) / 8 : 1184, n_scn);
-  if (M > 0) prep_kernel<<<mg, 256, 0, stream>>>(d_scs, d_active, d_pb);
+// `kpasses` passes whose permutations are consecutive in d_perms (perm_a,
+// perm_b per pass). inkernel: each block rebuilds its own mirrors/bitsets
+// between passes; otherwise kpasses must be 1 and the grid-wide sweep runs
+// first.
+cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
+                        const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,
+                        bool tabu, long long tenure, bool debug, int V, int B, int K,
+                        cudaStream_t stream, int threads) {
+  if (!inkernel) {
+    const int nwd = (M + 31) / 32;
+    dim3 mg((nwd + 7) / 8 < 1184 ? (nwd + 7) / 8 : 1184, n_scn);
+    if (M > 0) prep_kernel<<<mg, 256, 0, stream>>>(d_scs, d_active, d_perms + M);
+  }
   if (threads == 1024)
-    return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_pa, d_pb, tabu, tenure, debug, V, B, K,
-                                stream);
+    return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
+                                tabu, tenure, debug, V, B, K, stream);
   if (threads == 512)
-    return launch_pass_nt<512>(d_scs, d_active, n_scn, d_pa, d_pb, tabu, tenure, debug, V, B, K,
-                               stream);
-  return launch_pass_nt<256>(d_scs, d_active, n_scn, d_pa, d_pb, tabu, tenure, debug, V, B, K,
-                             stream);
+    return launch_pass_nt<512>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
+                               tabu, tenure, debug, V, B, K, stream);
+  return launch_pass_nt<256>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
+                             tabu, tenure, debug, V, B, K, stream);
 }
 
 cudaError_t launch_init(Scenario* d_scs, int n_scn, cudaStream_t stream) {

@@ -30,6 +30,8 @@ struct Counters {
   int error;                      // 0 = ok, else an fp_status
   double total_up;                // rigorous upper bound of the current total
   double final_total;             // exact fixed-order total (written at the end)
+  double total_exact;             // exact fixed-order total of the state ...
+  long long total_ver;            // ... at this applied-move count (-1: unknown)
   // SM cycles spent per automaton phase (thread 0's view, single-scenario
   // launches): 0 row skipping, 1 row context, 2 chunk scans, 3 event pairs,
   // 4 exact fallbacks, 5 relocation prepasses

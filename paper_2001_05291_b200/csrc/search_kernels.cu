@@ -57,6 +57,10 @@ struct Shared {
   int nj;                               // live j-keys in sm.jl_*
   long long jexp_max;                   // latest expiry of any vehicle's {Relocate, id} key
   int tmp;
+  double bd0;
+  double xs;                            // exact chain: partial sum so far ...
+  int xk;                               // ... after this many terms
+  long long red_l[33];
   int red_i[2][33];
   double red_d[3][33];
 };
@@ -70,6 +74,7 @@ struct Smem {
   double* acc_abs;     // [NW*V]
   double* stage;       // [NW*32]
   int* wsum;           // [NW*3] per-warp scan summaries
+  int* xidx;           // [2*NT] mission-index buffer for exact relocation deltas
   int* impc;           // [V] set bits of imp[g] (0 = no reassign/takeover to g improves)
   int* jl_v;           // [V] vehicles whose {Relocate, id} j-key is live
   int* jl_lim;         // [V] its live window (positions from the segment start)
@@ -118,38 +123,210 @@ __device__ __forceinline__ double single_bound(const Scenario& s, const Shared& 
   return (double)(s.M + 2) * kTwoPowM52 * sh.c.total_up * 1.0001;
 }
 
-// Exact fixed-order sums S (current) and S' (mission j charged newc),
-// proj/src/search.cpp:150-167 and proj/src/search_state.hpp:36-40.
-// Thread 0 only.
-__device__ bool exact_single_accept(const Scenario& s, int j, double newc) {
-  double a = 0.0, b = 0.0;
-  for (int m = 0; m < s.M; ++m) {
-    const double c = s.mc[m];
-    a += c;
-    b += m == j ? newc : c;
-  }
-  return b < a;
+// ---- exact fixed-order fp64 sums, block-parallel -------------------------
+//
+// The reference decides candidate_total < total with two sequential fp64
+// sums over the M mission costs (proj/src/search.cpp:150-167, search_state.hpp
+// :36-40). exact_chain reproduces such a sum bit for bit with the whole
+// block: while the running sum S stays in one binade [2^e, 2^(e+1)) every
+// partial sum is a multiple of u = 2^(e-52), so fl(S + c) = S + u*rn(c/u)
+// unless c/u is an exact tie (then round-to-even depends on S). A chunk of
+// terms is therefore an int64 prefix scan of rn(c/u); the step that leaves
+// the binade is done with one true fp64 add from the exact integer-form
+// partial sum, and a chunk holding a tie before its crossing is stepped
+// sequentially up to the tie. All terms are >= 0 (distances), so S is
+// monotone and crosses each binade once.
+//   kind 0: c_k = mc[k]                      (the current total)
+//   kind 1: c_k = (k == j ? newc : mc[k])    (takeover / reassignment)
+//   kind 2: c_k = (mv[k] == mover ? col[k] : mc[k])   (relocation)
+__device__ __forceinline__ double chain_term(const Scenario& s, int kind, int k, int j, double newc,
+                                             int mover, const double* col) {
+  if (kind == 1) return k == j ? newc : s.mc[k];
+  if (kind == 2) return s.mv[k] == mover ? col[k] : s.mc[k];
+  return s.mc[k];
 }
 
-// Exact relocation quick delta, proj/src/search.cpp:121-127. Thread 0.
-__device__ double exact_reloc_quick(const Scenario& s, int t, int mover) {
-  double d = 0.0;
-  const double* col = s.cost + (long long)t * s.M;
-  for (int m = 0; m < s.M; ++m)
-    if (s.mv[m] == mover) d += col[m] - s.mc[m];
-  return d;
+template <int NT>
+__device__ long long block_exclusive_scan(long long x, long long& total, Shared& sh) {
+  constexpr int NW = NT / 32;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  long long incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(FULL, incl, o);
+    if (l >= o) incl += y;
+  }
+  if (l == 31) sh.red_l[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    long long v = l < NW ? sh.red_l[l] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(FULL, v, o);
+      if (l >= o) v += y;
+    }
+    if (l < NW) sh.red_l[l] = v;  // inclusive warp prefix
+    if (l == 31) sh.red_l[32] = v;
+  }
+  __syncthreads();
+  const long long before = w > 0 ? sh.red_l[w - 1] : 0;
+  total = sh.red_l[32];
+  __syncthreads();
+  return before + incl - x;
 }
 
-// Exact relocation candidate_total < total. Thread 0.
-__device__ bool exact_reloc_accept(const Scenario& s, int t, int mover) {
-  double a = 0.0, b = 0.0;
-  const double* col = s.cost + (long long)t * s.M;
-  for (int m = 0; m < s.M; ++m) {
-    const double c = s.mc[m];
-    a += c;
-    b += s.mv[m] == mover ? col[m] : c;
+template <int NT>
+__device__ double exact_chain(const Scenario& s, Shared& sh, int kind, int j, double newc,
+                              int mover, const double* col) {
+  constexpr int UE = 8;
+  constexpr int CH = NT * UE;
+  const int M = s.M;
+  if (threadIdx.x == 0) {
+    double S = 0.0;
+    int k = 0;
+    while (k < M && !(S >= 0x1p-900)) {  // leading zeros / tiny values: plain adds
+      S += chain_term(s, kind, k, j, newc, mover, col);
+      ++k;
+    }
+    sh.xs = S;
+    sh.xk = k;
   }
-  return b < a;
+  __syncthreads();
+  const long long LIM = 1ll << 53;
+  while (true) {
+    const int k0 = sh.xk;
+    const double S0 = sh.xs;
+    if (k0 >= M) break;
+    const int e = ilogb(S0);
+    const double u = ldexp(1.0, e - 52);
+    const long long N0 = (long long)(S0 / u);
+    const int kb = k0 + threadIdx.x * UE;
+    long long rr[UE];
+    long long local = 0;
+    int first_tie = INT_MAX;
+#pragma unroll
+    for (int q = 0; q < UE; ++q) {
+      const int k = kb + q;
+      long long ri = 0;
+      if (k < M) {
+        const double x = chain_term(s, kind, k, j, newc, mover, col) / u;
+        if (x >= 4.0e15) {
+          ri = LIM;  // this step certainly leaves the binade
+        } else {
+          const double f = floor(x);
+          const double fr = x - f;
+          ri = (long long)f + (fr >= 0.5 ? 1 : 0);
+          if (fr == 0.5) first_tie = min(first_tie, k);
+        }
+      }
+      rr[q] = ri;
+      local += ri;
+    }
+    long long total;
+    long long run = N0 + block_exclusive_scan<NT>(local, total, sh);
+    int first_cross = INT_MAX;
+    long long before_cross = 0;
+#pragma unroll
+    for (int q = 0; q < UE; ++q) {
+      const int k = kb + q;
+      if (k < M && first_cross == INT_MAX) {
+        if (run + rr[q] >= LIM) {
+          first_cross = k;
+          before_cross = run;
+        }
+        run += rr[q];
+      }
+    }
+    const int cross = block_min<NT>(first_cross, sh);
+    const int tie = block_min<NT>(first_tie, sh);
+    const int chunk_end = min(M, k0 + CH);
+    if (tie < min(cross, chunk_end)) {
+      // a rounding tie before the binade crossing: step to it exactly
+      if (threadIdx.x == 0) {
+        double S = S0;
+        for (int k = k0; k <= tie; ++k) S += chain_term(s, kind, k, j, newc, mover, col);
+        sh.xs = S;
+        sh.xk = tie + 1;
+      }
+    } else if (cross == INT_MAX) {
+      if (threadIdx.x == 0) {
+        sh.xs = (double)(N0 + total) * u;
+        sh.xk = chunk_end;
+      }
+    } else if (first_cross == cross) {
+      // owner of the crossing step: exact partial sum, then one fp64 add
+      const double prev = (double)before_cross * u;
+      sh.xs = prev + chain_term(s, kind, cross, j, newc, mover, col);
+      sh.xk = cross + 1;
+    }
+    __syncthreads();
+  }
+  const double r = sh.xs;
+  __syncthreads();
+  return r;
+}
+
+// Exact current total, cached per applied-move count.
+template <int NT>
+__device__ double exact_total(const Scenario& s, Shared& sh) {
+  if (sh.c.total_ver == (long long)sh.c.applied) return sh.c.total_exact;
+  const double t = exact_chain<NT>(s, sh, 0, -1, 0.0, -1, nullptr);
+  if (threadIdx.x == 0) {
+    sh.c.total_exact = t;
+    sh.c.total_ver = (long long)sh.c.applied;
+  }
+  __syncthreads();
+  return t;
+}
+
+// Exact relocation quick delta (proj/src/search.cpp:121-127): the mover's
+// terms in ascending mission order. The block compacts the mover's mission
+// indices (order preserving) into `idx`, thread 0 adds them in order.
+template <int NT>
+__device__ double exact_reloc_quick(const Scenario& s, Shared& sh, const double* col, int mover,
+                                    int* idx, int cap) {
+  constexpr int NW = NT / 32;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sh.tmp = 0;
+    sh.xs = 0.0;
+  }
+  __syncthreads();
+  for (int base = 0; base < s.M; base += NT) {
+    const int m = base + threadIdx.x;
+    const bool mine = m < s.M && s.mv[m] == mover;
+    const unsigned b = __ballot_sync(FULL, mine);
+    if (l == 0) sh.red_i[0][w] = __popc(b);
+    __syncthreads();
+    int off = sh.tmp;
+    for (int k = 0; k < w; ++k) off += sh.red_i[0][k];
+    if (mine) {
+      const int pos = off + __popc(b & ((1u << l) - 1u));
+      if (pos < cap) idx[pos] = m;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int k = 0; k < NW; ++k) t += sh.red_i[0][k];
+      // flush a full buffer into the running sum, in order
+      int n = sh.tmp + t;
+      if (n > cap - NT) {
+        double d = sh.xs;
+        for (int k = 0; k < n && k < cap; ++k) d += col[idx[k]] - s.mc[idx[k]];
+        sh.xs = d;
+        n = 0;
+      }
+      sh.tmp = n;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double d = sh.xs;
+    for (int k = 0; k < sh.tmp; ++k) d += col[idx[k]] - s.mc[idx[k]];
+    sh.xs = d;
+  }
+  __syncthreads();
+  const double r = sh.xs;
+  __syncthreads();
+  return r;
 }
 
 // Classification of one vehicle's relocation from its (any-order) delta sum,
@@ -424,6 +601,23 @@ __device__ void debug_check(const Scenario& s, Shared& sh) {
   }
 }
 
+// Exact accept of a single-substitution candidate (takeover/reassign):
+// candidate_total < total, both fixed-order fp64 sums. Block-wide; the new
+// exact total is cached when the move is accepted.
+template <int NT>
+__device__ bool exact_accept_single(const Scenario& s, Shared& sh, int j, double newc) {
+  const long long f0 = ph_now();
+  const double S = exact_total<NT>(s, sh);
+  const double S2 = exact_chain<NT>(s, sh, 1, j, newc, -1, nullptr);
+  if (threadIdx.x == 0) {
+    sh.c.fallbacks += 1;
+    sh.xs = S2;  // the total after the move, if accepted
+  }
+  PH_ADD(sh, 4, f0);
+  __syncthreads();
+  return S2 < S;
+}
+
 // Processes the pair (i, j) exactly as try_move x3 (proj/src/search.cpp:277-303,
 // 333-341). Block-cooperative; returns with the block synchronised.
 template <int NT>
@@ -431,39 +625,46 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
                              bool tabu, long long tenure, bool debug) {
   const int j = sm.pb[q];
   const long long exp = sh.c.tick + tenure;
-  // ---- takeover (thread 0 decides and applies)
+  // ---- takeover: thread 0 screens, the block settles the exact sum if needed
   if (threadIdx.x == 0) {
     sh.c.evaluations += 1;
-    sh.bi[4] = 0;
+    sh.bi[4] = 0;  // 1: accept, 2: needs the exact sums
     if (i < sh.c.psize && s.pkind[i] == POOL_IDLE) {
       const int g = s.pidx[i];
       if (compat_vm(s.vfixed[g], s.ro[j])) {
         const double newc = cost_at(s, s.vbase[g], j);
         const double mcj = s.mc[j];
         if (newc - mcj < 0.0) {
-          bool acc = mcj - newc > single_bound(s, sh);
-          if (!acc) {
-            const long long f0 = ph_now();
-            sh.c.fallbacks += 1;
-            acc = exact_single_accept(s, j, newc);
-            PH_ADD(sh, 4, f0);
-          }
-          if (acc) {
-            sh.bi[4] = 1;
-            sh.bi[5] = s.mv[j];
-            sh.bi[6] = g;
-            apply_takeover(s, sh, j, g, i);
-            sh.c.applied += 1;
-            sh.c.pass_applied += 1;
-            if (tabu) s.exp_take[g] = exp;
-            if (debug) debug_check(s, sh);
-          }
+          sh.bi[4] = mcj - newc > single_bound(s, sh) ? 1 : 2;
+          sh.bi[6] = g;
+          sh.bd0 = newc;
         }
       }
     }
   }
   __syncthreads();
-  if (sh.bi[4]) bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
+  if (sh.bi[4] == 2) {
+    const bool acc = exact_accept_single<NT>(s, sh, j, sh.bd0);
+    if (threadIdx.x == 0) sh.bi[4] = acc ? 3 : 0;  // 3: accepted, exact total known
+    __syncthreads();
+  }
+  if (sh.bi[4]) {
+    if (threadIdx.x == 0) {
+      const int g = sh.bi[6];
+      sh.bi[5] = s.mv[j];
+      apply_takeover(s, sh, j, g, i);
+      sh.c.applied += 1;
+      sh.c.pass_applied += 1;
+      if (sh.bi[4] == 3) {
+        sh.c.total_exact = sh.xs;
+        sh.c.total_ver = (long long)sh.c.applied;
+      }
+      if (tabu) s.exp_take[g] = exp;
+      if (debug) debug_check(s, sh);
+    }
+    __syncthreads();
+    bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
+  }
   // relocation preconditions (on the state the takeover left)
   if (threadIdx.x == 0) {
     sh.c.evaluations += 1;
@@ -481,25 +682,35 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
   const int t = sh.bi[0], mover = sh.bi[1];
   if (t >= 0) {
     relocation_classes<NT>(s, sh, sm, t);
-    if (threadIdx.x == 0) {
-      const uint8_t cls = sm.cls[mover];
-      bool acc = cls == CLS_ACC;
-      if (cls == CLS_NEG || cls == CLS_AMB) {
-        const long long f0 = ph_now();
-        sh.c.fallbacks += 1;
-        const bool neg = cls == CLS_NEG || exact_reloc_quick(s, t, mover) < 0.0;
-        acc = neg && exact_reloc_accept(s, t, mover);
-        PH_ADD(sh, 4, f0);
+    const uint8_t cls = sm.cls[mover];
+    bool acc = cls == CLS_ACC;
+    bool exact_known = false;
+    if (cls == CLS_NEG || cls == CLS_AMB) {
+      const long long f0 = ph_now();
+      const double* col = s.cost + (long long)t * s.M;
+      bool neg = cls == CLS_NEG;
+      if (!neg) neg = exact_reloc_quick<NT>(s, sh, col, mover, sm.xidx, 2 * NT) < 0.0;
+      if (neg) {
+        const double S = exact_total<NT>(s, sh);
+        const double S2 = exact_chain<NT>(s, sh, 2, -1, 0.0, mover, col);
+        acc = S2 < S;
+        exact_known = true;
+        if (threadIdx.x == 0) sh.bd0 = S2;
       }
-      sh.bi[2] = acc;
+      if (threadIdx.x == 0) sh.c.fallbacks += 1;
+      PH_ADD(sh, 4, f0);
+      __syncthreads();
     }
-    __syncthreads();
-    if (sh.bi[2]) {
+    if (acc) {
       apply_relocate<NT>(s, sh, mover, t, i);
       bits_after_relocation<NT>(s, sh, sm, mover);
       if (threadIdx.x == 0) {
         sh.c.applied += 1;
         sh.c.pass_applied += 1;
+        if (exact_known) {
+          sh.c.total_exact = sh.bd0;
+          sh.c.total_ver = (long long)sh.c.applied;
+        }
         if (tabu) {
           // outer {Relocate, target base id} then inner {Relocate, mover id};
           // the second insert wins when the two ids coincide.
@@ -512,6 +723,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         }
         if (debug) debug_check(s, sh);
       }
+      __syncthreads();
     }
   }
   // ---- reassignment
@@ -523,29 +735,37 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       const double newc = cost_at(s, s.vbase[g], j);
       const double mcj = s.mc[j];
       if (newc - mcj < 0.0) {
-        bool acc = mcj - newc > single_bound(s, sh);
-        if (!acc) {
-          const long long f0 = ph_now();
-          sh.c.fallbacks += 1;
-          acc = exact_single_accept(s, j, newc);
-          PH_ADD(sh, 4, f0);
-        }
-        if (acc) {
-          sh.bi[4] = 1;
-          sh.bi[5] = l;
-          sh.bi[6] = g;
-          apply_reassign(s, sh, j, g);
-          sh.c.applied += 1;
-          sh.c.pass_applied += 1;
-          if (tabu) s.exp_reas[g] = exp;
-          if (debug) debug_check(s, sh);
-        }
+        sh.bi[4] = mcj - newc > single_bound(s, sh) ? 1 : 2;
+        sh.bi[6] = g;
+        sh.bd0 = newc;
       }
     }
-    sh.c.tick += 1;
   }
   __syncthreads();
-  if (sh.bi[4]) bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
+  if (sh.bi[4] == 2) {
+    const bool acc = exact_accept_single<NT>(s, sh, j, sh.bd0);
+    if (threadIdx.x == 0) sh.bi[4] = acc ? 3 : 0;
+    __syncthreads();
+  }
+  if (sh.bi[4]) {
+    if (threadIdx.x == 0) {
+      const int g = sh.bi[6];
+      sh.bi[5] = s.mv[j];
+      apply_reassign(s, sh, j, g);
+      sh.c.applied += 1;
+      sh.c.pass_applied += 1;
+      if (sh.bi[4] == 3) {
+        sh.c.total_exact = sh.xs;
+        sh.c.total_ver = (long long)sh.c.applied;
+      }
+      if (tabu) s.exp_reas[g] = exp;
+      if (debug) debug_check(s, sh);
+    }
+    __syncthreads();
+    bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
+  }
+  if (threadIdx.x == 0) sh.c.tick += 1;
+  __syncthreads();
 }
 
 // Row context after any state change (thread 0 writes, all read after sync).
@@ -840,7 +1060,7 @@ size_t pass_smem_core(int V, int NT) {
   const int NW = NT / 32;
   return align16(4ull * V) + align16(V) + align16(V) + 2 * align16(8ull * NW * V) +
          align16(8ull * NW * 32) + align16(4ull * NW * 3) + 3 * align16(4ull * V) + align16(V) +
-         64;
+         align16(8ull * NT) + 64;
 }
 size_t pass_smem_state(int V, int B, int K) {
   return align16(8ull * V) * 2 + align16(8ull * K) + align16(K) + align16(4ull * V) * 3 +
@@ -849,7 +1069,7 @@ size_t pass_smem_state(int V, int B, int K) {
 
 // One pass over perm_a for every active scenario (blockIdx.x = scenario).
 template <int NT>
-__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
+__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
                 int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
                 int debug_i, int state_in_smem) {
@@ -875,6 +1095,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 4))
   sm.acc_abs = reinterpret_cast<double*>(take(8ull * NW * V));
   sm.stage = reinterpret_cast<double*>(take(8ull * NW * 32));
   sm.wsum = reinterpret_cast<int*>(take(4ull * NW * 3));
+  sm.xidx = reinterpret_cast<int*>(take(8ull * NT));
   sm.jl_v = reinterpret_cast<int*>(take(4ull * V));
   sm.jl_lim = reinterpret_cast<int*>(take(4ull * V));
   sm.jl_outer = take(V);
@@ -1064,6 +1285,8 @@ __global__ void init_kernel(Scenario* scs) {
     for (int m = 0; m < s.M; ++m) t += s.mc[m];
     s.ctr->total_up = t;
     s.ctr->final_total = t;
+    s.ctr->total_exact = t;
+    s.ctr->total_ver = 0;
   }
 }
 

@@ -13,6 +13,7 @@ from paper_2001_05291_b200 import fleetplace as F  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--c3", action="store_true")
+ap.add_argument("--c4", action="store_true")
 ap.add_argument("--c5", type=int, default=0, help="scenarios in the c5 batch")
 ap.add_argument("--c5-passes", type=int, default=-1)
 ap.add_argument("--ref", action="store_true", help="compare prefixes with the reference")
@@ -60,6 +61,30 @@ if a.c3:
             print(f"c3 parity max_passes={mp}: {mine == ref.stats} ref {ref.seconds:.1f}s "
                   f"(wall {time.time()-t0:.1f}s) {ref.stats}", flush=True)
             print("assignment equal:", np.array_equal(r.mission_vehicle, ref.mission_vehicle), flush=True)
+
+if a.c4:
+    import torch
+    t0 = time.time()
+    inst = F.survey_instance(5000, 1000000, 250, seed=1)
+    t1 = time.time()
+    print(f"c4 gen {t1-t0:.1f}s", flush=True)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t = F.build_distance_table(inst)
+    t2 = time.time()
+    start = F.rank_bases(inst, t)
+    t3 = time.time()
+    print(f"c4 table {t2-t1:.2f}s rank {t3-t2:.2f}s (wall)", flush=True)
+    pool = F.initial_pool(start, inst)
+    vb, mv, pk, px = F._state_arrays(start.assignment, pool, inst)
+    for mp in [int(x) for x in a.passes.split(",")]:
+        r = F.search_arrays(inst, t, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=mp),
+                            vb, mv, pk, px)
+        s = r.stats
+        print(f"c4 max_passes={mp}: {s.device_ms:.1f} ms, passes {s.passes} evals {s.evaluations} "
+              f"moves {s.applied_moves} obj {s.final_objective_km:.6f} fallbacks {s.exact_fallbacks} "
+              f"events {s.event_counts} phases_ms "
+              f"{[round(c / 1965e3, 1) for c in s.phase_cycles]}", flush=True)
 
 if a.c5:
     n = a.c5

@@ -192,10 +192,60 @@ def run_ours(args) -> None:
     }
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(inst, host_cost, start, pk, px)
+    if rank == 0 and not args.no_extras:
+        line["extra_workloads"] = extra_workloads(local)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def extra_workloads(device: int) -> dict:
+    """The other BASELINE.json shapes on this GPU (reported, not the headline):
+    c3 (2k x 100k x 100) capped at 10 passes, and one GPU's share of the c5
+    batch (512 of the 4096 independent 200 x 5k x 20 scenarios) to quiescence.
+    Device times from the library's CUDA events."""
+    import torch
+    from paper_2001_05291_b200 import fleetplace as F
+
+    out = {}
+    inst = F.survey_instance(2000, 100000, 100, seed=1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    t = F.build_distance_table(inst, device=device)
+    t1 = time.perf_counter()
+    start = F.rank_bases(inst, t)
+    t2 = time.perf_counter()
+    vb, mv, pk, px = F._state_arrays(start.assignment, F.initial_pool(start, inst), inst)
+    r = F.search_arrays(inst, t, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=10),
+                        vb, mv, pk, px)
+    out["c3_10_passes"] = {
+        "workload": "2000 bases x 100k missions x 100 vehicles, tabu seed 7, max_passes 10",
+        "table_build_s_wall": t1 - t0, "rank_s_wall": t2 - t1, "search_ms": r.stats.device_ms,
+        "evaluations": r.stats.evaluations, "applied_moves": r.stats.applied_moves,
+        "move_evals_per_s": r.stats.evaluations / (r.stats.device_ms / 1e3)}
+    del t
+    n = 512
+    insts, starts, tabs = [], [], []
+    for k in range(n):
+        ik = F.survey_instance(200, 5000, 20, seed=1 + k)
+        tk = F.build_distance_table(ik, device=device)
+        sk = F.rank_bases(ik, tk)
+        insts.append(ik)
+        starts.append(F._state_arrays(sk.assignment, F.initial_pool(sk, ik), ik))
+        tabs.append(np.ascontiguousarray(tk.cost.T).reshape(-1))
+        del tk
+    res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu), tabs,
+                         device=device)
+    ev = sum(x.stats.evaluations for x in res)
+    ms = res[0].stats.device_ms
+    out["c5_share_512"] = {
+        "workload": "512 of the 4096 c5 scenarios (200 x 5k x 20, seeds 1..512), tabu to quiescence",
+        "search_ms": ms, "evaluations": ev, "move_evals_per_s": ev / (ms / 1e3),
+        "passes_max": max(x.stats.passes for x in res),
+        "applied_moves": sum(x.stats.applied_moves for x in res)}
+    return out
 
 
 def _ref_lib():
@@ -258,6 +308,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the c3 / c5 extra workloads")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

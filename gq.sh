@@ -1,5 +1,5 @@
 #!/bin/bash
-python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-python bench.py --steps 1 --warmup 1 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['phase_ms'], d['event_counts'], d['search_stats'])"
-timeout 1200 python tools/scale_probe.py --c4 --passes 1,3 2>&1 | tail -3
-timeout 600 python tools/scale_probe.py --c5 296 2>&1 | tail -2
+mkdir -p gpurun_out
+python bench.py --steps 3 --warmup 3 > gpurun_out/bench_r1.json 2> gpurun_out/bench_r1.err; echo rc=$?
+tail -c 3000 gpurun_out/bench_r1.json
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_r1.json 2>&1; tail -c 1500 gpurun_out/bench_ref_r1.json

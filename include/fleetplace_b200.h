@@ -182,6 +182,14 @@ fp_status fp_table_upload(fp_ctx* ctx, int32_t n_missions, int32_t n_bases,
                           const double* cost_colmajor);
 fp_status fp_table_download(fp_ctx* ctx, double* out_cost);
 
+/* haversine_km / mission_cost_km (proj/include/fleetplace/geo.hpp:22-30) on
+ * n point pairs with kernel (1)'s arithmetic: out[k] = hav(a_k, b_k) +
+ * (c_lat ? hav(a_k, c_k) : 0). Host arrays; c_lat/c_lon may be NULL. */
+fp_status fp_haversine_batch(fp_ctx* ctx, int32_t n, const double* a_lat,
+                             const double* a_lon, const double* b_lat,
+                             const double* b_lon, const double* c_lat,
+                             const double* c_lon, double radius_km, double* out);
+
 /* ---- kernel (2): ranking ------------------------------------------------ */
 /* column_totals (proj/src/rank.cpp:10-23): out[b] = sum_m cost(m, b) in row
  * order, bit-identical to the sequential reference. */

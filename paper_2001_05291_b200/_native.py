@@ -19,7 +19,7 @@ EXPORTS = (
     "fp_ctx_kernel_launches", "fp_validate_instance", "fp_generate_instance",
     "fp_build_distance_table", "fp_table_upload", "fp_table_download",
     "fp_column_totals", "fp_rank_bases", "fp_initial_pool", "fp_search",
-    "fp_search_batch", "fp_enumerate_moves", "fp_objective_km",
+    "fp_search_batch", "fp_enumerate_moves", "fp_objective_km", "fp_haversine_batch",
 )
 
 _lib: C.CDLL | None = None
@@ -74,6 +74,8 @@ def lib() -> C.CDLL:
                                      f64p, i32p]
     l.fp_enumerate_moves.restype = i32
     l.fp_objective_km.argtypes = [p, i32p, i32p, f64p]
+    l.fp_haversine_batch.argtypes = [p, i32, f64p, f64p, f64p, f64p, f64p, f64p, f64, f64p]
+    l.fp_haversine_batch.restype = i32
     l.fp_objective_km.restype = i32
     _lib = l
     return l

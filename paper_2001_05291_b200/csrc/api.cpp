@@ -635,6 +635,34 @@ fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* in, double rad
   });
 }
 
+fp_status fp_haversine_batch(fp_ctx* ctx, int32_t n, const double* a_lat, const double* a_lon,
+                             const double* b_lat, const double* b_lon, const double* c_lat,
+                             const double* c_lon, double radius_km, double* out) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (n <= 0) return;
+    const bool three = c_lat && c_lon;
+    DBuf<double> d((three ? 7ull : 5ull) * n);
+    double* p = d.p;
+    h2d(p, a_lat, n, ctx->stream);
+    h2d(p + n, a_lon, n, ctx->stream);
+    h2d(p + 2ll * n, b_lat, n, ctx->stream);
+    h2d(p + 3ll * n, b_lon, n, ctx->stream);
+    if (three) {
+      h2d(p + 5ll * n, c_lat, n, ctx->stream);
+      h2d(p + 6ll * n, c_lon, n, ctx->stream);
+    }
+    check(fpk::launch_haversine_pairs(n, p, p + n, p + 2ll * n, p + 3ll * n,
+                                      three ? p + 5ll * n : nullptr,
+                                      three ? p + 6ll * n : nullptr, radius_km, p + 4ll * n,
+                                      ctx->stream),
+          "haversine");
+    ctx->launches += 1;
+    d2h(out, p + 4ll * n, n, ctx->stream);
+    check(cudaStreamSynchronize(ctx->stream), "haversine sync");
+  });
+}
+
 fp_status fp_table_upload(fp_ctx* ctx, int32_t n_missions, int32_t n_bases,
                           const double* cost_colmajor) {
   return guarded([&] {

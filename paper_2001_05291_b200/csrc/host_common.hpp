@@ -17,6 +17,10 @@ cudaError_t launch_table(const double* blat, const double* blon, const double* b
                          const double* plat, const double* plon, const double* pcos,
                          const double* dlat, const double* dlon, const double* dcos, int M,
                          double radius_km, double* cost, cudaStream_t st);
+cudaError_t launch_haversine_pairs(int n, const double* alat, const double* alon,
+                                   const double* blat, const double* blon, const double* clat,
+                                   const double* clon, double radius_km, double* out,
+                                   cudaStream_t st);
 cudaError_t launch_column_totals(const double* cost, int M, int B, double* out, cudaStream_t st);
 cudaError_t launch_mission_argmin(const double* cost, int M, const int32_t* cb, const int32_t* cbid,
                                   const uint8_t* cf, const int32_t* cv, int n, const uint8_t* ro,

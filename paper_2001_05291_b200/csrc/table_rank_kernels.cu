@@ -63,6 +63,23 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Point-pair haversines (geo.hpp API) with the table kernel's arithmetic.
+__global__ void haversine_pairs_kernel(int n, const double* __restrict__ alat,
+                                       const double* __restrict__ alon,
+                                       const double* __restrict__ blat,
+                                       const double* __restrict__ blon,
+                                       const double* __restrict__ clat,
+                                       const double* __restrict__ clon, double two_r,
+                                       double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double ca = cos(__dmul_rn(alat[k], kDegToRad));
+  double r = hav(alat[k], alon[k], ca, blat[k], blon[k], cos(__dmul_rn(blat[k], kDegToRad)), two_r);
+  if (clat) r = __dadd_rn(r, hav(alat[k], alon[k], ca, clat[k], clon[k],
+                                 cos(__dmul_rn(clat[k], kDegToRad)), two_r));
+  out[k] = r;
+}
+
 // Column totals: warp w owns columns [32w, 32w+32). Per 32-row tile, lane l
 // loads row (r0+l) of each of the 32 columns (coalesced within a column),
 // the tile is transposed in shared memory, and lane l adds its column's 32
@@ -178,6 +195,16 @@ cudaError_t launch_table(const double* blat, const double* blon, const double* b
   dim3 grid((M + 255) / 256, (B + bpb - 1) / bpb);
   table_kernel<<<grid, 256, 0, st>>>(blat, blon, bcos, B, plat, plon, pcos, dlat, dlon, dcos, M,
                                      2.0 * radius_km, bpb, cost);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_haversine_pairs(int n, const double* alat, const double* alon,
+                                   const double* blat, const double* blon, const double* clat,
+                                   const double* clon, double radius_km, double* out,
+                                   cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  haversine_pairs_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, alat, alon, blat, blon, clat, clon,
+                                                          2.0 * radius_km, out);
   return cudaGetLastError();
 }
 

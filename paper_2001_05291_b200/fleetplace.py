@@ -255,6 +255,47 @@ class Instance:
         return self._cstruct
 
 
+def valid(p) -> bool:
+    """proj/src/geo.cpp:12-15: lat in [-90, 90], lon in [-180, 180]."""
+    return -90.0 <= p[0] <= 90.0 and -180.0 <= p[1] <= 180.0
+
+
+_geo_ctx = None
+
+
+def _geo():
+    global _geo_ctx
+    if _geo_ctx is None:
+        _geo_ctx = _Ctx(0)
+    return _geo_ctx
+
+
+def haversine_km_batch(a_lat, a_lon, b_lat, b_lon, radius_km: float = kEarthRadiusKm,
+                       c_lat=None, c_lon=None) -> np.ndarray:
+    """Vectorised haversine_km (+ a second leg from the same points when c_*
+    is given, i.e. mission_cost_km) on the device, kernel (1)'s arithmetic."""
+    arrs = [np.ascontiguousarray(np.atleast_1d(x), np.float64) for x in (a_lat, a_lon, b_lat, b_lon)]
+    n = arrs[0].size
+    cl = None if c_lat is None else np.ascontiguousarray(np.atleast_1d(c_lat), np.float64)
+    co = None if c_lon is None else np.ascontiguousarray(np.atleast_1d(c_lon), np.float64)
+    out = np.empty(n, np.float64)
+    _check(lib().fp_haversine_batch(_geo().p, n, *(A.ptr(x, C.c_double) for x in arrs),
+                                    A.ptr(cl, C.c_double), A.ptr(co, C.c_double), radius_km,
+                                    A.ptr(out, C.c_double)))
+    return out
+
+
+def haversine_km(a, b, radius_km: float = kEarthRadiusKm) -> float:
+    """proj/include/fleetplace/geo.hpp:22-27 (device arithmetic)."""
+    return float(haversine_km_batch(a[0], a[1], b[0], b[1], radius_km)[0])
+
+
+def mission_cost_km(base, pickup, delivery, radius_km: float = kEarthRadiusKm) -> float:
+    """proj/include/fleetplace/geo.hpp:28-30: base->pickup + base->delivery."""
+    return float(haversine_km_batch(base[0], base[1], pickup[0], pickup[1], radius_km,
+                                    delivery[0], delivery[1])[0])
+
+
 def validate_instance(inst: Instance) -> None:
     """proj/src/model.cpp:46-74."""
     _check(lib().fp_validate_instance(C.byref(inst.c())))

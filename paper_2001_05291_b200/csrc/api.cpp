@@ -287,7 +287,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
-      invb, exp_take, exp_reas, exp_rel, role_rel, cls_cache, cls_ver, cls_any, imp, mem, ctr, cost, total;
+      invb, exp_take, exp_reas, exp_rel, role_rel, cls_cache, cls_ver, cls_any, imp, mem, scratch, ctr, cost, total;
 };
 
 Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
@@ -324,6 +324,7 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   const size_t nwd = ((size_t)M + 31) / 32;
   L.imp = put(4ull * V * nwd);
   L.mem = put(4ull * V * nwd);
+  L.scratch = put(4ull * M + 4);
   L.cost = own_cost ? put(8ull * M * B) : 0;
   L.total = o;
   return L;
@@ -432,6 +433,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.cls_any = db + L.cls_any;
     S.imp = reinterpret_cast<uint32_t*>(db + L.imp);
     S.mem = reinterpret_cast<uint32_t*>(db + L.mem);
+    S.scratch = reinterpret_cast<int32_t*>(db + L.scratch);
     S.nwd = (M + 31) / 32;
     S.ctr = run.d_ctr.p + s;
     S.M = M;
@@ -532,7 +534,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     o.final_objective_km = c.final_total;
     outs[s].device_ms = ms;
     outs[s].exact_fallbacks = c.fallbacks;
-    for (int k = 0; k < 6; ++k) outs[s].phase_cycles[k] = c.cycles[k];
+    for (int k = 0; k < 10; ++k) outs[s].phase_cycles[k] = c.cycles[k];
     for (int k = 0; k < 5; ++k) outs[s].event_counts[k] = c.counts[k];
     outs[s].kernel_launches = ctx->launches;
   }

@@ -35,7 +35,8 @@ struct Counters {
   // SM cycles spent per automaton phase (thread 0's view, single-scenario
   // launches): 0 row skipping, 1 row context, 2 chunk scans, 3 event pairs,
   // 4 exact fallbacks, 5 relocation prepasses
-  unsigned long long cycles[6];
+  unsigned long long cycles[10];  // ... 6 relocation bit updates, 7 substitution bit updates,
+                                  // 8 relocation apply, 9 exact totals
   // event counts: 0 interesting rows, 1 chunk iterations, 2 row contexts,
   // 3 relocation prepasses
   unsigned long long counts[5];   // ... 4 rows resolved by the O(1) eventless test
@@ -82,6 +83,7 @@ struct Scenario {
   //  mem[v]: the position's mission is served by vehicle v
   uint32_t* imp;             // [V*NWD]
   uint32_t* mem;             // [V*NWD]
+  int32_t* scratch;          // [M] per-scenario scratch (relocation position lists)
   Counters* ctr;
   int32_t M, B, V, K, pool_cap, nwd;
 };

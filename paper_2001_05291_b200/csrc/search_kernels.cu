@@ -75,6 +75,8 @@ struct Smem {
   double* stage;       // [NW*32]
   int* wsum;           // [NW*3] per-warp scan summaries
   int* xidx;           // [2*NT] mission-index buffer for exact relocation deltas
+  int* xlist;          // position buffer for relocation bitset updates (global scratch)
+  int xlist_cap;
   int* impc;           // [V] set bits of imp[g] (0 = no reassign/takeover to g improves)
   int* jl_v;           // [V] vehicles whose {Relocate, id} j-key is live
   int* jl_lim;         // [V] its live window (positions from the segment start)
@@ -268,7 +270,9 @@ __device__ double exact_chain(const Scenario& s, Shared& sh, int kind, int j, do
 template <int NT>
 __device__ double exact_total(const Scenario& s, Shared& sh) {
   if (sh.c.total_ver == (long long)sh.c.applied) return sh.c.total_exact;
+  const long long e0 = ph_now();
   const double t = exact_chain<NT>(s, sh, 0, -1, 0.0, -1, nullptr);
+  PH_ADD(sh, 9, e0);
   if (threadIdx.x == 0) {
     sh.c.total_exact = t;
     sh.c.total_ver = (long long)sh.c.applied;
@@ -388,49 +392,106 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
 }
 
 // After vehicle x moved to a new base (its missions' costs already updated):
-// its own imp row in full (warp per word, lane per position), and the bits of
-// the positions it serves in every other row (thread per word). Block-wide.
+// (1) its own imp row in full (warp per word, lane per position, 4 words in
+// flight per warp); (2) the bits of the positions it serves in every other
+// row: the positions are compacted from mem[x] into `list`, then the block
+// runs over the flattened (position, vehicle) pairs with independent gathers
+// and sets / clears bits with word atomics. Block-wide.
 template <int NT>
-__device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem& sm, int x) {
+__device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem& sm, int x,
+                                      int* list, int cap) {
   constexpr int NW = NT / 32;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int nwd = s.nwd, M = s.M;
+  const int nwd = s.nwd, M = s.M, V = s.V;
   const double* colx = s.cost + (long long)s.vbase[x] * M;
   const bool fx = s.vfixed[x];
   if (threadIdx.x == 0) sh.tmp = 0;
   __syncthreads();
-  for (int wd = w; wd < nwd; wd += NW) {
-    const int q = wd * 32 + l;
-    bool b = false;
-    if (q < M) b = s.mvp[q] != x && compat_vm(fx, s.rop[q]) && colx[sm.pb[q]] < s.mcp[q];
-    const unsigned m = __ballot_sync(FULL, b);
-    if (l == 0) {
-      s.imp[(long long)x * nwd + wd] = m;
-      atomicAdd(&sh.tmp, __popc(m));
+  int cnt = 0;
+  for (int wd0 = w * 8; wd0 < nwd; wd0 += NW * 8) {
+    bool b[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = (wd0 + u) * 32 + l;
+      b[u] = false;
+      if (wd0 + u < nwd && q < M)
+        b[u] = s.mvp[q] != x && compat_vm(fx, s.rop[q]) && colx[sm.pb[q]] < s.mcp[q];
     }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const unsigned m = __ballot_sync(FULL, b[u]);
+      if (l == 0 && wd0 + u < nwd) {
+        s.imp[(long long)x * nwd + wd0 + u] = m;
+        cnt += __popc(m);
+      }
+    }
+  }
+  if (l == 0) atomicAdd(&sh.tmp, cnt);
+  // compact the positions x serves (order irrelevant)
+  if (threadIdx.x == 0) sh.bi[7] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sm.impc[x] = sh.tmp;
   }
   for (int wd = threadIdx.x; wd < nwd; wd += NT) {
     uint32_t mx = s.mem[(long long)x * nwd + wd];
-    while (mx) {
-      const int bn = __ffs(mx) - 1;
-      mx &= mx - 1;
-      const int q = wd * 32 + bn;
-      const int j = sm.pb[q];
-      const double mcq = s.mcp[q];
-      const bool ro = s.rop[q];
-      for (int g = 0; g < s.V; ++g) {
-        if (g == x) continue;
+    if (mx) {
+      const int at = atomicAdd(&sh.bi[7], __popc(mx));
+      for (int k = at; mx; mx &= mx - 1, ++k)
+        if (k < cap) list[k] = wd * 32 + __ffs(mx) - 1;
+    }
+  }
+  __syncthreads();
+  const int n = min(sh.bi[7], cap);
+  // warp per position, lanes over vehicles: all gathers of a position are
+  // independent; bits of one position live in different words (rows), and
+  // positions sharing a word use word atomics
+  for (int k = w; k < n; k += NW) {
+    const int q = list[k];
+    const int j = sm.pb[q];
+    const double mcq = s.mcp[q];
+    const bool ro = s.rop[q];
+    const int wd = q >> 5;
+    const uint32_t bit = 1u << (q & 31);
+    for (int g0 = 0; g0 < V; g0 += 32 * 4) {
+      bool on[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int g = g0 + u * 32 + l;
+        on[u] = g < V && g != x && compat_vm(s.vfixed[g], ro) && cost_at(s, s.vbase[g], j) < mcq;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int g = g0 + u * 32 + l;
+        if (g >= V || g == x) continue;
         uint32_t* wp = s.imp + (long long)g * nwd + wd;
-        const bool was = (*wp & (1u << bn)) != 0u;
-        const bool now = compat_vm(s.vfixed[g], ro) && cost_at(s, s.vbase[g], j) < mcq;
-        put_bit(wp, 1u << bn, now);
-        if (now != was) atomicAdd(&sm.impc[g], now ? 1 : -1);
+        const uint32_t old = on[u] ? atomicOr(wp, bit) : atomicAnd(wp, ~bit);
+        if (((old & bit) != 0u) != on[u]) atomicAdd(&sm.impc[g], on[u] ? 1 : -1);
       }
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) sm.impc[x] = sh.tmp;
-  __syncthreads();
+  if (sh.bi[7] > cap) {
+    // more positions than the buffer holds: finish them one word at a time
+    for (int wd = threadIdx.x; wd < nwd; wd += NT) {
+      uint32_t mx = s.mem[(long long)x * nwd + wd];
+      while (mx) {
+        const int bn = __ffs(mx) - 1;
+        mx &= mx - 1;
+        const int q = wd * 32 + bn;
+        const int j = sm.pb[q];
+        for (int g = 0; g < V; ++g) {
+          if (g == x) continue;
+          uint32_t* wp = s.imp + (long long)g * nwd + wd;
+          const bool was = (*wp & (1u << bn)) != 0u;
+          const bool now = compat_vm(s.vfixed[g], s.rop[q]) && cost_at(s, s.vbase[g], j) < s.mcp[q];
+          put_bit(wp, 1u << bn, now);
+          if (now != was) atomicAdd(&sm.impc[g], now ? 1 : -1);
+        }
+      }
+    }
+    __syncthreads();
+  }
 }
 
 // Relocation classes of every vehicle towards empty base t, into sm.cls,
@@ -461,7 +522,7 @@ __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm
   double* st = sm.stage + w * 32;
   __syncwarp();
   const double* col = s.cost + (long long)t * s.M;
-  constexpr int UR = 4;  // independent 32-mission groups in flight per warp
+  constexpr int UR = 8;  // independent 32-mission groups in flight per warp
   for (int base = w * 32; base < s.M; base += UR * NT) {
     int vv[UR];
     double dd[UR];
@@ -663,7 +724,9 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       if (debug) debug_check(s, sh);
     }
     __syncthreads();
+    const long long a2 = ph_now();
     bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
+    PH_ADD(sh, 7, a2);
   }
   // relocation preconditions (on the state the takeover left)
   if (threadIdx.x == 0) {
@@ -702,8 +765,12 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       __syncthreads();
     }
     if (acc) {
+      const long long a0 = ph_now();
       apply_relocate<NT>(s, sh, mover, t, i);
-      bits_after_relocation<NT>(s, sh, sm, mover);
+      PH_ADD(sh, 8, a0);
+      const long long a1 = ph_now();
+      bits_after_relocation<NT>(s, sh, sm, mover, sm.xlist, sm.xlist_cap);
+      PH_ADD(sh, 6, a1);
       if (threadIdx.x == 0) {
         sh.c.applied += 1;
         sh.c.pass_applied += 1;
@@ -762,7 +829,9 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       if (debug) debug_check(s, sh);
     }
     __syncthreads();
+    const long long a2 = ph_now();
     bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
+    PH_ADD(sh, 7, a2);
   }
   if (threadIdx.x == 0) sh.c.tick += 1;
   __syncthreads();
@@ -1096,6 +1165,8 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   sm.stage = reinterpret_cast<double*>(take(8ull * NW * 32));
   sm.wsum = reinterpret_cast<int*>(take(4ull * NW * 3));
   sm.xidx = reinterpret_cast<int*>(take(8ull * NT));
+  sm.xlist = s.scratch;
+  sm.xlist_cap = s.M;
   sm.jl_v = reinterpret_cast<int*>(take(4ull * V));
   sm.jl_lim = reinterpret_cast<int*>(take(4ull * V));
   sm.jl_outer = take(V);
@@ -1272,17 +1343,16 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   if (threadIdx.x == 0) *g.ctr = sh.c;
 }
 
-// Search start: per-mission costs, per-vehicle counts and the exact initial
-// total (SearchState::from, proj/src/search.cpp:41-48). One block per
-// scenario; the fixed-order total is one sequential chain (thread 0).
-__global__ void init_kernel(Scenario* scs) {
+// Search start: per-mission costs and the exact initial fixed-order total
+// (SearchState::from, proj/src/search.cpp:41-48), one block per scenario.
+__global__ void __launch_bounds__(512) init_kernel(Scenario* scs) {
   const Scenario s = scs[blockIdx.x];
+  __shared__ Shared sh;
   for (int m = threadIdx.x; m < s.M; m += blockDim.x)
     s.mc[m] = cost_at(s, s.vbase[s.mv[m]], m);
   __syncthreads();
+  const double t = exact_chain<512>(s, sh, 0, -1, 0.0, -1, nullptr);
   if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int m = 0; m < s.M; ++m) t += s.mc[m];
     s.ctr->total_up = t;
     s.ctr->final_total = t;
     s.ctr->total_exact = t;
@@ -1290,14 +1360,18 @@ __global__ void init_kernel(Scenario* scs) {
   }
 }
 
-// Exact fixed-order final total (st.total after the last move).
-__global__ void final_kernel(Scenario* scs) {
+// Exact fixed-order final total (st.total after the last move): the cached
+// exact total when it is current, else one block-parallel exact chain.
+__global__ void __launch_bounds__(512) final_kernel(Scenario* scs) {
   const Scenario s = scs[blockIdx.x];
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int m = 0; m < s.M; ++m) t += s.mc[m];
-    s.ctr->final_total = t;
+  __shared__ Shared sh;
+  const Counters c = *s.ctr;
+  if (c.total_ver == (long long)c.applied) {
+    if (threadIdx.x == 0) s.ctr->final_total = c.total_exact;
+    return;
   }
+  const double t = exact_chain<512>(s, sh, 0, -1, 0.0, -1, nullptr);
+  if (threadIdx.x == 0) s.ctr->final_total = t;
 }
 
 template <int NT>
@@ -1341,12 +1415,12 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
 }
 
 cudaError_t launch_init(Scenario* d_scs, int n_scn, cudaStream_t stream) {
-  init_kernel<<<n_scn, 256, 0, stream>>>(d_scs);
+  init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
   return cudaGetLastError();
 }
 
 cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream) {
-  final_kernel<<<n_scn, 32, 0, stream>>>(d_scs);
+  final_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
   return cudaGetLastError();
 }
 

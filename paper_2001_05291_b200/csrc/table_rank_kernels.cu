@@ -80,28 +80,45 @@ __global__ void haversine_pairs_kernel(int n, const double* __restrict__ alat,
   out[k] = r;
 }
 
-// Column totals: warp w owns columns [32w, 32w+32). Per 32-row tile, lane l
-// loads row (r0+l) of each of the 32 columns (coalesced within a column),
-// the tile is transposed in shared memory, and lane l adds its column's 32
-// values in row order to its running sum.
-__global__ void __launch_bounds__(128)
+// Column totals: one warp owns 32 columns and keeps, per lane, the single
+// sequential fp64 chain of its column in row order (bit-identical to the
+// reference by construction). The chains are fed through an S-stage cp.async
+// ring of 32x32 tiles in shared memory: lane l copies row r0+l of each of the
+// 32 columns (coalesced 256 B per column), so the loads of tiles t+1..t+S-1
+// are in flight while the lanes add tile t. Rows are padded to 33 doubles so
+// the transposed reads are conflict-free.
+constexpr int kTotStages = 8;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__global__ void __launch_bounds__(32)
     column_totals_kernel(const double* __restrict__ cost, int M, int B, double* __restrict__ out) {
-  __shared__ double tile[4][32][33];
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int c0 = (blockIdx.x * 4 + w) * 32;
-  if (c0 >= B) return;
-  double (*t)[33] = tile[w];
-  double sum = 0.0;
-  for (int r0 = 0; r0 < M; r0 += 32) {
-    const int r = r0 + l;
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const int c = c0 + k;
-      t[k][l] = (r < M && c < B) ? cost[(long long)c * M + r] : 0.0;
+  extern __shared__ __align__(16) double ring[];  // [kTotStages][32][33]
+  const int l = threadIdx.x;
+  const int c0 = blockIdx.x * 32;
+  const int ntiles = (M + 31) / 32;
+  auto issue = [&](int t) {
+    if (t < ntiles) {
+      double* tile = ring + (t % kTotStages) * 32 * 33;
+      const int r = t * 32 + l;
+      if (r < M)
+        for (int k = 0; k < 32 && c0 + k < B; ++k)
+          cp_async8(&tile[k * 33 + l], &cost[(long long)(c0 + k) * M + r]);
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  for (int t = 0; t < kTotStages - 1; ++t) issue(t);
+  double sum = 0.0;
+  for (int t = 0; t < ntiles; ++t) {
+    issue(t + kTotStages - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kTotStages - 1) : "memory");
     __syncwarp();
-    const int n = min(32, M - r0);
-    for (int k = 0; k < n; ++k) sum = __dadd_rn(sum, t[l][k]);
+    const double* tile = ring + (t % kTotStages) * 32 * 33;
+    const int n = min(32, M - t * 32);
+    for (int k = 0; k < n; ++k) sum = __dadd_rn(sum, tile[l * 33 + k]);
     __syncwarp();
   }
   if (c0 + l < B) out[c0 + l] = sum;
@@ -210,8 +227,9 @@ cudaError_t launch_haversine_pairs(int n, const double* alat, const double* alon
 
 cudaError_t launch_column_totals(const double* cost, int M, int B, double* out, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  const int blocks = (B + 127) / 128;
-  column_totals_kernel<<<blocks, 128, 0, st>>>(cost, M, B, out);
+  const size_t smem = sizeof(double) * kTotStages * 32 * 33;
+  cudaFuncSetAttribute(column_totals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  column_totals_kernel<<<(B + 31) / 32, 32, smem, st>>>(cost, M, B, out);
   return cudaGetLastError();
 }
 

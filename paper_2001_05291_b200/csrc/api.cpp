@@ -458,7 +458,11 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // sweep. Permutations for a chunk of passes are generated on the host
   // while the device runs the previous chunk.
   const bool inkernel = n > 1 || (long long)maxV * M <= (64ll << 10);
-  int kchunk = inkernel ? (int)std::max<long long>(1, std::min<long long>(64, (16ll << 20) / (8ll * std::max(M, 1)))) : 1;
+  // passes per host round trip: in-kernel mode runs them in one launch; the
+  // sweep mode enqueues (sweep, pass) launch pairs that exit at once when the
+  // scenario is done, so the host only synchronises once per chunk
+  int kchunk = (int)std::max<long long>(
+      1, std::min<long long>(inkernel ? 64 : 16, (16ll << 20) / (8ll * std::max(M, 1))));
   if (const char* e = std::getenv("FLEETPLACE_KPASSES")) kchunk = std::max(1, std::atoi(e));
   const size_t chunk_ints = 2ull * kchunk * M + 2;
   if (ctx->perm_cap < chunk_ints) {
@@ -485,11 +489,21 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   while (n_active > 0) {
     h2d(run.d_active.p, active.data(), n, st);
     h2d(run.d_perm.p, ctx->h_perm[buf], 2ull * kchunk * M, st);
-    check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p, kchunk, inkernel,
-                           cfg->max_passes, M, tabu, tenure, cfg->debug_check_deltas != 0, maxV,
-                           maxB, maxK, st, threads),
-          "pass_kernel");
-    ctx->launches += (M > 0 && !inkernel) ? 2 : 1;
+    if (inkernel) {
+      check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p, kchunk, true,
+                             cfg->max_passes, M, tabu, tenure, cfg->debug_check_deltas != 0, maxV,
+                             maxB, maxK, st, threads),
+            "pass_kernel");
+      ctx->launches += 1;
+    } else {
+      for (int k = 0; k < kchunk; ++k) {
+        check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p + 2ll * k * M, 1,
+                               false, cfg->max_passes, M, tabu, tenure,
+                               cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads),
+              "pass_kernel");
+        ctx->launches += M > 0 ? 2 : 1;
+      }
+    }
     // next chunk's permutations while the device works
     const int nb = buf ^ 1;
     gen_chunk(ctx->h_perm[nb]);

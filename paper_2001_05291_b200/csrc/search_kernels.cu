@@ -680,160 +680,131 @@ __device__ bool exact_accept_single(const Scenario& s, Shared& sh, int j, double
 }
 
 // Processes the pair (i, j) exactly as try_move x3 (proj/src/search.cpp:277-303,
-// 333-341). Block-cooperative; returns with the block synchronised.
+// 333-341). Block-cooperative; every thread screens each move redundantly
+// from the (block-uniform) state, so barriers are only needed around state
+// changes and exact sums. Returns with the block synchronised.
 template <int NT>
 __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int i, int q,
                              bool tabu, long long tenure, bool debug) {
   const int j = sm.pb[q];
   const long long exp = sh.c.tick + tenure;
-  // ---- takeover: thread 0 screens, the block settles the exact sum if needed
-  if (threadIdx.x == 0) {
-    sh.c.evaluations += 1;
-    sh.bi[4] = 0;  // 1: accept, 2: needs the exact sums
-    if (i < sh.c.psize && s.pkind[i] == POOL_IDLE) {
-      const int g = s.pidx[i];
-      if (compat_vm(s.vfixed[g], s.ro[j])) {
-        const double newc = cost_at(s, s.vbase[g], j);
-        const double mcj = s.mc[j];
-        if (newc - mcj < 0.0) {
-          sh.bi[4] = mcj - newc > single_bound(s, sh) ? 1 : 2;
-          sh.bi[6] = g;
-          sh.bd0 = newc;
+  // ---- takeover (proj/src/search.cpp:82-101)
+  if (i < sh.c.psize && s.pkind[i] == POOL_IDLE) {
+    const int g = s.pidx[i];
+    const double newc = cost_at(s, s.vbase[g], j);
+    const double mcj = s.mc[j];
+    if (compat_vm(s.vfixed[g], s.ro[j]) && newc - mcj < 0.0) {
+      int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
+      if (!acc) acc = exact_accept_single<NT>(s, sh, j, newc) ? 3 : 0;
+      if (acc) {
+        const int loser = s.mv[j];
+        __syncthreads();  // everyone has read the pre-move state
+        if (threadIdx.x == 0) {
+          apply_takeover(s, sh, j, g, i);
+          sh.c.applied += 1;
+          sh.c.pass_applied += 1;
+          if (acc == 3) {
+            sh.c.total_exact = sh.xs;
+            sh.c.total_ver = (long long)sh.c.applied;
+          }
+          if (tabu) s.exp_take[g] = exp;
+          if (debug) debug_check(s, sh);
         }
+        __syncthreads();
+        const long long a2 = ph_now();
+        bits_after_substitution<NT>(s, sh, sm, q, j, loser, g);
+        PH_ADD(sh, 7, a2);
       }
     }
   }
-  __syncthreads();
-  if (sh.bi[4] == 2) {
-    const bool acc = exact_accept_single<NT>(s, sh, j, sh.bd0);
-    if (threadIdx.x == 0) sh.bi[4] = acc ? 3 : 0;  // 3: accepted, exact total known
-    __syncthreads();
-  }
-  if (sh.bi[4]) {
-    if (threadIdx.x == 0) {
-      const int g = sh.bi[6];
-      sh.bi[5] = s.mv[j];
-      apply_takeover(s, sh, j, g, i);
-      sh.c.applied += 1;
-      sh.c.pass_applied += 1;
-      if (sh.bi[4] == 3) {
-        sh.c.total_exact = sh.xs;
-        sh.c.total_ver = (long long)sh.c.applied;
-      }
-      if (tabu) s.exp_take[g] = exp;
-      if (debug) debug_check(s, sh);
-    }
-    __syncthreads();
-    const long long a2 = ph_now();
-    bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
-    PH_ADD(sh, 7, a2);
-  }
-  // relocation preconditions (on the state the takeover left)
-  if (threadIdx.x == 0) {
-    sh.c.evaluations += 1;
-    int t = -1, mover = -1;
-    if (i < sh.c.psize && s.pkind[i] == POOL_EMPTY) {
-      t = s.pidx[i];
-      mover = s.mv[j];
-      if (s.vfixed[mover] && s.bheli[t]) t = -1;
-    }
-    sh.bi[0] = t;
-    sh.bi[1] = mover;
-  }
-  __syncthreads();
-  // ---- relocation
-  const int t = sh.bi[0], mover = sh.bi[1];
-  if (t >= 0) {
-    relocation_classes<NT>(s, sh, sm, t);
-    const uint8_t cls = sm.cls[mover];
-    bool acc = cls == CLS_ACC;
-    bool exact_known = false;
-    if (cls == CLS_NEG || cls == CLS_AMB) {
-      const long long f0 = ph_now();
-      const double* col = s.cost + (long long)t * s.M;
-      bool neg = cls == CLS_NEG;
-      if (!neg) neg = exact_reloc_quick<NT>(s, sh, col, mover, sm.xidx, 2 * NT) < 0.0;
-      if (neg) {
-        const double S = exact_total<NT>(s, sh);
-        const double S2 = exact_chain<NT>(s, sh, 2, -1, 0.0, mover, col);
-        acc = S2 < S;
-        exact_known = true;
-        if (threadIdx.x == 0) sh.bd0 = S2;
-      }
-      if (threadIdx.x == 0) sh.c.fallbacks += 1;
-      PH_ADD(sh, 4, f0);
-      __syncthreads();
-    }
-    if (acc) {
-      const long long a0 = ph_now();
-      apply_relocate<NT>(s, sh, mover, t, i);
-      PH_ADD(sh, 8, a0);
-      const long long a1 = ph_now();
-      bits_after_relocation<NT>(s, sh, sm, mover, sm.xlist, sm.xlist_cap);
-      PH_ADD(sh, 6, a1);
-      if (threadIdx.x == 0) {
-        sh.c.applied += 1;
-        sh.c.pass_applied += 1;
-        if (exact_known) {
-          sh.c.total_exact = sh.bd0;
-          sh.c.total_ver = (long long)sh.c.applied;
+  // ---- relocation (proj/src/search.cpp:103-129), on the state left behind
+  if (i < sh.c.psize && s.pkind[i] == POOL_EMPTY) {
+    const int t = s.pidx[i];
+    const int mover = s.mv[j];
+    if (!(s.vfixed[mover] && s.bheli[t])) {
+      relocation_classes<NT>(s, sh, sm, t);
+      const uint8_t cls = sm.cls[mover];
+      bool acc = cls == CLS_ACC;
+      bool exact_known = false;
+      double after = 0.0;
+      if (cls == CLS_NEG || cls == CLS_AMB) {
+        const long long f0 = ph_now();
+        const double* col = s.cost + (long long)t * s.M;
+        bool neg = cls == CLS_NEG;
+        if (!neg) neg = exact_reloc_quick<NT>(s, sh, col, mover, sm.xidx, 2 * NT) < 0.0;
+        if (neg) {
+          const double S = exact_total<NT>(s, sh);
+          after = exact_chain<NT>(s, sh, 2, -1, 0.0, mover, col);
+          acc = after < S;
+          exact_known = true;
         }
-        if (tabu) {
-          // outer {Relocate, target base id} then inner {Relocate, mover id};
-          // the second insert wins when the two ids coincide.
-          const int ko = s.brk[t], ki = s.vrk[mover];
-          s.exp_rel[ko] = exp;
-          s.role_rel[ko] = ROLE_OUTER;
-          s.exp_rel[ki] = exp;
-          s.role_rel[ki] = ROLE_INNER;
-          sh.jexp_max = max(sh.jexp_max, exp);
-        }
-        if (debug) debug_check(s, sh);
+        if (threadIdx.x == 0) sh.c.fallbacks += 1;
+        PH_ADD(sh, 4, f0);
       }
-      __syncthreads();
+      if (acc) {
+        const long long a0 = ph_now();
+        apply_relocate<NT>(s, sh, mover, t, i);
+        PH_ADD(sh, 8, a0);
+        const long long a1 = ph_now();
+        bits_after_relocation<NT>(s, sh, sm, mover, sm.xlist, sm.xlist_cap);
+        PH_ADD(sh, 6, a1);
+        if (threadIdx.x == 0) {
+          sh.c.applied += 1;
+          sh.c.pass_applied += 1;
+          if (exact_known) {
+            sh.c.total_exact = after;
+            sh.c.total_ver = (long long)sh.c.applied;
+          }
+          if (tabu) {
+            // outer {Relocate, target base id} then inner {Relocate, mover id};
+            // the second insert wins when the two ids coincide.
+            const int ko = s.brk[t], ki = s.vrk[mover];
+            s.exp_rel[ko] = exp;
+            s.role_rel[ko] = ROLE_OUTER;
+            s.exp_rel[ki] = exp;
+            s.role_rel[ki] = ROLE_INNER;
+            sh.jexp_max = max(sh.jexp_max, exp);
+          }
+          if (debug) debug_check(s, sh);
+        }
+        __syncthreads();
+      }
     }
   }
-  // ---- reassignment
-  if (threadIdx.x == 0) {
-    sh.c.evaluations += 1;
-    sh.bi[4] = 0;
+  // ---- reassignment (proj/src/search.cpp:131-148)
+  {
     const int g = s.mv[i], l = s.mv[j];
     if (g != l && compat_vm(s.vfixed[g], s.ro[j])) {
       const double newc = cost_at(s, s.vbase[g], j);
       const double mcj = s.mc[j];
       if (newc - mcj < 0.0) {
-        sh.bi[4] = mcj - newc > single_bound(s, sh) ? 1 : 2;
-        sh.bi[6] = g;
-        sh.bd0 = newc;
+        int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
+        if (!acc) acc = exact_accept_single<NT>(s, sh, j, newc) ? 3 : 0;
+        if (acc) {
+          __syncthreads();
+          if (threadIdx.x == 0) {
+            apply_reassign(s, sh, j, g);
+            sh.c.applied += 1;
+            sh.c.pass_applied += 1;
+            if (acc == 3) {
+              sh.c.total_exact = sh.xs;
+              sh.c.total_ver = (long long)sh.c.applied;
+            }
+            if (tabu) s.exp_reas[g] = exp;
+            if (debug) debug_check(s, sh);
+          }
+          __syncthreads();
+          const long long a2 = ph_now();
+          bits_after_substitution<NT>(s, sh, sm, q, j, l, g);
+          PH_ADD(sh, 7, a2);
+        }
       }
     }
   }
-  __syncthreads();
-  if (sh.bi[4] == 2) {
-    const bool acc = exact_accept_single<NT>(s, sh, j, sh.bd0);
-    if (threadIdx.x == 0) sh.bi[4] = acc ? 3 : 0;
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    sh.c.evaluations += 3;
+    sh.c.tick += 1;
   }
-  if (sh.bi[4]) {
-    if (threadIdx.x == 0) {
-      const int g = sh.bi[6];
-      sh.bi[5] = s.mv[j];
-      apply_reassign(s, sh, j, g);
-      sh.c.applied += 1;
-      sh.c.pass_applied += 1;
-      if (sh.bi[4] == 3) {
-        sh.c.total_exact = sh.xs;
-        sh.c.total_ver = (long long)sh.c.applied;
-      }
-      if (tabu) s.exp_reas[g] = exp;
-      if (debug) debug_check(s, sh);
-    }
-    __syncthreads();
-    const long long a2 = ph_now();
-    bits_after_substitution<NT>(s, sh, sm, q, j, sh.bi[5], sh.bi[6]);
-    PH_ADD(sh, 7, a2);
-  }
-  if (threadIdx.x == 0) sh.c.tick += 1;
   __syncthreads();
 }
 
@@ -882,7 +853,7 @@ __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int 
     sh.lim_ra = lim_ra;
   }
   __syncthreads();
-  if (tabu) {
+  if (tabu && sh.jexp_max > sh.t0) {
     const long long T = sh.t0;
     for (int v = threadIdx.x; v < s.V; v += NT) {
       const int k = s.vrk[v];
@@ -933,6 +904,7 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
   const int M = s.M, nwd = s.nwd;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   int p = 0;
+  int parity = 0;
   if (threadIdx.x == 0) sh.c.counts[0] += 1;
   while (p < M) {
     const long long c0 = ph_now();
@@ -1006,36 +978,35 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
       n_valid = (int)__reduce_add_sync(FULL, (unsigned)n_valid);
       n_blk = (int)__reduce_add_sync(FULL, (unsigned)n_blk);
       evpos = __reduce_min_sync(FULL, evpos);
+      // one barrier per step: summaries are double-buffered by step parity and
+      // every warp combines them itself (no broadcast round)
+      int* ws = sm.wsum + (parity & 1) * NW * 3;
+      parity ^= 1;
       if (l == 0) {
-        sm.wsum[w * 3 + 0] = evpos;
-        sm.wsum[w * 3 + 1] = n_valid;
-        sm.wsum[w * 3 + 2] = n_blk;
+        ws[w * 3 + 0] = evpos;
+        ws[w * 3 + 1] = n_valid;
+        ws[w * 3 + 2] = n_blk;
       }
       __syncthreads();
-      if (w == 0) {
-        const int e = l < NW ? sm.wsum[l * 3 + 0] : INT_MAX;
-        int nv = l < NW ? sm.wsum[l * 3 + 1] : 0;
-        int nb = l < NW ? sm.wsum[l * 3 + 2] : 0;
-        const unsigned any = __ballot_sync(FULL, e != INT_MAX);
-        const int wstar = any ? __ffs(any) - 1 : 32;
-        if (l > wstar) {
-          nv = 0;
-          nb = 0;
-        }
-        nv = (int)__reduce_add_sync(FULL, (unsigned)nv);
-        nb = (int)__reduce_add_sync(FULL, (unsigned)nb);
-        const int evp = any ? __shfl_sync(FULL, e, wstar) : INT_MAX;
-        if (l == 0) {
-          sh.ev = evp;
-          sh.c.counts[1] += 1;
-          sh.c.skips_inner += (unsigned long long)nb;
-          sh.c.evaluations += 3ull * (unsigned long long)(nv - nb);
-          if (tabu) sh.c.tick += nv;  // every position before the event is one pair
-          if (nb > 0) sh.c.pass_skipped = 1;
-        }
+      const int e = l < NW ? ws[l * 3 + 0] : INT_MAX;
+      int nv = l < NW ? ws[l * 3 + 1] : 0;
+      int nb = l < NW ? ws[l * 3 + 2] : 0;
+      const unsigned any = __ballot_sync(FULL, e != INT_MAX);
+      const int wstar = any ? __ffs(any) - 1 : 32;
+      if (l > wstar) {
+        nv = 0;
+        nb = 0;
       }
-      __syncthreads();
-      ev = sh.ev;
+      nv = (int)__reduce_add_sync(FULL, (unsigned)nv);
+      nb = (int)__reduce_add_sync(FULL, (unsigned)nb);
+      ev = any ? __shfl_sync(FULL, e, wstar) : INT_MAX;
+      if (threadIdx.x == 0) {
+        sh.c.counts[1] += 1;
+        sh.c.skips_inner += (unsigned long long)nb;
+        sh.c.evaluations += 3ull * (unsigned long long)(nv - nb);
+        if (tabu) sh.c.tick += nv;  // every position before the event is one pair
+        if (nb > 0) sh.c.pass_skipped = 1;
+      }
       p = ev != INT_MAX ? ev : (int)min((long long)M, (long long)(w0 + 32 * NW) * 32);
       if (ev != INT_MAX) break;
     }
@@ -1044,9 +1015,12 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
     // event at position p
     bool outer_ev = false;
     if (tabu) {
-      const int v = s.mvp[p];
       const int off = p - p_seg;
-      outer_ev = off < lim_ro || (off < sm.lim_j[v] && sm.outer_j[v]);
+      outer_ev = off < lim_ro;
+      if (!outer_ev && nj > 0) {
+        const int v = s.mvp[p];
+        outer_ev = off < sm.lim_j[v] && sm.outer_j[v];
+      }
     }
     if (outer_ev) {
       if (threadIdx.x == 0) {
@@ -1119,6 +1093,7 @@ __global__ void __launch_bounds__(256) prep_kernel(Scenario* scs, const int32_t*
                                                    const int32_t* __restrict__ pb) {
   if (!active[blockIdx.y]) return;
   const Scenario s = scs[blockIdx.y];
+  if (s.ctr->done) return;  // finished earlier in this chunk of launches
   const int warps = blockDim.x >> 5;
   prep_words(s, pb, blockIdx.x * warps + (threadIdx.x >> 5), gridDim.x * warps);
 }
@@ -1128,7 +1103,7 @@ __global__ void __launch_bounds__(256) prep_kernel(Scenario* scs, const int32_t*
 size_t pass_smem_core(int V, int NT) {
   const int NW = NT / 32;
   return align16(4ull * V) + align16(V) + align16(V) + 2 * align16(8ull * NW * V) +
-         align16(8ull * NW * 32) + align16(4ull * NW * 3) + 3 * align16(4ull * V) + align16(V) +
+         align16(8ull * NW * 32) + align16(8ull * NW * 3) + 3 * align16(4ull * V) + align16(V) +
          align16(8ull * NT) + 64;
 }
 size_t pass_smem_state(int V, int B, int K) {
@@ -1144,6 +1119,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
                 int debug_i, int state_in_smem) {
   if (!active[blockIdx.x]) return;
   const Scenario g = scs[blockIdx.x];
+  if (g.ctr->done) return;  // finished earlier in this chunk of launches
   Scenario s = g;
   const bool tabu = tabu_i != 0, debug = debug_i != 0;
   __shared__ Shared sh;
@@ -1163,7 +1139,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   sm.acc_sum = reinterpret_cast<double*>(take(8ull * NW * V));
   sm.acc_abs = reinterpret_cast<double*>(take(8ull * NW * V));
   sm.stage = reinterpret_cast<double*>(take(8ull * NW * 32));
-  sm.wsum = reinterpret_cast<int*>(take(4ull * NW * 3));
+  sm.wsum = reinterpret_cast<int*>(take(8ull * NW * 3));
   sm.xidx = reinterpret_cast<int*>(take(8ull * NT));
   sm.xlist = s.scratch;
   sm.xlist_cap = s.M;

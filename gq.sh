@@ -1,5 +1,6 @@
 #!/bin/bash
-python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-extras 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['phase_ms'], d['search_stats'], d['gpu_launches'])"
-timeout 600 python tools/scale_probe.py --c5 296 2>&1 | grep "c5 batch" | head -1
-timeout 600 python tools/scale_probe.py --c3 --passes 1,10 2>&1 | tail -2
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -q -x 2>&1 | grep -E "FAILED|passed|failed" | head -3
+python tools/profile_case.py --passes 4 > gpurun_out/plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:pass_kernel -s 1 -c 1 -o gpurun_out/pass_full3 python tools/profile_case.py --passes 4 > gpurun_out/ncu_full.log 2>&1
+tail -1 gpurun_out/ncu_full.log

@@ -287,7 +287,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
-      invb, exp_take, exp_reas, exp_rel, role_rel, cls_cache, cls_ver, cls_any, imp, mem, scratch, ctr, cost, total;
+      invb, exp_take, exp_reas, exp_rel, role_rel, rA, rE, rU, rcnt, imp, mem, scratch, ctr, cost, total;
 };
 
 Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
@@ -318,9 +318,10 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   L.exp_reas = put(8ull * V);
   L.exp_rel = put(8ull * K);
   L.role_rel = put(K);
-  L.cls_cache = put((size_t)B * V);
-  L.cls_ver = put(8ull * B);
-  L.cls_any = put(B);
+  L.rA = put(8ull * B * V);
+  L.rE = put(8ull * B * V);
+  L.rU = put(8ull * B * V);
+  L.rcnt = put(4ull * B);
   const size_t nwd = ((size_t)M + 31) / 32;
   L.imp = put(4ull * V * nwd);
   L.mem = put(4ull * V * nwd);
@@ -403,7 +404,6 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     if (B) std::memcpy(hb + L.bveh, h.bveh.data(), 4ull * B);
     if (h.psize) std::memcpy(hb + L.pkind, h.pkind.data(), 4ull * h.psize);
     if (h.psize) std::memcpy(hb + L.pidx, h.pidx.data(), 4ull * h.psize);
-    std::memset(hb + L.cls_ver, 0xff, 8ull * B);  // -1: no cached classes
     if (!dev_tables[s] && (size_t)M * B)
       std::memcpy(hb + L.cost, host_tables[s], 8ull * M * B);
     fpk::Scenario& S = run.arena.scs[s];
@@ -428,9 +428,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.exp_reas = reinterpret_cast<long long*>(db + L.exp_reas);
     S.exp_rel = reinterpret_cast<long long*>(db + L.exp_rel);
     S.role_rel = db + L.role_rel;
-    S.cls_cache = db + L.cls_cache;
-    S.cls_ver = reinterpret_cast<long long*>(db + L.cls_ver);
-    S.cls_any = db + L.cls_any;
+    S.rA = reinterpret_cast<double*>(db + L.rA);
+    S.rE = reinterpret_cast<double*>(db + L.rE);
+    S.rU = reinterpret_cast<double*>(db + L.rU);
+    S.rcnt = reinterpret_cast<int32_t*>(db + L.rcnt);
     S.imp = reinterpret_cast<uint32_t*>(db + L.imp);
     S.mem = reinterpret_cast<uint32_t*>(db + L.mem);
     S.scratch = reinterpret_cast<int32_t*>(db + L.scratch);
@@ -472,8 +473,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     ctx->perm_cap = chunk_ints;
   }
   run.d_perm.alloc(chunk_ints);
-  check(fpk::launch_init(run.d_scs.p, n, st), "init_kernel");
-  ctx->launches += 1;
+  check(fpk::launch_init(run.d_scs.p, n, maxB, maxV, st), "init_kernel");
+  ctx->launches += 2;
   PermStream rng(cfg->seed);
   auto gen_chunk = [&](int32_t* buf) {
     for (int k = 0; k < kchunk; ++k) {

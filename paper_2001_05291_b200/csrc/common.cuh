@@ -74,9 +74,14 @@ struct Scenario {
   uint8_t* role_rel;         // [K]
   // relocation-class cache: per target base t, the per-vehicle classes of
   // the relocation delta, valid while no move has been applied since
-  uint8_t* cls_cache;        // [B*V]
-  long long* cls_ver;        // [B] applied-move count the entry was built at
-  uint8_t* cls_any;          // [B] some compatible vehicle's class is not POS
+  // relocation-delta table, row t = an empty base, column v = a vehicle:
+  //  rA ~ X = sum over v's missions of (cost(m, t) - mc[m]) (exact reals),
+  //  |rA - X| <= rE, rU >= sum |cost(m, t) - mc[m]|; rcnt[t] = vehicles whose
+  //  relocation to t is not certainly non-improving
+  double* rA;                // [B*V]
+  double* rE;                // [B*V]
+  double* rU;                // [B*V]
+  int32_t* rcnt;             // [B]
   // perm_b-position bitsets, word w covers positions [32w, 32w+32):
   //  imp[g]: reassigning / taking over that position's mission to vehicle g
   //          would lower its cost (mv != g, compatible, cost(j, base(g)) < mc[j])

@@ -30,7 +30,7 @@ cudaError_t launch_objective(const double* cost, int M, const int32_t* vb, const
 cudaError_t launch_candidate_delta(const double* cost, int M, const int32_t* vb, const int32_t* mv,
                                    int kind, int j, int newcol, int mover, double* out,
                                    cudaStream_t st);
-cudaError_t launch_init(Scenario* d_scs, int n_scn, cudaStream_t stream);
+cudaError_t launch_init(Scenario* d_scs, int n_scn, int maxB, int maxV, cudaStream_t stream);
 cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream);
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,

@@ -374,8 +374,17 @@ __device__ __forceinline__ void put_bit(uint32_t* w, uint32_t bit, bool on) {
 // After mission j at position q moved from `loser` to `gain` (new cost in
 // mcp[q]): refresh bit q of every imp row, move its mem bit. Block-wide.
 template <int NT>
+__device__ void table_after_substitution(const Scenario& s, const Shared& sh, int j, int loser,
+                                         int gain, double mc_old, double mc_new, int nl, int ng);
+
+// After mission j at position q moved from `loser` (cost mc_old, nl missions)
+// to `gain` (new cost in mcp[q], ng missions): refresh bit q of every imp
+// row, move its mem bit, and patch the relocation-delta table, in one
+// block-wide phase with a single barrier.
+template <int NT>
 __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Smem& sm, int q,
-                                        int j, int loser, int gain) {
+                                        int j, int loser, int gain, double mc_old, int nl,
+                                        int ng) {
   const int wd = q >> 5;
   const uint32_t bit = 1u << (q & 31);
   for (int g = threadIdx.x; g < s.V; g += NT) {
@@ -388,6 +397,7 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     s.mem[(long long)loser * s.nwd + wd] &= ~bit;
     s.mem[(long long)gain * s.nwd + wd] |= bit;
   }
+  table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, s.mcp[q], nl, ng);
   __syncthreads();
 }
 
@@ -494,32 +504,64 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
   }
 }
 
-// Relocation classes of every vehicle towards empty base t, into sm.cls,
-// through the (t, version) cache. The per-vehicle sums use warp-private
-// accumulators: lanes of a warp holding the same vehicle are grouped with
-// __match_any_sync and their leader adds the group's terms, so no shared
-// memory atomics are needed (fp64 shared atomics are CAS loops). Any
-// summation order is fine: the class uses a rigorous error bound.
+// ---- relocation-delta table ------------------------------------------------
+//
+// eval_relocate's quick delta (proj/src/search.cpp:121-127) depends only on
+// (target base t, mover v): D(t, v) = fixed-order fp64 sum over v's missions
+// of fl(cost(m, t) - mc[m]). The table keeps, per empty base t and vehicle v,
+// an any-order value rA with |rA - X| <= rE around the exact real sum X and an
+// upper bound rU >= sum |cost - mc|; then |D - rA| <= rE + (n + 2) 2^-52 rU
+// (n = v's mission count), which classifies the relocation rigorously. Rows
+// are built once by a sweep (table_rows_kernel), patched O(P) per
+// reassignment / takeover (one term leaves the loser's sum, one enters the
+// gainer's) and shifted per relocation (a relocation of x to t changes every
+// D(t', x) by -D(t, x)); the vacated base gets a fresh row. Rounding of every
+// patch is added to rE, so classes stay rigorous; a row whose bounds got too
+// loose to classify (AMB) is rebuilt exactly.
+
+// Class of one (t, v) entry from its values (n = v's mission count).
+__device__ __forceinline__ bool table_unsettled(double A, double E0, double U, int n, double bt) {
+  if (n == 0 || U == 0.0) return false;  // no terms, or every term exactly zero
+  const double E = E0 + (double)(n + 2) * kTwoPowM52 * U * 1.0001;
+  return !(A - E > 0.0);
+  (void)bt;
+}
+
+__device__ __forceinline__ uint8_t table_class_n(const Scenario& s, const Shared& sh, int t, int v,
+                                                 int n) {
+  if (s.vfixed[v] && s.bheli[t]) return CLS_POS;
+  const long long k = (long long)t * s.V + v;
+  const double U = s.rU[k];
+  if (n == 0 || U == 0.0) return CLS_POS;  // no terms, or every term exactly zero
+  const double A = s.rA[k];
+  const double E = s.rE[k] + (double)(n + 2) * kTwoPowM52 * U * 1.0001;
+  if (A - E > 0.0) return CLS_POS;
+  if (A + E + single_bound(s, sh) < 0.0) return CLS_ACC;
+  if (A + E < 0.0) return CLS_NEG;
+  return CLS_AMB;
+}
+
+__device__ __forceinline__ uint8_t table_class(const Scenario& s, const Shared& sh, int t, int v) {
+  return table_class_n(s, sh, t, v, s.vcount[v]);
+}
+
+// Fresh row t from one streaming pass over the missions (warp-private
+// accumulators; lanes of a warp holding the same vehicle are grouped with
+// __match_any_sync so no fp64 shared atomics are needed). Block-wide; writes
+// rA/rE/rU and rcnt[t].
 template <int NT>
-__device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm, int t) {
-  const long long ver = (long long)sh.c.applied;
-  const int V = s.V;
-  if (s.cls_ver[t] == ver) {  // uniform: all threads read the same word
-    for (int v = threadIdx.x; v < V; v += NT) sm.cls[v] = s.cls_cache[(long long)t * V + v];
-    __syncthreads();
-    return;
-  }
-  const long long r0 = ph_now();
-  if (threadIdx.x == 0) sh.c.counts[3] += 1;
+__device__ void table_row_fresh(const Scenario& s, Shared& sh, double* acc_sum, double* acc_abs,
+                                double* stage, int t) {
   constexpr int NW = NT / 32;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  double* as = sm.acc_sum + (long long)w * V;
-  double* aa = sm.acc_abs + (long long)w * V;
+  const int V = s.V;
+  double* as = acc_sum + (long long)w * V;
+  double* aa = acc_abs + (long long)w * V;
   for (int v = l; v < V; v += 32) {
     as[v] = 0.0;
     aa[v] = 0.0;
   }
-  double* st = sm.stage + w * 32;
+  double* st = stage + w * 32;
   __syncwarp();
   const double* col = s.cost + (long long)t * s.M;
   constexpr int UR = 8;  // independent 32-mission groups in flight per warp
@@ -556,26 +598,123 @@ __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm
     }
   }
   __syncthreads();
-  const double bt = single_bound(s, sh);
-  const bool heli = s.bheli[t];
-  int any = 0;
+  if (threadIdx.x == 0) sh.tmp = 0;
+  __syncthreads();
+  int cnt = 0;
   for (int v = threadIdx.x; v < V; v += NT) {
     double sum = 0.0, abs = 0.0;
     for (int k = 0; k < NW; ++k) {
-      sum += sm.acc_sum[(long long)k * V + v];
-      abs += sm.acc_abs[(long long)k * V + v];
+      sum += acc_sum[(long long)k * V + v];
+      abs += acc_abs[(long long)k * V + v];
     }
-    const uint8_t c = (s.vfixed[v] && heli) ? CLS_POS : reloc_class(sum, abs, s.vcount[v], bt);
+    const int n = s.vcount[v];
+    const long long k = (long long)t * V + v;
+    const double U = abs * (1.0 + (double)(n + 2) * kTwoPowM52);
+    s.rA[k] = sum;
+    s.rU[k] = U;
+    s.rE[k] = (double)(n + 2) * kTwoPowM52 * U;
+    cnt += table_class(s, sh, t, v) != CLS_POS;
+  }
+  if (cnt) atomicAdd(&sh.tmp, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) s.rcnt[t] = sh.tmp;
+  __syncthreads();
+}
+
+// Relocation classes of every vehicle towards empty base t into sm.cls; a
+// row with an unsettled class is rebuilt exactly first.
+template <int NT>
+__device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm, int t) {
+  int amb = 0;
+  for (int v = threadIdx.x; v < s.V; v += NT) {
+    const uint8_t c = table_class(s, sh, t, v);
     sm.cls[v] = c;
-    s.cls_cache[(long long)t * V + v] = c;
-    any |= c != CLS_POS;
+    amb |= c == CLS_AMB;
   }
-  any = __syncthreads_or(any);
-  if (threadIdx.x == 0) {
-    s.cls_ver[t] = ver;
-    s.cls_any[t] = any ? 1 : 0;
+  amb = __syncthreads_or(amb);
+  if (amb) {
+    const long long r0 = ph_now();
+    if (threadIdx.x == 0) sh.c.counts[3] += 1;
+    table_row_fresh<NT>(s, sh, sm.acc_sum, sm.acc_abs, sm.stage, t);
+    for (int v = threadIdx.x; v < s.V; v += NT) sm.cls[v] = table_class(s, sh, t, v);
+    __syncthreads();
+    PH_ADD(sh, 5, r0);
   }
-  PH_ADD(sh, 5, r0);
+}
+
+// One term enters or leaves D(t, v): rA +/-= d, the bounds widened by the
+// rounding of d and of the update.
+__device__ __forceinline__ void table_patch(const Scenario& s, int t, int v, double d, bool add) {
+  const long long k = (long long)t * s.V + v;
+  const double A = add ? s.rA[k] + d : s.rA[k] - d;
+  s.rA[k] = A;
+  s.rE[k] += 2.0 * kTwoPowM52 * (fabs(d) + fabs(A));
+  const double U = s.rU[k];
+  s.rU[k] = add ? (U + fabs(d)) * (1.0 + 2.0 * kTwoPowM52)
+                : fmax(0.0, U - fabs(d)) + 2.0 * kTwoPowM52 * U;
+}
+
+// After mission j moved from `loser` (cost mc_old, nl missions before) to
+// `gain` (cost mc_new, ng missions before): patch every empty base's row and
+// its count of unsettled classes. Block-wide (one thread per empty base);
+// each entry is loaded once and patched in registers.
+template <int NT>
+__device__ void table_after_substitution(const Scenario& s, const Shared& sh, int j, int loser,
+                                         int gain, double mc_old, double mc_new, int nl, int ng) {
+  const double bt = single_bound(s, sh);
+  const bool fl = s.vfixed[loser], fg = s.vfixed[gain];
+  const long long V = s.V;
+  for (int k = threadIdx.x; k < sh.c.psize; k += NT) {
+    if (s.pkind[k] != POOL_EMPTY) continue;
+    const int t = s.pidx[k];
+    const bool heli = s.bheli[t];
+    const double c = cost_at(s, t, j);
+    const long long kl = t * V + loser, kg = t * V + gain;
+    double Al = s.rA[kl], El = s.rE[kl], Ul = s.rU[kl];
+    double Ag = s.rA[kg], Eg = s.rE[kg], Ug = s.rU[kg];
+    int delta = 0;
+    if (!(fl && heli)) delta -= table_unsettled(Al, El, Ul, nl, bt);
+    if (!(fg && heli)) delta -= table_unsettled(Ag, Eg, Ug, ng, bt);
+    const double dl = c - mc_old, dg = c - mc_new;
+    Al -= dl;
+    El += 2.0 * kTwoPowM52 * (fabs(dl) + fabs(Al));
+    Ul = fmax(0.0, Ul - fabs(dl)) + 2.0 * kTwoPowM52 * Ul;
+    Ag += dg;
+    Eg += 2.0 * kTwoPowM52 * (fabs(dg) + fabs(Ag));
+    Ug = (Ug + fabs(dg)) * (1.0 + 2.0 * kTwoPowM52);
+    if (!(fl && heli)) delta += table_unsettled(Al, El, Ul, nl - 1, bt);
+    if (!(fg && heli)) delta += table_unsettled(Ag, Eg, Ug, ng + 1, bt);
+    s.rA[kl] = Al;
+    s.rE[kl] = El;
+    s.rU[kl] = Ul;
+    s.rA[kg] = Ag;
+    s.rE[kg] = Eg;
+    s.rU[kg] = Ug;
+    if (delta) s.rcnt[t] += delta;
+  }
+}
+
+// After vehicle x moved from b_old to t (pool slot now lists b_old): every
+// other empty row shifts by -D(t, x); the vacated base gets a fresh row.
+template <int NT>
+__device__ void table_after_relocation(const Scenario& s, Shared& sh, const Smem& sm, int x, int t,
+                                       int b_old) {
+  const long long kt = (long long)t * s.V + x;
+  const double At = s.rA[kt], Et = s.rE[kt], Ut = s.rU[kt];
+  for (int k = threadIdx.x; k < sh.c.psize; k += NT) {
+    if (s.pkind[k] != POOL_EMPTY) continue;
+    const int t2 = s.pidx[k];
+    if (t2 == b_old) continue;
+    const long long k2 = (long long)t2 * s.V + x;
+    const int before = table_class(s, sh, t2, x) != CLS_POS;
+    const double A = s.rA[k2] - At;
+    s.rA[k2] = A;
+    s.rE[k2] += Et + 2.0 * kTwoPowM52 * (fabs(At) + fabs(A));
+    s.rU[k2] = (s.rU[k2] + Ut) * (1.0 + 2.0 * kTwoPowM52);
+    s.rcnt[t2] += (int)(table_class(s, sh, t2, x) != CLS_POS) - before;
+  }
+  __syncthreads();
+  table_row_fresh<NT>(s, sh, sm.acc_sum, sm.acc_abs, sm.stage, b_old);
 }
 
 // ---- moves (proj/src/search.cpp:169-220) ---------------------------------
@@ -698,6 +837,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       if (!acc) acc = exact_accept_single<NT>(s, sh, j, newc) ? 3 : 0;
       if (acc) {
         const int loser = s.mv[j];
+        const int nl = s.vcount[loser], ng = s.vcount[g];
         __syncthreads();  // everyone has read the pre-move state
         if (threadIdx.x == 0) {
           apply_takeover(s, sh, j, g, i);
@@ -712,7 +852,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         }
         __syncthreads();
         const long long a2 = ph_now();
-        bits_after_substitution<NT>(s, sh, sm, q, j, loser, g);
+        bits_after_substitution<NT>(s, sh, sm, q, j, loser, g, mcj, nl, ng);
         PH_ADD(sh, 7, a2);
       }
     }
@@ -742,11 +882,13 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         PH_ADD(sh, 4, f0);
       }
       if (acc) {
+        const int b_old = s.vbase[mover];
         const long long a0 = ph_now();
         apply_relocate<NT>(s, sh, mover, t, i);
         PH_ADD(sh, 8, a0);
         const long long a1 = ph_now();
         bits_after_relocation<NT>(s, sh, sm, mover, sm.xlist, sm.xlist_cap);
+        table_after_relocation<NT>(s, sh, sm, mover, t, b_old);
         PH_ADD(sh, 6, a1);
         if (threadIdx.x == 0) {
           sh.c.applied += 1;
@@ -781,6 +923,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
         if (!acc) acc = exact_accept_single<NT>(s, sh, j, newc) ? 3 : 0;
         if (acc) {
+          const int nl = s.vcount[l], ng = s.vcount[g];
           __syncthreads();
           if (threadIdx.x == 0) {
             apply_reassign(s, sh, j, g);
@@ -795,7 +938,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           }
           __syncthreads();
           const long long a2 = ph_now();
-          bits_after_substitution<NT>(s, sh, sm, q, j, l, g);
+          bits_after_substitution<NT>(s, sh, sm, q, j, l, g, mcj, nl, ng);
           PH_ADD(sh, 7, a2);
         }
       }
@@ -1248,7 +1391,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
               E = max(E, s.exp_take[x]);
             }
           } else {
-            st = st && s.cls_ver[x] == (long long)sh.c.applied && s.cls_any[x] == 0;
+            st = st && s.rcnt[x] == 0;
             if (tabu) {
               const int k = s.brk[x];
               F = max(F, s.exp_rel[k]);
@@ -1336,6 +1479,22 @@ __global__ void __launch_bounds__(512) init_kernel(Scenario* scs) {
   }
 }
 
+// The relocation-delta table's initial rows, one block per empty base (the
+// sweep over every empty base's column: 8*M bytes each, streamed coalesced).
+__global__ void __launch_bounds__(256) table_rows_kernel(Scenario* scs) {
+  const Scenario s = scs[blockIdx.y];
+  const int t = blockIdx.x;
+  if (t >= s.B || s.bveh[t] >= 0) return;
+  __shared__ Shared sh;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  double* acc_sum = reinterpret_cast<double*>(dyn);
+  double* acc_abs = acc_sum + 8 * s.V;
+  double* stage = acc_abs + 8 * s.V;
+  if (threadIdx.x == 0) sh.c = *s.ctr;
+  __syncthreads();
+  table_row_fresh<256>(s, sh, acc_sum, acc_abs, stage, t);
+}
+
 // Exact fixed-order final total (st.total after the last move): the cached
 // exact total when it is current, else one block-parallel exact chain.
 __global__ void __launch_bounds__(512) final_kernel(Scenario* scs) {
@@ -1390,8 +1549,11 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                              tabu, tenure, debug, V, B, K, stream);
 }
 
-cudaError_t launch_init(Scenario* d_scs, int n_scn, cudaStream_t stream) {
+cudaError_t launch_init(Scenario* d_scs, int n_scn, int maxB, int maxV, cudaStream_t stream) {
   init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
+  const size_t smem = sizeof(double) * (16ull * maxV + 8 * 32);
+  cudaFuncSetAttribute(table_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (maxB > 0) table_rows_kernel<<<dim3(maxB, n_scn), 256, smem, stream>>>(d_scs);
   return cudaGetLastError();
 }
 

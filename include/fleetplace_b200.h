@@ -122,11 +122,12 @@ typedef struct fp_search_result {
   double device_ms;              /* CUDA-event time of the device search */
   uint64_t kernel_launches;      /* kernels this call launched */
   uint64_t exact_fallbacks;      /* accept decisions settled by exact chains */
-  uint64_t phase_cycles[10];     /* SM cycles per automaton phase (scenario 0):
+  uint64_t phase_cycles[12];     /* SM cycles per automaton phase (scenario 0):
                                     row runs, row context, scan steps, event
                                     pairs, exact fallbacks, relocation prepass,
                                     relocation bit updates, substitution bit
-                                    updates, relocation apply, exact totals */
+                                    updates, relocation apply, exact totals,
+                                    table patches, per-pass setup */
   uint64_t event_counts[5];      /* scenario 0: scanned rows, scan steps, row
                                     contexts, relocation prepasses, rows settled
                                     by the O(1) eventless test */

@@ -120,7 +120,8 @@ void table_alloc(fp_ctx* ctx, int M, int B) {
     if (ctx->d_cost) cudaFree(ctx->d_cost);
     ctx->d_cost = nullptr;
     ctx->cost_cap = 0;
-    check(cudaMalloc(&ctx->d_cost, sizeof(double) * need), "cudaMalloc(table)");
+    // +2 doubles: 16-byte tail padding for the aligned bulk copies of kernel (2)
+    check(cudaMalloc(&ctx->d_cost, sizeof(double) * (need + 2)), "cudaMalloc(table)");
     ctx->cost_cap = need;
   }
   ctx->M = M;
@@ -326,7 +327,7 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   L.imp = put(4ull * V * nwd);
   L.mem = put(4ull * V * nwd);
   L.scratch = put(4ull * M + 4);
-  L.cost = own_cost ? put(8ull * M * B) : 0;
+  L.cost = own_cost ? put(8ull * M * B + 16) : 0;
   L.total = o;
   return L;
 }
@@ -549,7 +550,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     o.final_objective_km = c.final_total;
     outs[s].device_ms = ms;
     outs[s].exact_fallbacks = c.fallbacks;
-    for (int k = 0; k < 10; ++k) outs[s].phase_cycles[k] = c.cycles[k];
+    for (int k = 0; k < 12; ++k) outs[s].phase_cycles[k] = c.cycles[k];
     for (int k = 0; k < 5; ++k) outs[s].event_counts[k] = c.counts[k];
     outs[s].kernel_launches = ctx->launches;
   }

@@ -35,7 +35,7 @@ struct Counters {
   // SM cycles spent per automaton phase (thread 0's view, single-scenario
   // launches): 0 row skipping, 1 row context, 2 chunk scans, 3 event pairs,
   // 4 exact fallbacks, 5 relocation prepasses
-  unsigned long long cycles[10];  // ... 6 relocation bit updates, 7 substitution bit updates,
+  unsigned long long cycles[12];  // ... 10 table patches, 11 per-pass setup  // ... 6 relocation bit updates, 7 substitution bit updates,
                                   // 8 relocation apply, 9 exact totals
   // event counts: 0 interesting rows, 1 chunk iterations, 2 row contexts,
   // 3 relocation prepasses

@@ -397,7 +397,9 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     s.mem[(long long)loser * s.nwd + wd] &= ~bit;
     s.mem[(long long)gain * s.nwd + wd] |= bit;
   }
+  const long long tp0 = ph_now();
   table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, s.mcp[q], nl, ng);
+  PH_ADD(sh, 10, tp0);
   __syncthreads();
 }
 
@@ -1342,6 +1344,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   for (int kp = 0; kp < kpasses && !sh.c.done; ++kp) {
     const int32_t* pa = perms + 2ll * kp * M;
     sm.pb = pa + M;
+    const long long ps0 = ph_now();
     if (inkernel_prep) {
       prep_words(s, sm.pb, threadIdx.x >> 5, NW);
       __syncthreads();
@@ -1361,6 +1364,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       sh.c.pass_skipped = 0;
     }
     __syncthreads();
+    PH_ADD(sh, 11, ps0);
       int r = 0;
     while (r < M && !sh.c.error) {
       const long long b0 = ph_now();

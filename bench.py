@@ -201,32 +201,58 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
+def _kernel_rooflines(inst, t, start_ms, r, peak):
+    """Device-timed data-parallel kernels of one shape against the measured
+    HBM copy bandwidth (algorithmic bytes)."""
+    B, M, V = inst.n_bases, inst.n_missions, inst.n_vehicles
+    P = B - V
+    nwd = (M + 31) // 32
+    out = {
+        "table_kernel": {"ms": start_ms["table"], "bytes": 8 * B * M, "bound": "fp64 ALU",
+                         "note": "4 sin + 2 asin + 2 sqrt per entry; bytes are the writes"},
+        "column_totals_kernel": {"ms": start_ms["totals"], "bytes": 8 * B * M, "bound": "hbm"},
+        "search_init (exact total + relocation-table sweep)": {
+            "ms": r.stats.init_ms, "bytes": 8 * P * M + 12 * M, "bound": "hbm"},
+    }
+    if r.stats.sweep_ms > 0:
+        out["prep_kernel (per-pass bitset sweep, mean)"] = {
+            "ms": r.stats.sweep_ms / max(r.stats.passes, 1),
+            "bytes": 8 * V * M + 21 * M + 8 * V * nwd, "bound": "hbm (gathered columns)"}
+    for k in out.values():
+        k["achieved_gbs"] = k["bytes"] / (k["ms"] / 1e3) / 1e9 if k["ms"] > 0 else None
+        if k["bound"].startswith("hbm") and k["achieved_gbs"]:
+            k["frac_of_measured_hbm"] = k["achieved_gbs"] / peak
+    return out
+
+
 def extra_workloads(device: int) -> dict:
     """The other BASELINE.json shapes on this GPU (reported, not the headline):
-    c3 (2k x 100k x 100) capped at 10 passes, and one GPU's share of the c5
-    batch (512 of the 4096 independent 200 x 5k x 20 scenarios) to quiescence.
-    Device times from the library's CUDA events."""
-    import torch
+    c3 (2k x 100k x 100) capped at 10 passes, c4 (5k x 1M x 250, a 40 GB
+    table) capped at 1 pass, and one GPU's share of the c5 batch (512 of the
+    4096 independent 200 x 5k x 20 scenarios) to quiescence. Device times from
+    the library's CUDA events."""
     from paper_2001_05291_b200 import fleetplace as F
 
+    peak, _ = _peaks()
     out = {}
-    inst = F.survey_instance(2000, 100000, 100, seed=1)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    t = F.build_distance_table(inst, device=device)
-    t1 = time.perf_counter()
-    start = F.rank_bases(inst, t)
-    t2 = time.perf_counter()
-    vb, mv, pk, px = F._state_arrays(start.assignment, F.initial_pool(start, inst), inst)
-    r = F.search_arrays(inst, t, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=10),
-                        vb, mv, pk, px)
-    out["c3_10_passes"] = {
-        "workload": "2000 bases x 100k missions x 100 vehicles, tabu seed 7, max_passes 10",
-        "table_build_s_wall": t1 - t0, "rank_s_wall": t2 - t1, "search_ms": r.stats.device_ms,
-        "evaluations": r.stats.evaluations, "applied_moves": r.stats.applied_moves,
-        "move_evals_per_s": r.stats.evaluations / (r.stats.device_ms / 1e3)}
-    del t
+    for name, shape, passes in (("c3_10_passes", (2000, 100000, 100), 10),
+                                ("c4_1_pass", (5000, 1000000, 250), 1)):
+        inst = F.survey_instance(*shape, seed=1)
+        t = F.build_distance_table(inst, device=device)
+        ms = {"table": t._ctx.last_kernel_ms()}
+        start = F.rank_bases(inst, t)
+        ms["totals"] = t._ctx.last_kernel_ms()
+        vb, mv, pk, px = F._state_arrays(start.assignment, F.initial_pool(start, inst), inst)
+        r = F.search_arrays(inst, t, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu,
+                                                    max_passes=passes), vb, mv, pk, px)
+        out[name] = {
+            "workload": f"{shape[0]} bases x {shape[1]} missions x {shape[2]} vehicles, "
+                        f"tabu seed 7, max_passes {passes}",
+            "search_ms": r.stats.device_ms, "evaluations": r.stats.evaluations,
+            "applied_moves": r.stats.applied_moves,
+            "move_evals_per_s": r.stats.evaluations / (r.stats.device_ms / 1e3),
+            "kernels": _kernel_rooflines(inst, t, ms, r, peak)}
+        del t
     n = 512
     insts, starts, tabs = [], [], []
     for k in range(n):

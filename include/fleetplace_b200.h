@@ -128,6 +128,9 @@ typedef struct fp_search_result {
                                     relocation bit updates, substitution bit
                                     updates, relocation apply, exact totals,
                                     table patches, per-pass setup */
+  double init_ms;                /* search start: costs, exact total, relocation
+                                    table sweep (CUDA events) */
+  double sweep_ms;               /* per-pass bitset sweeps (grid-wide mode) */
   uint64_t event_counts[5];      /* scenario 0: scanned rows, scan steps, row
                                     contexts, relocation prepasses, rows settled
                                     by the O(1) eventless test */
@@ -152,6 +155,9 @@ fp_status fp_ctx_create(int32_t device, fp_ctx** out);
 void fp_ctx_destroy(fp_ctx* ctx);
 /* Kernel launches issued by this context since creation (evidence counter). */
 uint64_t fp_ctx_kernel_launches(const fp_ctx* ctx);
+/* CUDA-event time of the main kernel of the last fp_build_distance_table /
+ * fp_column_totals / fp_rank_bases call on this context (ms). */
+double fp_ctx_last_kernel_ms(const fp_ctx* ctx);
 
 /* ---- instance validation / generation (host) -------------------------- */
 /* validate_instance (proj/src/model.cpp:46-74). */

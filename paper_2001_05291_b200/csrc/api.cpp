@@ -41,6 +41,7 @@ struct fp_ctx {
   size_t cost_cap = 0;  // elements
   int M = -1, B = -1;
   uint64_t launches = 0;
+  double last_kernel_ms = 0.0;
   // pinned staging for permutations (double-buffered)
   int32_t* h_perm[2] = {nullptr, nullptr};
   size_t perm_cap = 0;
@@ -177,6 +178,28 @@ void validate(const fp_instance* in) {
     throw FpError(FP_ERR_VALIDATION,
                   "validation failed for fleet: needs at least one aerodrome per fixed-wing vehicle");
 }
+
+// CUDA-event timer on a stream.
+struct EvTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t st;
+  explicit EvTimer(cudaStream_t s) : st(s) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  double stop_ms() {
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+  }
+  ~EvTimer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
 
 // ---- permutations (proj/include/fleetplace/rng.hpp:14-42) ------------------
 struct PermStream {
@@ -474,8 +497,14 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     ctx->perm_cap = chunk_ints;
   }
   run.d_perm.alloc(chunk_ints);
-  check(fpk::launch_init(run.d_scs.p, n, maxB, maxV, st), "init_kernel");
+  double init_ms = 0.0, sweep_ms = 0.0;
+  {
+    EvTimer ti(st);
+    check(fpk::launch_init(run.d_scs.p, n, maxB, maxV, st), "init_kernel");
+    init_ms = ti.stop_ms();
+  }
   ctx->launches += 2;
+  std::vector<cudaEvent_t> sweep_ev;  // (start, end) pairs around grid-wide sweeps
   PermStream rng(cfg->seed);
   auto gen_chunk = [&](int32_t* buf) {
     for (int k = 0; k < kchunk; ++k) {
@@ -499,6 +528,15 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       ctx->launches += 1;
     } else {
       for (int k = 0; k < kchunk; ++k) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        check(fpk::launch_sweep(run.d_scs.p, run.d_active.p, n, run.d_perm.p + 2ll * k * M, M, st),
+              "prep_kernel");
+        cudaEventRecord(e1, st);
+        sweep_ev.push_back(e0);
+        sweep_ev.push_back(e1);
         check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p + 2ll * k * M, 1,
                                false, cfg->max_passes, M, tabu, tenure,
                                cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads),
@@ -511,6 +549,14 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     gen_chunk(ctx->h_perm[nb]);
     d2h(ctrs.data(), run.d_ctr.p, n, st);
     check(cudaStreamSynchronize(st), "pass sync");
+    for (size_t e = 0; e + 1 < sweep_ev.size(); e += 2) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, sweep_ev[e], sweep_ev[e + 1]);
+      sweep_ms += ms;
+      cudaEventDestroy(sweep_ev[e]);
+      cudaEventDestroy(sweep_ev[e + 1]);
+    }
+    sweep_ev.clear();
     buf = nb;
     for (int s = 0; s < n; ++s) {
       if (!active[s]) continue;
@@ -550,6 +596,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     o.final_objective_km = c.final_total;
     outs[s].device_ms = ms;
     outs[s].exact_fallbacks = c.fallbacks;
+    outs[s].init_ms = init_ms;
+    outs[s].sweep_ms = sweep_ms;
     for (int k = 0; k < 12; ++k) outs[s].phase_cycles[k] = c.cycles[k];
     for (int k = 0; k < 5; ++k) outs[s].event_counts[k] = c.counts[k];
     outs[s].kernel_launches = ctx->launches;
@@ -594,6 +642,8 @@ void fp_ctx_destroy(fp_ctx* ctx) {
 }
 
 uint64_t fp_ctx_kernel_launches(const fp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+double fp_ctx_last_kernel_ms(const fp_ctx* ctx) { return ctx ? ctx->last_kernel_ms : 0.0; }
 
 fp_status fp_validate_instance(const fp_instance* inst) {
   return guarded([&] { validate(inst); });
@@ -644,9 +694,11 @@ fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* in, double rad
     check(fpk::launch_point_cos(blat, B, cosv, st), "cos(bases)");
     check(fpk::launch_point_cos(plat, M, cosv + B, st), "cos(pickups)");
     check(fpk::launch_point_cos(dlat, M, cosv + B + M, st), "cos(deliveries)");
+    EvTimer tk(st);
     check(fpk::launch_table(blat, blon, cosv, B, plat, plon, cosv + B, dlat, dlon, cosv + B + M,
                             M, radius_km, ctx->d_cost, st),
           "table_kernel");
+    ctx->last_kernel_ms = tk.stop_ms();
     ctx->launches += 4;
     if (out_cost) d2h(out_cost, ctx->d_cost, (size_t)M * B, st);
     check(cudaStreamSynchronize(st), "table sync");
@@ -705,7 +757,9 @@ fp_status fp_column_totals(fp_ctx* ctx, double* out_totals) {
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (ctx->M < 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "no resident table");
     DBuf<double> d(ctx->B);
+    EvTimer tk(ctx->stream);
     check(fpk::launch_column_totals(ctx->d_cost, ctx->M, ctx->B, d.p, ctx->stream), "totals");
+    ctx->last_kernel_ms = tk.stop_ms();
     ctx->launches += 1;
     d2h(out_totals, d.p, ctx->B, ctx->stream);
     check(cudaStreamSynchronize(ctx->stream), "totals sync");
@@ -721,7 +775,9 @@ fp_status fp_rank_bases(fp_ctx* ctx, const fp_instance* in, fp_ranked_start* out
     cudaStream_t st = ctx->stream;
     // (1) fixed-order column totals on the device
     DBuf<double> d_tot(B);
+    EvTimer tk(st);
     check(fpk::launch_column_totals(ctx->d_cost, M, B, d_tot.p, st), "totals");
+    ctx->last_kernel_ms = tk.stop_ms();
     ctx->launches += 1;
     d2h(out->base_totals, d_tot.p, B, st);
     check(cudaStreamSynchronize(st), "totals sync");

@@ -32,6 +32,8 @@ cudaError_t launch_candidate_delta(const double* cost, int M, const int32_t* vb,
                                    cudaStream_t st);
 cudaError_t launch_init(Scenario* d_scs, int n_scn, int maxB, int maxV, cudaStream_t stream);
 cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream);
+cudaError_t launch_sweep(Scenario* d_scs, const int32_t* d_active, int n_scn,
+                         const int32_t* d_perms, int M, cudaStream_t stream);
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,
                         bool tabu, long long tenure, bool debug, int V, int B, int K,

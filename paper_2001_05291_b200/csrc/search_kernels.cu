@@ -1530,19 +1530,24 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   return cudaGetLastError();
 }
 
+// The grid-wide per-pass sweep (mirrors + imp/mem bitsets) for the pass whose
+// permutations start at d_perms.
+cudaError_t launch_sweep(Scenario* d_scs, const int32_t* d_active, int n_scn,
+                         const int32_t* d_perms, int M, cudaStream_t stream) {
+  const int nwd = (M + 31) / 32;
+  dim3 mg((nwd + 7) / 8 < 1184 ? (nwd + 7) / 8 : 1184, n_scn);
+  if (M > 0) prep_kernel<<<mg, 256, 0, stream>>>(d_scs, d_active, d_perms + M);
+  return cudaGetLastError();
+}
+
 // `kpasses` passes whose permutations are consecutive in d_perms (perm_a,
 // perm_b per pass). inkernel: each block rebuilds its own mirrors/bitsets
 // between passes; otherwise kpasses must be 1 and the grid-wide sweep runs
-// first.
+// first (launch_sweep).
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,
                         bool tabu, long long tenure, bool debug, int V, int B, int K,
                         cudaStream_t stream, int threads) {
-  if (!inkernel) {
-    const int nwd = (M + 31) / 32;
-    dim3 mg((nwd + 7) / 8 < 1184 ? (nwd + 7) / 8 : 1184, n_scn);
-    if (M > 0) prep_kernel<<<mg, 256, 0, stream>>>(d_scs, d_active, d_perms + M);
-  }
   if (threads == 1024)
     return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
                                 tabu, tenure, debug, V, B, K, stream);

@@ -320,6 +320,9 @@ class _Ctx:
     def launches(self) -> int:
         return int(lib().fp_ctx_kernel_launches(self.p))
 
+    def last_kernel_ms(self) -> float:
+        return float(lib().fp_ctx_last_kernel_ms(self.p))
+
     def __del__(self):
         try:
             if getattr(self, "p", None):
@@ -483,6 +486,8 @@ class SearchStats:
     exact_fallbacks: int = 0
     phase_cycles: tuple = ()
     event_counts: tuple = ()
+    init_ms: float = 0.0
+    sweep_ms: float = 0.0
 
 
 @dataclass
@@ -549,7 +554,8 @@ def _stats(r: A.fp_search_result) -> SearchStats:
     return SearchStats(int(s.passes), int(s.evaluations), int(s.applied_moves), int(s.committed_moves),
                        int(s.tabu_skips_outer), int(s.tabu_skips_inner), float(s.final_objective_km),
                        float(r.device_ms), int(r.exact_fallbacks), tuple(int(x) for x in r.phase_cycles),
-                       tuple(int(x) for x in r.event_counts))
+                       tuple(int(x) for x in r.event_counts), float(r.init_ms),
+                       float(r.sweep_ms))
 
 
 def search_arrays(inst: Instance, t: DistanceTable, cfg: SearchConfig, vehicle_base: np.ndarray,

@@ -362,6 +362,7 @@ struct SearchRun {
   DBuf<int32_t> d_active;
   DBuf<int32_t> d_perm;  // [2*M]
   DBuf<fpk::Counters> d_ctr;  // [n], contiguous: one copy per pass
+  DBuf<double> costT;         // row-major table copies (optional)
   std::vector<Layout> lay;
 };
 
@@ -386,6 +387,21 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   for (int s = 0; s < n; ++s) run.hs.push_back(prepare(&insts[s], &starts[s]));
 
   // ---- arena
+  // A row-major copy of each table (mission-major: one mission's costs at
+  // every base contiguous) serves the per-move updates that run over bases;
+  // it is made when device memory allows (FLEETPLACE_COST_T=0 disables it).
+  bool cost_t = true;
+  if (const char* e = std::getenv("FLEETPLACE_COST_T")) cost_t = std::atoi(e) != 0;
+  if (cost_t) {
+    size_t need = 0;
+    for (int s = 0; s < n; ++s) {
+      const int V = insts[s].n_vehicles, B = insts[s].n_bases;
+      need += layout(M, B, V, run.hs[s].K, run.hs[s].psize + V + 1, dev_tables[s] == nullptr).total +
+              8ull * M * B;
+    }
+    size_t free_b = 0, total_b = 0;
+    cost_t = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && need + (2ull << 30) <= free_b;
+  }
   size_t total = 0;
   run.lay.resize(n);
   std::vector<size_t> base(n);
@@ -401,6 +417,16 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     total += run.lay[s].total;
   }
   run.arena.mem.alloc(std::max<size_t>(total, 256));
+  // the row-major copies: device-only, filled by launch_init, never staged
+  std::vector<size_t> tbase(n, 0);
+  if (cost_t) {
+    size_t tt = 0;
+    for (int s = 0; s < n; ++s) {
+      tbase[s] = tt;
+      tt += (size_t)M * insts[s].n_bases;
+    }
+    run.costT.alloc(std::max<size_t>(tt, 1));
+  }
   run.d_ctr.alloc(n);
   std::vector<fpk::Counters> ctrs(n);
   for (int s = 0; s < n; ++s) {
@@ -432,6 +458,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       std::memcpy(hb + L.cost, host_tables[s], 8ull * M * B);
     fpk::Scenario& S = run.arena.scs[s];
     S.cost = dev_tables[s] ? dev_tables[s] : reinterpret_cast<const double*>(db + L.cost);
+    S.costT = cost_t ? run.costT.p + tbase[s] : nullptr;
     S.ro = db + L.ro;
     S.vfixed = db + L.vfixed;
     S.bheli = db + L.bheli;
@@ -500,10 +527,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   double init_ms = 0.0, sweep_ms = 0.0;
   {
     EvTimer ti(st);
-    check(fpk::launch_init(run.d_scs.p, n, maxB, maxV, st), "init_kernel");
+    check(fpk::launch_init(run.d_scs.p, n, M, maxB, maxV, cost_t, st), "init_kernel");
     init_ms = ti.stop_ms();
   }
-  ctx->launches += 2;
+  ctx->launches += 1 + (maxB > 0 ? 1 : 0) + (cost_t && M > 0 && maxB > 0 ? 1 : 0);
   std::vector<cudaEvent_t> sweep_ev;  // (start, end) pairs around grid-wide sweeps
   PermStream rng(cfg->seed);
   auto gen_chunk = [&](int32_t* buf) {

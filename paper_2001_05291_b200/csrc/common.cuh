@@ -32,14 +32,15 @@ struct Counters {
   double final_total;             // exact fixed-order total (written at the end)
   double total_exact;             // exact fixed-order total of the state ...
   long long total_ver;            // ... at this applied-move count (-1: unknown)
-  // SM cycles spent per automaton phase (thread 0's view, single-scenario
-  // launches): 0 row skipping, 1 row context, 2 chunk scans, 3 event pairs,
-  // 4 exact fallbacks, 5 relocation prepasses
-  unsigned long long cycles[12];  // ... 10 table patches, 11 per-pass setup  // ... 6 relocation bit updates, 7 substitution bit updates,
-                                  // 8 relocation apply, 9 exact totals
-  // event counts: 0 interesting rows, 1 chunk iterations, 2 row contexts,
-  // 3 relocation prepasses
-  unsigned long long counts[5];   // ... 4 rows resolved by the O(1) eventless test
+  // SM cycles spent per automaton phase (thread 0's view): 0 row runs,
+  // 1 row contexts, 2 scan steps, 3 event pairs, 4 exact fallbacks, 5 exact
+  // table-row rebuilds, 6 relocation bit updates, 7 substitution bit
+  // updates, 8 relocation apply, 9 exact totals, 10 table patches, 11
+  // per-pass setup
+  unsigned long long cycles[12];
+  // event counts: 0 scanned rows, 1 scan steps, 2 row contexts, 3 exact
+  // table-row rebuilds, 4 rows resolved by the O(1) eventless test
+  unsigned long long counts[5];
 };
 
 // One search scenario: the resident distance table plus the index-based
@@ -49,6 +50,7 @@ struct Counters {
 struct Scenario {
   // read-only instance data
   const double* cost;        // [B*M] column-major, entry (m, b) at b*M + m
+  const double* costT;       // [M*B] row-major copy, entry (m, b) at m*B + b, or null
   const uint8_t* ro;         // [M] mission rotary_only
   const uint8_t* vfixed;     // [V] vehicle is fixed-wing
   const uint8_t* bheli;      // [B] base is a helipad
@@ -72,9 +74,8 @@ struct Scenario {
   long long* exp_reas;       // [V] {Reassign, vehicle id}
   long long* exp_rel;        // [K] {Relocate, id}, ids of bases and vehicles
   uint8_t* role_rel;         // [K]
-  // relocation-class cache: per target base t, the per-vehicle classes of
-  // the relocation delta, valid while no move has been applied since
-  // relocation-delta table, row t = an empty base, column v = a vehicle:
+  // relocation-delta table, entry (t, v) at v*B + t, t an empty base, v a
+  // vehicle:
   //  rA ~ X = sum over v's missions of (cost(m, t) - mc[m]) (exact reals),
   //  |rA - X| <= rE, rU >= sum |cost(m, t) - mc[m]|; rcnt[t] = vehicles whose
   //  relocation to t is not certainly non-improving

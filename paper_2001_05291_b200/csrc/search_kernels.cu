@@ -95,6 +95,12 @@ __device__ __forceinline__ double cost_at(const Scenario& s, int col, int m) {
   return s.cost[(long long)col * s.M + m];
 }
 
+// The same entry for accesses that run over bases with the mission fixed
+// (one mission's costs at every base are contiguous in the row-major copy).
+__device__ __forceinline__ double cost_mb(const Scenario& s, int m, int b) {
+  return s.costT ? s.costT[(long long)m * s.B + b] : s.cost[(long long)b * s.M + m];
+}
+
 __device__ __forceinline__ int clamp_lim(long long e, int M) {
   return e <= 0 ? 0 : (e > M + 1 ? M + 1 : (int)e);
 }
@@ -364,7 +370,7 @@ __device__ __forceinline__ uint32_t prefix_bits(long long n) {
 // lowers its cost (proj/src/search.cpp:82-101, 131-148 preconditions + sign).
 __device__ __forceinline__ bool imp_bit(const Scenario& s, int g, int q, int j) {
   return s.mvp[q] != g && compat_vm(s.vfixed[g], s.rop[q]) &&
-         cost_at(s, s.vbase[g], j) < s.mcp[q];
+         cost_mb(s, j, s.vbase[g]) < s.mcp[q];
 }
 
 __device__ __forceinline__ void put_bit(uint32_t* w, uint32_t bit, bool on) {
@@ -470,7 +476,7 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int g = g0 + u * 32 + l;
-        on[u] = g < V && g != x && compat_vm(s.vfixed[g], ro) && cost_at(s, s.vbase[g], j) < mcq;
+        on[u] = g < V && g != x && compat_vm(s.vfixed[g], ro) && cost_mb(s, j, s.vbase[g]) < mcq;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -496,7 +502,7 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
           if (g == x) continue;
           uint32_t* wp = s.imp + (long long)g * nwd + wd;
           const bool was = (*wp & (1u << bn)) != 0u;
-          const bool now = compat_vm(s.vfixed[g], s.rop[q]) && cost_at(s, s.vbase[g], j) < s.mcp[q];
+          const bool now = compat_vm(s.vfixed[g], s.rop[q]) && cost_mb(s, j, s.vbase[g]) < s.mcp[q];
           put_bit(wp, 1u << bn, now);
           if (now != was) atomicAdd(&sm.impc[g], now ? 1 : -1);
         }
@@ -521,6 +527,12 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
 // patch is added to rE, so classes stay rigorous; a row whose bounds got too
 // loose to classify (AMB) is rebuilt exactly.
 
+// Entry (t, v) of rA/rE/rU: vehicle-major, so one vehicle's entries over
+// consecutive bases are contiguous (coalesced patches after a move).
+__device__ __forceinline__ long long tix(const Scenario& s, int t, int v) {
+  return (long long)v * s.B + t;
+}
+
 // Class of one (t, v) entry from its values (n = v's mission count).
 __device__ __forceinline__ bool table_unsettled(double A, double E0, double U, int n, double bt) {
   if (n == 0 || U == 0.0) return false;  // no terms, or every term exactly zero
@@ -532,7 +544,7 @@ __device__ __forceinline__ bool table_unsettled(double A, double E0, double U, i
 __device__ __forceinline__ uint8_t table_class_n(const Scenario& s, const Shared& sh, int t, int v,
                                                  int n) {
   if (s.vfixed[v] && s.bheli[t]) return CLS_POS;
-  const long long k = (long long)t * s.V + v;
+  const long long k = tix(s, t, v);
   const double U = s.rU[k];
   if (n == 0 || U == 0.0) return CLS_POS;  // no terms, or every term exactly zero
   const double A = s.rA[k];
@@ -610,7 +622,7 @@ __device__ void table_row_fresh(const Scenario& s, Shared& sh, double* acc_sum, 
       abs += acc_abs[(long long)k * V + v];
     }
     const int n = s.vcount[v];
-    const long long k = (long long)t * V + v;
+    const long long k = tix(s, t, v);
     const double U = abs * (1.0 + (double)(n + 2) * kTwoPowM52);
     s.rA[k] = sum;
     s.rU[k] = U;
@@ -647,7 +659,7 @@ __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm
 // One term enters or leaves D(t, v): rA +/-= d, the bounds widened by the
 // rounding of d and of the update.
 __device__ __forceinline__ void table_patch(const Scenario& s, int t, int v, double d, bool add) {
-  const long long k = (long long)t * s.V + v;
+  const long long k = tix(s, t, v);
   const double A = add ? s.rA[k] + d : s.rA[k] - d;
   s.rA[k] = A;
   s.rE[k] += 2.0 * kTwoPowM52 * (fabs(d) + fabs(A));
@@ -658,20 +670,21 @@ __device__ __forceinline__ void table_patch(const Scenario& s, int t, int v, dou
 
 // After mission j moved from `loser` (cost mc_old, nl missions before) to
 // `gain` (cost mc_new, ng missions before): patch every empty base's row and
-// its count of unsettled classes. Block-wide (one thread per empty base);
-// each entry is loaded once and patched in registers.
+// its count of unsettled classes. Block-wide (thread per base: the loser's
+// and the gainer's entries of consecutive bases are contiguous); each entry
+// is loaded once and patched in registers. Rows of empty bases outside the
+// pool are kept current too (harmless; they are rebuilt fresh or patched
+// the same way when they enter it).
 template <int NT>
 __device__ void table_after_substitution(const Scenario& s, const Shared& sh, int j, int loser,
                                          int gain, double mc_old, double mc_new, int nl, int ng) {
   const double bt = single_bound(s, sh);
   const bool fl = s.vfixed[loser], fg = s.vfixed[gain];
-  const long long V = s.V;
-  for (int k = threadIdx.x; k < sh.c.psize; k += NT) {
-    if (s.pkind[k] != POOL_EMPTY) continue;
-    const int t = s.pidx[k];
+  for (int t = threadIdx.x; t < s.B; t += NT) {
+    if (s.bveh[t] >= 0) continue;
     const bool heli = s.bheli[t];
-    const double c = cost_at(s, t, j);
-    const long long kl = t * V + loser, kg = t * V + gain;
+    const double c = cost_mb(s, j, t);
+    const long long kl = tix(s, t, loser), kg = tix(s, t, gain);
     double Al = s.rA[kl], El = s.rE[kl], Ul = s.rU[kl];
     double Ag = s.rA[kg], Eg = s.rE[kg], Ug = s.rU[kg];
     int delta = 0;
@@ -701,13 +714,11 @@ __device__ void table_after_substitution(const Scenario& s, const Shared& sh, in
 template <int NT>
 __device__ void table_after_relocation(const Scenario& s, Shared& sh, const Smem& sm, int x, int t,
                                        int b_old) {
-  const long long kt = (long long)t * s.V + x;
+  const long long kt = tix(s, t, x);
   const double At = s.rA[kt], Et = s.rE[kt], Ut = s.rU[kt];
-  for (int k = threadIdx.x; k < sh.c.psize; k += NT) {
-    if (s.pkind[k] != POOL_EMPTY) continue;
-    const int t2 = s.pidx[k];
-    if (t2 == b_old) continue;
-    const long long k2 = (long long)t2 * s.V + x;
+  for (int t2 = threadIdx.x; t2 < s.B; t2 += NT) {
+    if (s.bveh[t2] >= 0 || t2 == b_old) continue;
+    const long long k2 = tix(s, t2, x);
     const int before = table_class(s, sh, t2, x) != CLS_POS;
     const double A = s.rA[k2] - At;
     s.rA[k2] = A;
@@ -732,7 +743,7 @@ __device__ void set_mission(const Scenario& s, int j, int v, double c) {
 
 __device__ void apply_takeover(const Scenario& s, Shared& sh, int j, int gain, int pos) {
   const int loser = s.mv[j];
-  set_mission(s, j, gain, cost_at(s, s.vbase[gain], j));
+  set_mission(s, j, gain, cost_mb(s, j, s.vbase[gain]));
   s.vcount[gain] += 1;
   s.vcount[loser] -= 1;
   if (s.vcount[loser] == 0) {
@@ -749,7 +760,7 @@ __device__ void apply_takeover(const Scenario& s, Shared& sh, int j, int gain, i
 
 __device__ void apply_reassign(const Scenario& s, Shared& sh, int j, int gain) {
   const int loser = s.mv[j];
-  set_mission(s, j, gain, cost_at(s, s.vbase[gain], j));
+  set_mission(s, j, gain, cost_mb(s, j, s.vbase[gain]));
   s.vcount[gain] += 1;
   s.vcount[loser] -= 1;
   if (s.vcount[loser] == 0) {
@@ -832,7 +843,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
   // ---- takeover (proj/src/search.cpp:82-101)
   if (i < sh.c.psize && s.pkind[i] == POOL_IDLE) {
     const int g = s.pidx[i];
-    const double newc = cost_at(s, s.vbase[g], j);
+    const double newc = cost_mb(s, j, s.vbase[g]);
     const double mcj = s.mc[j];
     if (compat_vm(s.vfixed[g], s.ro[j]) && newc - mcj < 0.0) {
       int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
@@ -919,7 +930,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
   {
     const int g = s.mv[i], l = s.mv[j];
     if (g != l && compat_vm(s.vfixed[g], s.ro[j])) {
-      const double newc = cost_at(s, s.vbase[g], j);
+      const double newc = cost_mb(s, j, s.vbase[g]);
       const double mcj = s.mc[j];
       if (newc - mcj < 0.0) {
         int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
@@ -1243,6 +1254,29 @@ __global__ void __launch_bounds__(256) prep_kernel(Scenario* scs, const int32_t*
   prep_words(s, pb, blockIdx.x * warps + (threadIdx.x >> 5), gridDim.x * warps);
 }
 
+// Block-wide copy of n words from global memory into shared memory (both
+// 16-byte aligned): four 16-byte loads in flight per thread.
+template <int NT>
+__device__ void copy_words(uint32_t* dst, const uint32_t* __restrict__ src, long long n) {
+  const long long n4 = n >> 2;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (long long k0 = 0; k0 < n4; k0 += 4ll * NT) {
+    uint4 r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long k = k0 + u * NT + threadIdx.x;
+      if (k < n4) r[u] = __ldg(s4 + k);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long k = k0 + u * NT + threadIdx.x;
+      if (k < n4) d4[k] = r[u];
+    }
+  }
+  for (long long k = (n4 << 2) + threadIdx.x; k < n; k += NT) dst[k] = src[k];
+}
+
 // Shared-memory bytes of the always-resident part and of the optional copy
 // of the small per-vehicle / per-key state.
 size_t pass_smem_core(int V, int NT) {
@@ -1253,7 +1287,7 @@ size_t pass_smem_core(int V, int NT) {
 }
 size_t pass_smem_state(int V, int B, int K) {
   return align16(8ull * V) * 2 + align16(8ull * K) + align16(K) + align16(4ull * V) * 3 +
-         align16(V) + align16(4ull * B) + align16(B) + 64;
+         align16(V) + 2 * align16(4ull * B) + align16(B) + 64;
 }
 
 // One pass over perm_a for every active scenario (blockIdx.x = scenario).
@@ -1261,7 +1295,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
                 int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
-                int debug_i, int state_in_smem) {
+                int debug_i, int state_in_smem, int bits_in_smem) {
   if (!active[blockIdx.x]) return;
   const Scenario g = scs[blockIdx.x];
   if (g.ctr->done) return;  // finished earlier in this chunk of launches
@@ -1305,6 +1339,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     uint8_t* vfixed = take(V);
     int32_t* brk = reinterpret_cast<int32_t*>(take(4ull * B));
     uint8_t* bheli = take(B);
+    s.bveh = reinterpret_cast<int32_t*>(take(4ull * B));
     for (int v = threadIdx.x; v < V; v += NT) {
       s.exp_take[v] = g.exp_take[v];
       s.exp_reas[v] = g.exp_reas[v];
@@ -1320,11 +1355,18 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     for (int b = threadIdx.x; b < B; b += NT) {
       brk[b] = g.brk[b];
       bheli[b] = g.bheli[b];
+      s.bveh[b] = g.bveh[b];
     }
     s.vrk = vrk;
     s.vfixed = vfixed;
     s.brk = brk;
     s.bheli = bheli;
+  }
+  if (bits_in_smem) {
+    // the imp / mem bitsets live in shared memory: every scan step, event
+    // and bit update of the pass then stays on the SM
+    s.imp = reinterpret_cast<uint32_t*>(take(4ull * V * s.nwd));
+    s.mem = reinterpret_cast<uint32_t*>(take(4ull * V * s.nwd));
   }
   if (threadIdx.x == 0) {
     sh.c = *s.ctr;
@@ -1347,6 +1389,12 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     const long long ps0 = ph_now();
     if (inkernel_prep) {
       prep_words(s, sm.pb, threadIdx.x >> 5, NW);
+      __syncthreads();
+    } else if (bits_in_smem) {
+      // the grid-wide sweep built them in global memory: 16-byte loads, a
+      // batch of them in flight per thread before any store
+      copy_words<NT>(s.imp, g.imp, (long long)V * s.nwd);
+      copy_words<NT>(s.mem, g.mem, (long long)V * s.nwd);
       __syncthreads();
     }
     {
@@ -1462,8 +1510,30 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       g.exp_rel[k] = s.exp_rel[k];
       g.role_rel[k] = s.role_rel[k];
     }
+    for (int b = threadIdx.x; b < B; b += NT) g.bveh[b] = s.bveh[b];
   }
   if (threadIdx.x == 0) *g.ctr = sh.c;
+}
+
+// The row-major copy of the table, 32 x 32 tiles through shared memory.
+__global__ void __launch_bounds__(256) transpose_kernel(Scenario* scs) {
+  const Scenario s = scs[blockIdx.z];
+  const int m0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  if (!s.costT || m0 >= s.M || b0 >= s.B) return;
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int b = b0 + r, m = m0 + tx;
+    if (b < s.B && m < s.M) tile[r][tx] = s.cost[(long long)b * s.M + m];
+  }
+  __syncthreads();
+  double* out = const_cast<double*>(s.costT);
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {
+    const int m = m0 + r, b = b0 + tx;
+    if (m < s.M && b < s.B) out[(long long)m * s.B + b] = tile[tx][r];
+  }
 }
 
 // Search start: per-mission costs and the exact initial fixed-order total
@@ -1516,17 +1586,22 @@ __global__ void __launch_bounds__(512) final_kernel(Scenario* scs) {
 template <int NT>
 static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int n_scn,
                                   const int32_t* d_perms, int kpasses, bool inkernel,
-                                  int max_passes, bool tabu, long long tenure, bool debug, int V,
-                                  int B, int K, cudaStream_t stream) {
+                                  int max_passes, int M, bool tabu, long long tenure, bool debug,
+                                  int V, int B, int K, cudaStream_t stream) {
   const size_t core = pass_smem_core(V, NT);
   const size_t state = pass_smem_state(V, B, K);
+  const size_t bits = 2 * align16(4ull * V * ((M + 31) / 32));
   const size_t limit = 200 * 1024;
+  // 256-thread blocks run two per SM: the bitsets only join while two fit
+  const size_t bits_limit = NT == 256 ? 100 * 1024 : limit;
   if (core > limit) return cudaErrorInvalidConfiguration;
   const int in_smem = core + state <= limit ? 1 : 0;
-  const size_t smem = core + (in_smem ? state : 0);
+  const int bits_smem = in_smem && core + state + bits <= bits_limit ? 1 : 0;
+  const size_t smem = core + (in_smem ? state : 0) + (bits_smem ? bits : 0);
   cudaFuncSetAttribute(pass_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   pass_kernel<NT><<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
-                                               max_passes, tabu, tenure, debug, in_smem);
+                                               max_passes, tabu, tenure, debug, in_smem,
+                                               bits_smem);
   return cudaGetLastError();
 }
 
@@ -1550,15 +1625,18 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         cudaStream_t stream, int threads) {
   if (threads == 1024)
     return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                                tabu, tenure, debug, V, B, K, stream);
+                                M, tabu, tenure, debug, V, B, K, stream);
   if (threads == 512)
     return launch_pass_nt<512>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                               tabu, tenure, debug, V, B, K, stream);
+                               M, tabu, tenure, debug, V, B, K, stream);
   return launch_pass_nt<256>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                             tabu, tenure, debug, V, B, K, stream);
+                             M, tabu, tenure, debug, V, B, K, stream);
 }
 
-cudaError_t launch_init(Scenario* d_scs, int n_scn, int maxB, int maxV, cudaStream_t stream) {
+cudaError_t launch_init(Scenario* d_scs, int n_scn, int M, int maxB, int maxV, bool cost_t,
+                        cudaStream_t stream) {
+  if (cost_t && M > 0 && maxB > 0)
+    transpose_kernel<<<dim3((M + 31) / 32, (maxB + 31) / 32, n_scn), 256, 0, stream>>>(d_scs);
   init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
   const size_t smem = sizeof(double) * (16ull * maxV + 8 * 32);
   cudaFuncSetAttribute(table_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

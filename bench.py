@@ -176,8 +176,10 @@ def run_ours(args) -> None:
                                                        "tabu_skips_outer", "tabu_skips_inner",
                                                        "final_objective_km", "exact_fallbacks")},
         "phase_ms": dict(zip(("row_runs", "row_context", "scan_steps", "event_pairs",
-                              "exact_fallbacks", "reloc_prepass", "reloc_bits", "subst_bits",
-                              "reloc_apply", "exact_totals", "table_patches", "pass_setup"),
+                              "exact_fallbacks", "table_row_rebuilds", "reloc_bits", "subst_bits",
+                              "reloc_apply", "exact_totals", "table_patches", "pass_setup",
+                              "exact_reloc_deltas", "exact_candidate_totals", "helper_waits",
+                              "reserved"),
                              [c / (clocks["sm_mhz"] or 1965.0) / 1e3 for c in st.phase_cycles])),
         "event_counts": dict(zip(("scanned_rows", "scan_steps", "row_contexts",
                                   "reloc_prepasses", "eventless_rows_o1"), st.event_counts)),

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define FP_ABI_VERSION 1
+#define FP_ABI_VERSION 2
 
 typedef enum fp_status {
   FP_OK = 0,
@@ -122,12 +122,14 @@ typedef struct fp_search_result {
   double device_ms;              /* CUDA-event time of the device search */
   uint64_t kernel_launches;      /* kernels this call launched */
   uint64_t exact_fallbacks;      /* accept decisions settled by exact chains */
-  uint64_t phase_cycles[12];     /* SM cycles per automaton phase (scenario 0):
+  uint64_t phase_cycles[16];     /* SM cycles per automaton phase (scenario 0):
                                     row runs, row context, scan steps, event
-                                    pairs, exact fallbacks, relocation prepass,
+                                    pairs, exact fallbacks, table-row rebuilds,
                                     relocation bit updates, substitution bit
                                     updates, relocation apply, exact totals,
-                                    table patches, per-pass setup */
+                                    table patches, per-pass setup, exact
+                                    relocation deltas, exact candidate totals,
+                                    helper waits, (reserved) */
   double init_ms;                /* search start: costs, exact total, relocation
                                     table sweep (CUDA events) */
   double sweep_ms;               /* per-pass bitset sweeps (grid-wide mode) */

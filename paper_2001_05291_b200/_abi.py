@@ -63,7 +63,7 @@ class fp_search_result(C.Structure):
     _fields_ = [("vehicle_base", _i32p), ("mission_vehicle", _i32p),
                 ("stats", fp_search_stats), ("device_ms", C.c_double),
                 ("kernel_launches", C.c_uint64), ("exact_fallbacks", C.c_uint64),
-                ("phase_cycles", C.c_uint64 * 12), ("init_ms", C.c_double),
+                ("phase_cycles", C.c_uint64 * 16), ("init_ms", C.c_double),
                 ("sweep_ms", C.c_double), ("event_counts", C.c_uint64 * 5)]
 
 

@@ -311,7 +311,8 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
   size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
-      invb, exp_take, exp_reas, exp_rel, role_rel, rA, rE, rU, rcnt, imp, mem, scratch, ctr, cost, total;
+      invb, exp_take, exp_reas, exp_rel, role_rel, rA, rE, rU, rcnt, imp, mem, scratch, hc, hdelta,
+      hsum, habs, hec, hrs, hue, ctr, cost, total;
 };
 
 Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
@@ -350,6 +351,14 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   L.imp = put(4ull * V * nwd);
   L.mem = put(4ull * V * nwd);
   L.scratch = put(4ull * M + 4);
+  L.hc = put(sizeof(fpk::HelperCtl));
+  L.hdelta = put(4ull * V);
+  L.hsum = put(8ull * V);
+  L.habs = put(8ull * V);
+  const size_t nsub = ((size_t)M + fpk::kChainSub - 1) / fpk::kChainSub + 1;
+  L.hec = put(4ull * nsub);
+  L.hrs = put(8ull * nsub);
+  L.hue = put(4ull * nsub);
   L.cost = own_cost ? put(8ull * M * B + 16) : 0;
   L.total = o;
   return L;
@@ -432,6 +441,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   for (int s = 0; s < n; ++s) {
     ctrs[s] = fpk::Counters{};
     ctrs[s].psize = run.hs[s].psize;
+    // test hook: every accept decision through the exact sums (same results)
+    if (const char* e = std::getenv("FLEETPLACE_FORCE_EXACT")) ctrs[s].force_exact = std::atoi(e);
+    if (const char* e = std::getenv("FLEETPLACE_HELPED_CHAINS")) ctrs[s].chain_mode = std::atoi(e) == 0;
   }
   unsigned char* d0 = run.arena.mem.p;
   std::vector<unsigned char> stage(total, 0);
@@ -486,6 +498,18 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.imp = reinterpret_cast<uint32_t*>(db + L.imp);
     S.mem = reinterpret_cast<uint32_t*>(db + L.mem);
     S.scratch = reinterpret_cast<int32_t*>(db + L.scratch);
+    S.hc = reinterpret_cast<fpk::HelperCtl*>(db + L.hc);
+    S.hdelta = reinterpret_cast<int32_t*>(db + L.hdelta);
+    S.hsum = reinterpret_cast<double*>(db + L.hsum);
+    S.habs = reinterpret_cast<double*>(db + L.habs);
+    S.hec = reinterpret_cast<int32_t*>(db + L.hec);
+    S.hrs = reinterpret_cast<long long*>(db + L.hrs);
+    S.hue = reinterpret_cast<int32_t*>(db + L.hue);
+    {
+      const size_t nsub = ((size_t)M + fpk::kChainSub - 1) / fpk::kChainSub + 1;
+      int32_t* he = reinterpret_cast<int32_t*>(hb + L.hec);
+      for (size_t c = 0; c < nsub; ++c) he[c] = fpk::kNoBinade;
+    }
     S.nwd = (M + 31) / 32;
     S.ctr = run.d_ctr.p + s;
     S.M = M;
@@ -543,6 +567,11 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   gen_chunk(ctx->h_perm[buf]);
   int threads = n == 1 ? 512 : 256;
   if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
+  // large single scenarios share each relocation's O(M) work with helper
+  // blocks (-1 = as many as fit; FLEETPLACE_HELPERS=0 disables)
+  int helpers = n == 1 && M >= (32 << 10) ? -1 : 0;
+  if (const char* e = std::getenv("FLEETPLACE_HELPERS")) helpers = std::atoi(e);
+  unsigned epoch = 0;
   int n_active = n;
   while (n_active > 0) {
     h2d(run.d_active.p, active.data(), n, st);
@@ -550,7 +579,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     if (inkernel) {
       check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p, kchunk, true,
                              cfg->max_passes, M, tabu, tenure, cfg->debug_check_deltas != 0, maxV,
-                             maxB, maxK, st, threads),
+                             maxB, maxK, st, threads, 0, 0u),
             "pass_kernel");
       ctx->launches += 1;
     } else {
@@ -566,7 +595,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
         sweep_ev.push_back(e1);
         check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p + 2ll * k * M, 1,
                                false, cfg->max_passes, M, tabu, tenure,
-                               cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads),
+                               cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads,
+                               helpers, ++epoch),
               "pass_kernel");
         ctx->launches += M > 0 ? 2 : 1;
       }
@@ -625,7 +655,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     outs[s].exact_fallbacks = c.fallbacks;
     outs[s].init_ms = init_ms;
     outs[s].sweep_ms = sweep_ms;
-    for (int k = 0; k < 12; ++k) outs[s].phase_cycles[k] = c.cycles[k];
+    for (int k = 0; k < 16; ++k) outs[s].phase_cycles[k] = c.cycles[k];
     for (int k = 0; k < 5; ++k) outs[s].event_counts[k] = c.counts[k];
     outs[s].kernel_launches = ctx->launches;
   }

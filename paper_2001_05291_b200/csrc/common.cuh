@@ -28,6 +28,9 @@ struct Counters {
   int pass_applied;               // moves applied in the current pass
   int pass_skipped;               // any tabu skip in the current pass
   int error;                      // 0 = ok, else an fp_status
+  int force_exact;                // test hook: 1 = every total comparison through the exact
+                                  // chains, 2 = every unsettled relocation delta exactly
+  int chain_mode;                 // 0 = helper-assisted exact chains when possible, 1 = never
   double total_up;                // rigorous upper bound of the current total
   double final_total;             // exact fixed-order total (written at the end)
   double total_exact;             // exact fixed-order total of the state ...
@@ -36,12 +39,34 @@ struct Counters {
   // 1 row contexts, 2 scan steps, 3 event pairs, 4 exact fallbacks, 5 exact
   // table-row rebuilds, 6 relocation bit updates, 7 substitution bit
   // updates, 8 relocation apply, 9 exact totals, 10 table patches, 11
-  // per-pass setup
-  unsigned long long cycles[12];
+  // per-pass setup, 12 exact relocation deltas, 13 exact candidate totals,
+  // 14 helper waits, 15 reserved
+  unsigned long long cycles[16];
   // event counts: 0 scanned rows, 1 scan steps, 2 row contexts, 3 exact
   // table-row rebuilds, 4 rows resolved by the O(1) eventless test
   unsigned long long counts[5];
 };
+
+// Work sharing for large single scenarios: the pass kernel runs one master
+// block (the automaton) plus helper blocks that split the O(M) work of a
+// relocation. The master posts a job by publishing seq = (epoch << 32) | k
+// (epoch = launch number, k = job number within the launch); every helper
+// adds one to `done` when its share is finished.
+enum : int { HJOB_QUIT = 0, HJOB_RELOCATE = 1, HJOB_CHAIN = 2 };
+struct HelperCtl {
+  unsigned long long seq;
+  unsigned done;
+  int kind;
+  int x, t, b_old;   // relocation: mover, target base, vacated base
+  int impc_x;        // out: set bits of the mover's new imp row
+  int ckind, cj, cmover, ct;  // chain: term kind, mission, mover, base (-1)
+  double cnewc;               // chain: the substituted cost (kind 1)
+};
+
+// Exact fixed-order sums are walked in chunks of kChainSub terms (see
+// exact_chain_helped).
+constexpr int kChainSub = 2048;
+constexpr int kNoBinade = -100000;
 
 // One search scenario: the resident distance table plus the index-based
 // SearchState of proj/src/search_state.hpp:20-31 in structure-of-arrays
@@ -90,6 +115,15 @@ struct Scenario {
   uint32_t* imp;             // [V*NWD]
   uint32_t* mem;             // [V*NWD]
   int32_t* scratch;          // [M] per-scenario scratch (relocation position lists)
+  HelperCtl* hc;             // helper work sharing (zeroed at search start)
+  int32_t* hdelta;           // [V] helpers' imp-row popcount deltas
+  double* hsum;              // [V] helpers' partial relocation sums (fresh row)
+  double* habs;              // [V]
+  int32_t* hec;              // [ceil(M/kChainSub)] binade of the running sum at each chunk
+                             //   start in the latest exact chain (kNoBinade: unknown)
+  long long* hrs;            // [..] helpers: chunk sums of rn(term / ulp) in binade hue
+  int32_t* hue;              // [..] helpers: the binade hrs is for, kNoBinade when the
+                             //   chunk holds a rounding tie / a huge term / no prediction
   Counters* ctr;
   int32_t M, B, V, K, pool_cap, nwd;
 };

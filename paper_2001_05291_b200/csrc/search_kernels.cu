@@ -33,6 +33,7 @@
 
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -60,6 +61,8 @@ struct Shared {
   double bd0;
   double xs;                            // exact chain: partial sum so far ...
   int xk;                               // ... after this many terms
+  unsigned hk;                          // helper jobs posted in this launch
+  unsigned hdone;                       // helper completions expected so far
   long long red_l[33];
   int red_i[2][33];
   double red_d[3][33];
@@ -82,6 +85,9 @@ struct Smem {
   int* jl_lim;         // [V] its live window (positions from the segment start)
   uint8_t* jl_outer;   // [V] its role is Outer
   const int32_t* pb;   // perm_b
+  int helpers;         // helper blocks sharing relocations (0 = none)
+  unsigned epoch;      // launch number (helper job tags)
+  int32_t* gvbase;     // global vbase (helpers read the mover's new base)
 };
 
 // Phase timing (thread 0's SM clock), accumulated into Counters::cycles.
@@ -128,6 +134,7 @@ __device__ int block_min(int v, Shared& sh) {
 // S' < S whenever the exact decrease exceeds 2 gamma_{M-1} X
 // <= (M + 2) 2^-52 total_up.
 __device__ __forceinline__ double single_bound(const Scenario& s, const Shared& sh) {
+  if (sh.c.force_exact & 1) return INFINITY;
   return (double)(s.M + 2) * kTwoPowM52 * sh.c.total_up * 1.0001;
 }
 
@@ -154,9 +161,66 @@ __device__ __forceinline__ double chain_term(const Scenario& s, int kind, int k,
   return s.mc[k];
 }
 
+// ---- helper blocks (large single scenarios) --------------------------------
+//
+// A relocation touches O(M) state: the mover's missions get new costs, the
+// mover's imp row is rebuilt, the bits of its positions change in every
+// other row, and the vacated base needs a fresh relocation row. For large
+// scenarios that work is split over helper blocks that wait in the same
+// launch; the master block shifts the other table rows meanwhile. The
+// handshake is a release/acquire pair at gpu scope on HelperCtl::seq and
+// HelperCtl::done; all spins are bounded (a hang guard that reports an error).
+
+constexpr long long kSpinLimit = 1ll << 35;  // ~17 s of SM clock
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Master, thread 0: publish a job (the block's earlier writes are ordered
+// before it by the caller's barrier).
+__device__ void post_job(const Scenario& s, Shared& sh, const Smem& sm, int kind, int x, int t,
+                         int b_old) {
+  HelperCtl* hc = s.hc;
+  hc->kind = kind;
+  hc->x = x;
+  hc->t = t;
+  hc->b_old = b_old;
+  sh.hk += 1;
+  __threadfence();
+  st_release_u64(&hc->seq, ((unsigned long long)sm.epoch << 32) | sh.hk);
+}
+
+// Master, block-wide: wait until every helper finished the last job.
 template <int NT>
-__device__ long long block_exclusive_scan(long long x, long long& total, Shared& sh) {
-  constexpr int NW = NT / 32;
+__device__ void wait_helpers(const Scenario& s, Shared& sh, const Smem& sm) {
+  if (threadIdx.x == 0) {
+    sh.hdone += (unsigned)sm.helpers;
+    const long long t0 = clock64();
+    while ((int)(ld_acquire_u32(&s.hc->done) - sh.hdone) < 0) {
+      if (clock64() - t0 > kSpinLimit) {
+        sh.c.error = 8;  // FP_ERR_CUDA: helper blocks stopped answering
+        break;
+      }
+      __nanosleep(32);
+    }
+    sh.c.cycles[14] += (unsigned long long)(clock64() - t0);
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__device__ long long block_inclusive_scan(long long x, Shared& sh) {
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   long long incl = x;
   for (int o = 1; o < 32; o <<= 1) {
@@ -165,32 +229,43 @@ __device__ long long block_exclusive_scan(long long x, long long& total, Shared&
   }
   if (l == 31) sh.red_l[w] = incl;
   __syncthreads();
-  if (w == 0) {
-    long long v = l < NW ? sh.red_l[l] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(FULL, v, o);
-      if (l >= o) v += y;
-    }
-    if (l < NW) sh.red_l[l] = v;  // inclusive warp prefix
-    if (l == 31) sh.red_l[32] = v;
-  }
+  long long before = 0;
+  for (int k = 0; k < w; ++k) before += sh.red_l[k];
   __syncthreads();
-  const long long before = w > 0 ? sh.red_l[w - 1] : 0;
-  total = sh.red_l[32];
-  __syncthreads();
-  return before + incl - x;
+  return before + incl;
 }
 
+// rn(x / u) for u = 2^(e-52) (an exact power-of-two scaling), with the
+// tie flag; x >= 4e15 u certainly leaves the binade in one step.
+__device__ __forceinline__ long long chain_round(double x, double inv_u, bool& tie) {
+  const double y = x * inv_u;
+  tie = false;
+  if (y >= 4.0e15) return 1ll << 53;
+  const double f = floor(y);
+  const double fr = y - f;
+  tie = fr == 0.5;
+  return (long long)f + (fr >= 0.5 ? 1 : 0);
+}
+
+// Advances the exact chain held in (sh.xk, sh.xs) to term kend. Each step
+// covers 32*UE consecutive terms per warp (coalesced); the first EVENT of a
+// step -- the term whose addition leaves the binade, or a rounding tie
+// (round-half-even then depends on the running sum) -- is found by the warp
+// whose range holds it with one lane scan per 32 terms; the sum before it
+// is exact in integer form and the event itself is one true fp64 add. Every
+// kChainSub-aligned boundary a step passes gets its binade recorded in
+// s.hec (the prediction exact_chain_helped hands to its helpers).
 template <int NT>
-__device__ double exact_chain(const Scenario& s, Shared& sh, int kind, int j, double newc,
-                              int mover, const double* col) {
-  constexpr int UE = 8;
-  constexpr int CH = NT * UE;
-  const int M = s.M;
+__device__ void chain_steps(const Scenario& s, Shared& sh, int kind, int j, double newc,
+                            int mover, const double* col, int kend) {
+  constexpr int NW = NT / 32;
+  constexpr int UE = 32;
+  constexpr long long LIM = 1ll << 53;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    double S = 0.0;
-    int k = 0;
-    while (k < M && !(S >= 0x1p-900)) {  // leading zeros / tiny values: plain adds
+    double S = sh.xs;
+    int k = sh.xk;
+    while (k < kend && !(S >= 0x1p-900)) {  // leading zeros / tiny values: plain adds
       S += chain_term(s, kind, k, j, newc, mover, col);
       ++k;
     }
@@ -198,86 +273,234 @@ __device__ double exact_chain(const Scenario& s, Shared& sh, int kind, int j, do
     sh.xk = k;
   }
   __syncthreads();
-  const long long LIM = 1ll << 53;
   while (true) {
     const int k0 = sh.xk;
     const double S0 = sh.xs;
-    if (k0 >= M) break;
+    if (k0 >= kend) break;
     const int e = ilogb(S0);
-    const double u = ldexp(1.0, e - 52);
-    const long long N0 = (long long)(S0 / u);
-    const int kb = k0 + threadIdx.x * UE;
-    long long rr[UE];
+    const double u = ldexp(1.0, e - 52), inv_u = ldexp(1.0, 52 - e);
+    const long long N0 = (long long)(S0 * inv_u);
+    // warp range [wb, wb + 32*nq): lane l holds terms wb + 32q + l; the
+    // warp's integer total is order-free. Short ranges are spread over all
+    // warps (one load round instead of nq).
+    const int per = min(32 * UE, (((kend - k0 + NW - 1) / NW) + 31) & ~31);
+    const int nq = per >> 5;
+    const int wb = k0 + w * per;
     long long local = 0;
     int first_tie = INT_MAX;
-#pragma unroll
-    for (int q = 0; q < UE; ++q) {
-      const int k = kb + q;
-      long long ri = 0;
-      if (k < M) {
-        const double x = chain_term(s, kind, k, j, newc, mover, col) / u;
-        if (x >= 4.0e15) {
-          ri = LIM;  // this step certainly leaves the binade
-        } else {
-          const double f = floor(x);
-          const double fr = x - f;
-          ri = (long long)f + (fr >= 0.5 ? 1 : 0);
-          if (fr == 0.5) first_tie = min(first_tie, k);
-        }
-      }
-      rr[q] = ri;
-      local += ri;
-    }
-    long long total;
-    long long run = N0 + block_exclusive_scan<NT>(local, total, sh);
-    int first_cross = INT_MAX;
-    long long before_cross = 0;
-#pragma unroll
-    for (int q = 0; q < UE; ++q) {
-      const int k = kb + q;
-      if (k < M && first_cross == INT_MAX) {
-        if (run + rr[q] >= LIM) {
-          first_cross = k;
-          before_cross = run;
-        }
-        run += rr[q];
+#pragma unroll 8
+    for (int q = 0; q < nq; ++q) {
+      const int k = wb + q * 32 + l;
+      if (k < kend) {
+        bool tie = false;
+        local += chain_round(chain_term(s, kind, k, j, newc, mover, col), inv_u, tie);
+        if (tie) first_tie = min(first_tie, k);
       }
     }
-    const int cross = block_min<NT>(first_cross, sh);
-    const int tie = block_min<NT>(first_tie, sh);
-    const int chunk_end = min(M, k0 + CH);
-    if (tie < min(cross, chunk_end)) {
-      // a rounding tie before the binade crossing: step to it exactly
-      if (threadIdx.x == 0) {
-        double S = S0;
-        for (int k = k0; k <= tie; ++k) S += chain_term(s, kind, k, j, newc, mover, col);
-        sh.xs = S;
-        sh.xk = tie + 1;
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(FULL, local, o);
+    local = min(local, LIM);  // saturate: only reaching LIM matters
+    first_tie = __reduce_min_sync(FULL, first_tie);
+    if (l == 0) sh.red_l[w] = local;
+    __syncthreads();
+    long long run = N0, total = 0;
+    for (int k = 0; k < NW; ++k) {
+      const long long v = sh.red_l[k];
+      if (k < w) run += v;
+      total += v;
+    }
+    int first_ev = INT_MAX;
+    long long before_ev = 0;
+    if (run + local >= LIM || first_tie != INT_MAX) {
+      for (int q = 0; q < nq; ++q) {
+        const int k = wb + q * 32 + l;
+        long long r = 0;
+        bool tq = false;
+        if (k < kend) r = chain_round(chain_term(s, kind, k, j, newc, mover, col), inv_u, tq);
+        long long incl = r;
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(FULL, incl, o);
+          if (l >= o) incl += y;
+        }
+        const unsigned hit = __ballot_sync(FULL, k < kend && (tq || run + incl >= LIM));
+        if (hit) {
+          const int f = __ffs(hit) - 1;
+          const long long excl = __shfl_sync(FULL, incl - r, f);
+          first_ev = wb + q * 32 + f;
+          before_ev = run + excl;
+          break;
+        }
+        run += __shfl_sync(FULL, incl, 31);
       }
-    } else if (cross == INT_MAX) {
+    }
+    const int ev = block_min<NT>(first_ev, sh);
+    // aligned boundaries in [k0, lim] have their running sum in binade e
+    const int lim = ev == INT_MAX ? min(kend, k0 + per * NW) : ev;
+    {
+      const int c = (k0 + kChainSub - 1) / kChainSub + threadIdx.x;
+      if ((long long)c * kChainSub <= lim) s.hec[c] = e;
+    }
+    if (ev == INT_MAX) {
       if (threadIdx.x == 0) {
         sh.xs = (double)(N0 + total) * u;
-        sh.xk = chunk_end;
+        sh.xk = min(kend, k0 + per * NW);
       }
-    } else if (first_cross == cross) {
-      // owner of the crossing step: exact partial sum, then one fp64 add
-      const double prev = (double)before_cross * u;
-      sh.xs = prev + chain_term(s, kind, cross, j, newc, mover, col);
-      sh.xk = cross + 1;
+    } else if (first_ev == ev && l == 0) {
+      // exact partial sum before the event, then the event's true fp64 add
+      const double prev = (double)before_ev * u;
+      sh.xs = prev + chain_term(s, kind, ev, j, newc, mover, col);
+      sh.xk = ev + 1;
     }
     __syncthreads();
+  }
+}
+
+template <int NT>
+__device__ double exact_chain(const Scenario& s, Shared& sh, int kind, int j, double newc,
+                              int mover, const double* col) {
+  if (threadIdx.x == 0) {
+    sh.xs = 0.0;
+    sh.xk = 0;
+  }
+  __syncthreads();
+  chain_steps<NT>(s, sh, kind, j, newc, mover, col, s.M);
+  const double r = sh.xs;
+  __syncthreads();
+  return r;
+}
+
+// Helper share of an exact chain: for chunks part, part + parts, ... the
+// sum of rn(term / u) in the binade the latest chain recorded for the
+// chunk's start, with that binade in hue -- or kNoBinade when the chunk
+// holds a rounding tie or a term that leaves the binade by itself (or no
+// binade is known).
+template <int NT>
+__device__ void helper_chain(const Scenario& s, Shared& sh, int kind, int j, double newc,
+                             int mover, int t, int part, int parts) {
+  constexpr int NW = NT / 32;
+  constexpr long long LIM = 1ll << 53;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int M = s.M;
+  const double* col = t >= 0 ? s.cost + (long long)t * M : nullptr;
+  const int nsub = (M + kChainSub - 1) / kChainSub;
+  for (int c = part; c < nsub; c += parts) {
+    const int e = __ldcg(&s.hec[c]);
+    if (e == kNoBinade) {
+      if (threadIdx.x == 0) s.hue[c] = kNoBinade;
+      continue;
+    }
+    const double inv_u = ldexp(1.0, 52 - e);
+    long long local = 0;
+    bool flag = false;
+#pragma unroll 4
+    for (int q = 0; q < kChainSub / NT; ++q) {
+      const int k = c * kChainSub + q * NT + threadIdx.x;
+      if (k < M) {
+        bool tie = false;
+        const long long r = chain_round(chain_term(s, kind, k, j, newc, mover, col), inv_u, tie);
+        flag |= tie || r >= LIM;
+        local = min(local + r, LIM);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(FULL, local, o);
+    local = min(local, LIM);
+    const bool wf = __any_sync(FULL, flag);
+    if (l == 0) {
+      sh.red_l[w] = local;
+      sh.red_i[1][w] = wf;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long tot = 0;
+      int f = 0;
+      for (int k = 0; k < NW; ++k) {
+        tot = min(tot + sh.red_l[k], LIM);
+        f |= sh.red_i[1][k];
+      }
+      s.hrs[c] = tot;
+      s.hue[c] = f ? kNoBinade : e;
+    }
+    __syncthreads();
+  }
+}
+
+// Exact chain with the helper blocks: the helpers sum every chunk's rounded
+// terms in its predicted binade (the binade recorded by the latest chain:
+// one move changes the sums too little to move most chunk boundaries across
+// a binade); the master then walks the chunks, consuming NT chunks per block
+// scan while the prediction holds (same binade, no tie, no crossing inside),
+// and runs chain_steps on every other chunk. Block-wide.
+template <int NT>
+__device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& sm, int kind,
+                                     int j, double newc, int mover, int t) {
+  constexpr long long LIM = 1ll << 53;
+  const int M = s.M;
+  const double* col = t >= 0 ? s.cost + (long long)t * M : nullptr;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    HelperCtl* hc = s.hc;
+    hc->ckind = kind;
+    hc->cj = j;
+    hc->cmover = mover;
+    hc->ct = t;
+    hc->cnewc = newc;
+    post_job(s, sh, sm, HJOB_CHAIN, 0, 0, 0);
+  }
+  wait_helpers<NT>(s, sh, sm);
+  if (threadIdx.x == 0) {
+    sh.xs = 0.0;
+    sh.xk = 0;
+  }
+  __syncthreads();
+  const int nsub = (M + kChainSub - 1) / kChainSub;
+  while (true) {
+    const int k = sh.xk;
+    const double S = sh.xs;
+    if (k >= M || sh.c.error) break;
+    if (k % kChainSub != 0 || !(S >= 0x1p-900)) {
+      chain_steps<NT>(s, sh, kind, j, newc, mover, col, min(M, (k / kChainSub + 1) * kChainSub));
+      continue;
+    }
+    const int e = ilogb(S);
+    const double u = ldexp(1.0, e - 52), inv_u = ldexp(1.0, 52 - e);
+    const long long N = (long long)(S * inv_u);
+    const int c = k / kChainSub;
+    const int cc = c + threadIdx.x;
+    // hue, not hec: the walk itself re-records hec as it goes
+    const bool ok = cc < nsub && __ldcg(&s.hue[cc]) == e;
+    const long long v = ok ? __ldcg(&s.hrs[cc]) : 0;
+    const long long incl = block_inclusive_scan<NT>(v, sh);
+    const bool good = ok && N + incl < LIM;
+    const int bad = block_min<NT>(good ? INT_MAX : (int)threadIdx.x, sh);
+    const int nok = bad == INT_MAX ? NT : bad;
+    if (nok > 0 && (int)threadIdx.x == nok - 1) {
+      sh.xs = (double)(N + incl) * u;
+      sh.xk = min(M, (c + nok) * kChainSub);
+    }
+    __syncthreads();
+    if (nok < NT && sh.xk < M)
+      chain_steps<NT>(s, sh, kind, j, newc, mover, col, min(M, (c + nok + 1) * kChainSub));
   }
   const double r = sh.xs;
   __syncthreads();
   return r;
 }
 
+// Exact chain, with the helpers when there are any and M is large.
+template <int NT>
+__device__ double exact_chain_any(const Scenario& s, Shared& sh, const Smem& sm, int kind, int j,
+                                  double newc, int mover, int t) {
+  if (sm.helpers > 0 && s.M >= 8 * kChainSub && sh.c.chain_mode == 0)
+    return exact_chain_helped<NT>(s, sh, sm, kind, j, newc, mover, t);
+  return exact_chain<NT>(s, sh, kind, j, newc, mover,
+                         t >= 0 ? s.cost + (long long)t * s.M : nullptr);
+}
+
 // Exact current total, cached per applied-move count.
 template <int NT>
-__device__ double exact_total(const Scenario& s, Shared& sh) {
+__device__ double exact_total(const Scenario& s, Shared& sh, const Smem& sm) {
   if (sh.c.total_ver == (long long)sh.c.applied) return sh.c.total_exact;
   const long long e0 = ph_now();
-  const double t = exact_chain<NT>(s, sh, 0, -1, 0.0, -1, nullptr);
+  const double t = exact_chain_any<NT>(s, sh, sm, 0, -1, 0.0, -1, -1);
   PH_ADD(sh, 9, e0);
   if (threadIdx.x == 0) {
     sh.c.total_exact = t;
@@ -550,6 +773,7 @@ __device__ __forceinline__ uint8_t table_class_n(const Scenario& s, const Shared
   const double A = s.rA[k];
   const double E = s.rE[k] + (double)(n + 2) * kTwoPowM52 * U * 1.0001;
   if (A - E > 0.0) return CLS_POS;
+  if (sh.c.force_exact & 2) return CLS_AMB;
   if (A + E + single_bound(s, sh) < 0.0) return CLS_ACC;
   if (A + E < 0.0) return CLS_NEG;
   return CLS_AMB;
@@ -730,6 +954,243 @@ __device__ void table_after_relocation(const Scenario& s, Shared& sh, const Smem
   table_row_fresh<NT>(s, sh, sm.acc_sum, sm.acc_abs, sm.stage, b_old);
 }
 
+
+// Helper share `part` of `parts` of the relocation of x from b_old to t:
+//  A. missions [m0, m1): x's missions take their cost at t (mc, mcp); the bit
+//     of their position in every other vehicle's imp row is recomputed; every
+//     mission's term cost(m, b_old) - mc[m] is summed per vehicle into
+//     hsum/habs (the vacated base's fresh relocation row, any-order sums
+//     with the same rigorous bounds as table_row_fresh);
+//  B. words [w0, w1) of x's own imp row.
+template <int NT>
+__device__ void helper_relocate(const Scenario& s, const Smem& sm, const int32_t* __restrict__ pb,
+                                int x, int t, int b_old, int part, int parts) {
+  constexpr int NW = NT / 32;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int V = s.V, M = s.M, nwd = s.nwd;
+  int* dlt = sm.lim_j;  // [V] this block's imp-row popcount deltas
+  double* as = sm.acc_sum + (long long)w * V;
+  double* aa = sm.acc_abs + (long long)w * V;
+  double* st = sm.stage + w * 32;
+  int* list = sm.xidx;  // [2*NT]
+  int* cnt = sm.wsum;
+  for (int v = l; v < V; v += 32) {
+    as[v] = 0.0;
+    aa[v] = 0.0;
+  }
+  for (int v = threadIdx.x; v < V; v += NT) dlt[v] = 0;
+  if (threadIdx.x == 0) *cnt = 0;
+  __syncthreads();
+  const double* colt = s.cost + (long long)t * M;
+  const double* colo = s.cost + (long long)b_old * M;
+  const int chunk = (int)((((long long)M + parts - 1) / parts + 31) & ~31ll);
+  const int m0 = (int)min((long long)M, (long long)part * chunk);
+  const int m1 = min(M, m0 + chunk);
+  for (int base = m0; base < m1; base += NT) {
+    const int m = base + threadIdx.x;
+    int v = -1;
+    double term = 0.0;
+    if (m < m1) {
+      v = s.mv[m];
+      double c = s.mc[m];
+      if (v == x) {
+        c = colt[m];
+        s.mc[m] = c;
+        s.mcp[s.invb[m]] = c;
+        list[atomicAdd(cnt, 1)] = m;
+      }
+      term = colo[m] - c;
+    }
+    const unsigned peers = __match_any_sync(FULL, v);
+    st[l] = term;
+    __syncwarp();
+    if (v >= 0 && l == __ffs(peers) - 1) {
+      double sum = 0.0, abs = 0.0;
+      for (unsigned b = peers; b; b &= b - 1) {
+        const double y = st[__ffs(b) - 1];
+        sum += y;
+        abs += fabs(y);
+      }
+      as[v] += sum;
+      aa[v] += abs;
+    }
+    __syncwarp();
+    __syncthreads();
+    // warp per listed mission, lanes over the other vehicles
+    const int n = *cnt;
+    for (int k = w; k < n; k += NW) {
+      const int mm = list[k];
+      const int q = s.invb[mm];
+      const double mcq = colt[mm];
+      const bool ro = s.ro[mm];
+      const uint32_t bit = 1u << (q & 31);
+      const int wd = q >> 5;
+      for (int g0 = 0; g0 < V; g0 += 32 * 4) {
+        bool on[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int g = g0 + u * 32 + l;
+          on[u] = g < V && g != x && compat_vm(s.vfixed[g], ro) && cost_mb(s, mm, s.vbase[g]) < mcq;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int g = g0 + u * 32 + l;
+          if (g >= V || g == x) continue;
+          uint32_t* wp = s.imp + (long long)g * nwd + wd;
+          const uint32_t old = on[u] ? atomicOr(wp, bit) : atomicAnd(wp, ~bit);
+          if (((old & bit) != 0u) != on[u]) atomicAdd(&dlt[g], on[u] ? 1 : -1);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *cnt = 0;
+  }
+  // B. x's own row
+  const bool fx = s.vfixed[x];
+  const int wchunk = (nwd + parts - 1) / parts;
+  const int w0 = (int)min((long long)nwd, (long long)part * wchunk);
+  const int w1 = min(nwd, w0 + wchunk);
+  int cb = 0;
+  for (int wd0 = w0 + w * 4; wd0 < w1; wd0 += NW * 4) {
+    bool b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = (wd0 + u) * 32 + l;
+      b[u] = false;
+      if (wd0 + u < w1 && q < M)
+        b[u] = s.mvp[q] != x && compat_vm(fx, s.rop[q]) && colt[pb[q]] < s.mcp[q];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned mk = __ballot_sync(FULL, b[u]);
+      if (l == 0 && wd0 + u < w1) {
+        s.imp[(long long)x * nwd + wd0 + u] = mk;
+        cb += __popc(mk);
+      }
+    }
+  }
+  if (l == 0 && cb) atomicAdd(&s.hc->impc_x, cb);
+  __syncthreads();
+  for (int v = threadIdx.x; v < V; v += NT) {
+    double sum = 0.0, abs = 0.0;
+    for (int k = 0; k < NW; ++k) {
+      sum += sm.acc_sum[(long long)k * V + v];
+      abs += sm.acc_abs[(long long)k * V + v];
+    }
+    if (abs != 0.0) {
+      atomicAdd(&s.hsum[v], sum);
+      atomicAdd(&s.habs[v], abs);
+    }
+    if (dlt[v]) atomicAdd(&s.hdelta[v], dlt[v]);
+  }
+}
+
+// Helper block main loop: wait for a job of this launch, do its share,
+// count done; return on QUIT (or on the hang guard).
+template <int NT>
+__device__ void helper_loop(const Scenario& s, Shared& sh, const Smem& sm, const int32_t* pb,
+                            int part, int parts) {
+  unsigned seen = 0;
+  while (true) {
+    if (threadIdx.x == 0) {
+      const long long t0 = clock64();
+      int kind = -1;
+      while (true) {
+        const unsigned long long v = ld_acquire_u64(&s.hc->seq);
+        if ((unsigned)(v >> 32) == sm.epoch && (unsigned)v > seen) {
+          seen = (unsigned)v;
+          kind = __ldcg(&s.hc->kind);
+          sh.bi[2] = __ldcg(&s.hc->x);
+          sh.bi[3] = __ldcg(&s.hc->t);
+          sh.bi[4] = __ldcg(&s.hc->b_old);
+          sh.bi[5] = __ldcg(&s.hc->ckind);
+          sh.bi[6] = __ldcg(&s.hc->cj);
+          sh.bi[7] = __ldcg(&s.hc->cmover);
+          sh.tmp = __ldcg(&s.hc->ct);
+          sh.bd0 = __ldcg(&s.hc->cnewc);
+          break;
+        }
+        if (clock64() - t0 > kSpinLimit) break;
+        __nanosleep(64);
+      }
+      sh.bi[0] = kind;
+    }
+    __syncthreads();
+    const int kind = sh.bi[0];
+    if (kind == HJOB_RELOCATE)
+      helper_relocate<NT>(s, sm, pb, sh.bi[2], sh.bi[3], sh.bi[4], part, parts);
+    else if (kind == HJOB_CHAIN)
+      helper_chain<NT>(s, sh, sh.bi[5], sh.bi[6], sh.bd0, sh.bi[7], sh.tmp, part, parts);
+    else
+      return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&s.hc->done, 1u);
+    }
+  }
+}
+
+// Relocation of x from b_old to t through pool slot pos, shared with the
+// helper blocks. Block-wide.
+template <int NT>
+__device__ void relocate_with_helpers(const Scenario& s, Shared& sh, const Smem& sm, int x, int t,
+                                      int pos, int b_old) {
+  __syncthreads();  // everyone has read the pre-move state
+  if (threadIdx.x == 0) {
+    s.bveh[b_old] = -1;
+    s.bveh[t] = x;
+    s.vbase[x] = t;
+    sm.gvbase[x] = t;
+    s.pkind[pos] = POOL_EMPTY;
+    s.pidx[pos] = b_old;
+    post_job(s, sh, sm, HJOB_RELOCATE, x, t, b_old);
+  }
+  // meanwhile every other empty row shifts by -D(t, x)
+  const long long kt = tix(s, t, x);
+  const double At = s.rA[kt], Et = s.rE[kt], Ut = s.rU[kt];
+  __syncthreads();  // bveh / vbase updated
+  for (int t2 = threadIdx.x; t2 < s.B; t2 += NT) {
+    if (s.bveh[t2] >= 0 || t2 == b_old) continue;
+    const long long k2 = tix(s, t2, x);
+    const int before = table_class(s, sh, t2, x) != CLS_POS;
+    const double A = s.rA[k2] - At;
+    s.rA[k2] = A;
+    s.rE[k2] += Et + 2.0 * kTwoPowM52 * (fabs(At) + fabs(A));
+    s.rU[k2] = (s.rU[k2] + Ut) * (1.0 + 2.0 * kTwoPowM52);
+    s.rcnt[t2] += (int)(table_class(s, sh, t2, x) != CLS_POS) - before;
+  }
+  if (threadIdx.x == 0) sh.tmp = 0;
+  wait_helpers<NT>(s, sh, sm);
+  // the vacated base's fresh row and the imp-row counts
+  int cnt = 0;
+  for (int v = threadIdx.x; v < s.V; v += NT) {
+    const double sum = __ldcg(&s.hsum[v]), abs = __ldcg(&s.habs[v]);
+    s.hsum[v] = 0.0;
+    s.habs[v] = 0.0;
+    const int n = s.vcount[v];
+    const long long k = tix(s, b_old, v);
+    const double U = abs * (1.0 + (double)(n + 2) * kTwoPowM52);
+    s.rA[k] = sum;
+    s.rU[k] = U;
+    s.rE[k] = (double)(n + 2) * kTwoPowM52 * U;
+    cnt += table_class(s, sh, b_old, v) != CLS_POS;
+    const int d = __ldcg(&s.hdelta[v]);
+    if (d) {
+      sm.impc[v] += d;
+      s.hdelta[v] = 0;
+    }
+  }
+  if (cnt) atomicAdd(&sh.tmp, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    s.rcnt[b_old] = sh.tmp;
+    sm.impc[x] = __ldcg(&s.hc->impc_x);
+    s.hc->impc_x = 0;
+  }
+  __syncthreads();
+}
+
 // ---- moves (proj/src/search.cpp:169-220) ---------------------------------
 // Thread 0 only unless noted.
 
@@ -818,10 +1279,13 @@ __device__ void debug_check(const Scenario& s, Shared& sh) {
 // candidate_total < total, both fixed-order fp64 sums. Block-wide; the new
 // exact total is cached when the move is accepted.
 template <int NT>
-__device__ bool exact_accept_single(const Scenario& s, Shared& sh, int j, double newc) {
+__device__ bool exact_accept_single(const Scenario& s, Shared& sh, const Smem& sm, int j,
+                                    double newc) {
   const long long f0 = ph_now();
-  const double S = exact_total<NT>(s, sh);
-  const double S2 = exact_chain<NT>(s, sh, 1, j, newc, -1, nullptr);
+  const double S = exact_total<NT>(s, sh, sm);
+  const long long c0 = ph_now();
+  const double S2 = exact_chain_any<NT>(s, sh, sm, 1, j, newc, -1, -1);
+  PH_ADD(sh, 13, c0);
   if (threadIdx.x == 0) {
     sh.c.fallbacks += 1;
     sh.xs = S2;  // the total after the move, if accepted
@@ -847,7 +1311,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
     const double mcj = s.mc[j];
     if (compat_vm(s.vfixed[g], s.ro[j]) && newc - mcj < 0.0) {
       int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
-      if (!acc) acc = exact_accept_single<NT>(s, sh, j, newc) ? 3 : 0;
+      if (!acc) acc = exact_accept_single<NT>(s, sh, sm, j, newc) ? 3 : 0;
       if (acc) {
         const int loser = s.mv[j];
         const int nl = s.vcount[loser], ng = s.vcount[g];
@@ -884,10 +1348,16 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         const long long f0 = ph_now();
         const double* col = s.cost + (long long)t * s.M;
         bool neg = cls == CLS_NEG;
-        if (!neg) neg = exact_reloc_quick<NT>(s, sh, col, mover, sm.xidx, 2 * NT) < 0.0;
+        if (!neg) {
+          const long long q0 = ph_now();
+          neg = exact_reloc_quick<NT>(s, sh, col, mover, sm.xidx, 2 * NT) < 0.0;
+          PH_ADD(sh, 12, q0);
+        }
         if (neg) {
-          const double S = exact_total<NT>(s, sh);
-          after = exact_chain<NT>(s, sh, 2, -1, 0.0, mover, col);
+          const double S = exact_total<NT>(s, sh, sm);
+          const long long c0 = ph_now();
+          after = exact_chain_any<NT>(s, sh, sm, 2, -1, 0.0, mover, t);
+          PH_ADD(sh, 13, c0);
           acc = after < S;
           exact_known = true;
         }
@@ -896,13 +1366,19 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       }
       if (acc) {
         const int b_old = s.vbase[mover];
-        const long long a0 = ph_now();
-        apply_relocate<NT>(s, sh, mover, t, i);
-        PH_ADD(sh, 8, a0);
-        const long long a1 = ph_now();
-        bits_after_relocation<NT>(s, sh, sm, mover, sm.xlist, sm.xlist_cap);
-        table_after_relocation<NT>(s, sh, sm, mover, t, b_old);
-        PH_ADD(sh, 6, a1);
+        if (sm.helpers > 0) {
+          const long long a1 = ph_now();
+          relocate_with_helpers<NT>(s, sh, sm, mover, t, i, b_old);
+          PH_ADD(sh, 6, a1);
+        } else {
+          const long long a0 = ph_now();
+          apply_relocate<NT>(s, sh, mover, t, i);
+          PH_ADD(sh, 8, a0);
+          const long long a1 = ph_now();
+          bits_after_relocation<NT>(s, sh, sm, mover, sm.xlist, sm.xlist_cap);
+          table_after_relocation<NT>(s, sh, sm, mover, t, b_old);
+          PH_ADD(sh, 6, a1);
+        }
         if (threadIdx.x == 0) {
           sh.c.applied += 1;
           sh.c.pass_applied += 1;
@@ -934,7 +1410,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       const double mcj = s.mc[j];
       if (newc - mcj < 0.0) {
         int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
-        if (!acc) acc = exact_accept_single<NT>(s, sh, j, newc) ? 3 : 0;
+        if (!acc) acc = exact_accept_single<NT>(s, sh, sm, j, newc) ? 3 : 0;
         if (acc) {
           const int nl = s.vcount[l], ng = s.vcount[g];
           __syncthreads();
@@ -1295,9 +1771,11 @@ template <int NT>
 __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
                 int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
-                int debug_i, int state_in_smem, int bits_in_smem) {
-  if (!active[blockIdx.x]) return;
-  const Scenario g = scs[blockIdx.x];
+                int debug_i, int state_in_smem, int bits_in_smem, int helpers, unsigned epoch) {
+  // with helpers the grid is one scenario: block 0 runs it, the others help
+  const int scn = helpers > 0 ? 0 : blockIdx.x;
+  if (!active[scn]) return;
+  const Scenario g = scs[scn];
   if (g.ctr->done) return;  // finished earlier in this chunk of launches
   Scenario s = g;
   const bool tabu = tabu_i != 0, debug = debug_i != 0;
@@ -1327,6 +1805,13 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   sm.jl_outer = take(V);
   sm.impc = reinterpret_cast<int*>(take(4ull * V));
   sm.pb = perms + s.M;
+  sm.helpers = helpers;
+  sm.epoch = epoch;
+  sm.gvbase = g.vbase;
+  if (helpers > 0 && blockIdx.x > 0) {
+    helper_loop<NT>(g, sh, sm, perms + s.M, blockIdx.x - 1, helpers);
+    return;
+  }
   if (state_in_smem) {
     // the small mutable state lives in shared memory for the whole pass
     s.exp_take = reinterpret_cast<long long*>(take(8ull * V));
@@ -1371,6 +1856,8 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   if (threadIdx.x == 0) {
     sh.c = *s.ctr;
     sh.jexp_max = LLONG_MIN;
+    sh.hk = 0;
+    sh.hdone = helpers > 0 ? s.hc->done : 0u;
   }
   __syncthreads();
   {
@@ -1513,6 +2000,10 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     for (int b = threadIdx.x; b < B; b += NT) g.bveh[b] = s.bveh[b];
   }
   if (threadIdx.x == 0) *g.ctr = sh.c;
+  if (helpers > 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) post_job(s, sh, sm, HJOB_QUIT, -1, -1, -1);
+  }
 }
 
 // The row-major copy of the table, 32 x 32 tiles through shared memory.
@@ -1587,7 +2078,8 @@ template <int NT>
 static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int n_scn,
                                   const int32_t* d_perms, int kpasses, bool inkernel,
                                   int max_passes, int M, bool tabu, long long tenure, bool debug,
-                                  int V, int B, int K, cudaStream_t stream) {
+                                  int V, int B, int K, int helpers_req, unsigned epoch,
+                                  cudaStream_t stream) {
   const size_t core = pass_smem_core(V, NT);
   const size_t state = pass_smem_state(V, B, K);
   const size_t bits = 2 * align16(4ull * V * ((M + 31) / 32));
@@ -1596,12 +2088,32 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   const size_t bits_limit = NT == 256 ? 100 * 1024 : limit;
   if (core > limit) return cudaErrorInvalidConfiguration;
   const int in_smem = core + state <= limit ? 1 : 0;
-  const int bits_smem = in_smem && core + state + bits <= bits_limit ? 1 : 0;
+  int bits_smem = in_smem && core + state + bits <= bits_limit ? 1 : 0;
+  if (const char* e = std::getenv("FLEETPLACE_BITS_SMEM")) bits_smem = bits_smem && std::atoi(e) != 0;
   const size_t smem = core + (in_smem ? state : 0) + (bits_smem ? bits : 0);
   cudaFuncSetAttribute(pass_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // helper blocks: one scenario, one pass per launch, bitsets in global
+  // memory, and every block co-resident (cooperative launch)
+  int helpers = 0;
+  if (helpers_req != 0 && n_scn == 1 && kpasses == 1 && !inkernel && !bits_smem) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_kernel<NT>, NT, smem);
+    helpers = per_sm * sms - 1;
+    if (helpers_req > 0 && helpers_req < helpers) helpers = helpers_req;
+    if (helpers < 0) helpers = 0;
+  }
+  if (helpers > 0) {
+    int ip = inkernel ? 1 : 0, t = tabu ? 1 : 0, d = debug ? 1 : 0;
+    void* args[] = {&d_scs, &d_active, &d_perms, &kpasses, &ip, &max_passes, &t, &tenure, &d,
+                    (void*)&in_smem, (void*)&bits_smem, &helpers, &epoch};
+    return cudaLaunchCooperativeKernel((const void*)pass_kernel<NT>, dim3(1 + helpers), dim3(NT),
+                                       args, smem, stream);
+  }
   pass_kernel<NT><<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
                                                max_passes, tabu, tenure, debug, in_smem,
-                                               bits_smem);
+                                               bits_smem, 0, epoch);
   return cudaGetLastError();
 }
 
@@ -1622,15 +2134,15 @@ cudaError_t launch_sweep(Scenario* d_scs, const int32_t* d_active, int n_scn,
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,
                         bool tabu, long long tenure, bool debug, int V, int B, int K,
-                        cudaStream_t stream, int threads) {
+                        cudaStream_t stream, int threads, int helpers_req, unsigned epoch) {
   if (threads == 1024)
     return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                                M, tabu, tenure, debug, V, B, K, stream);
+                                M, tabu, tenure, debug, V, B, K, helpers_req, epoch, stream);
   if (threads == 512)
     return launch_pass_nt<512>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                               M, tabu, tenure, debug, V, B, K, stream);
+                               M, tabu, tenure, debug, V, B, K, helpers_req, epoch, stream);
   return launch_pass_nt<256>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                             M, tabu, tenure, debug, V, B, K, stream);
+                             M, tabu, tenure, debug, V, B, K, helpers_req, epoch, stream);
 }
 
 cudaError_t launch_init(Scenario* d_scs, int n_scn, int M, int maxB, int maxV, bool cost_t,

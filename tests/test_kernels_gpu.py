@@ -184,3 +184,59 @@ def test_golden_shapes_on_device():
         assert s.final_objective_km == sh["final_objective_km"]
         assert hashlib.sha256(r.vehicle_base.tobytes() + r.mission_vehicle.tobytes()).hexdigest() \
             == sh["assignment_sha256"]
+
+
+def test_large_instance_helpers_and_table_copy_do_not_change_trajectory(monkeypatch):
+    """c3 shape (2000 x 100k x 100), 3 passes: the helper-block relocations
+    and the row-major table copy are execution strategies only — the same
+    SearchStats and Assignment with each of them switched off."""
+    inst = F.survey_instance(2000, 100000, 100, seed=1)
+    t = F.build_distance_table(inst)
+    start = F.rank_bases(inst, t)
+    pool = F.initial_pool(start, inst)
+    vb, mv, pk, px = F._state_arrays(start.assignment, pool, inst)
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=3)
+    runs = []
+    for env in ({}, {"FLEETPLACE_HELPERS": "0"}, {"FLEETPLACE_COST_T": "0"}):
+        for k in ("FLEETPLACE_HELPERS", "FLEETPLACE_COST_T"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        r = F.search_arrays(inst, t, cfg, vb, mv, pk, px)
+        runs.append(r)
+    keys = ("passes", "evaluations", "applied_moves", "tabu_skips_outer", "tabu_skips_inner",
+            "final_objective_km")
+    for r in runs[1:]:
+        assert tuple(getattr(r.stats, k) for k in keys) == tuple(getattr(runs[0].stats, k) for k in keys)
+        assert np.array_equal(r.vehicle_base, runs[0].vehicle_base)
+        assert np.array_equal(r.mission_vehicle, runs[0].mission_vehicle)
+
+
+def _stats_key(r):
+    return tuple(getattr(r.stats, k) for k in ("passes", "evaluations", "applied_moves",
+                                               "tabu_skips_outer", "tabu_skips_inner",
+                                               "final_objective_km"))
+
+
+@pytest.mark.parametrize("shape,passes,force", [((2000, 100000, 100), 3, "1"),
+                                                ((5000, 1000000, 250), 2, "0")])
+def test_helper_assisted_exact_chains_match_single_block_chains(monkeypatch, shape, passes, force):
+    """The helper-assisted exact chains (predicted-binade chunk sums walked by
+    the master) against the single-block chains: identical trajectories on
+    c3 with every total comparison forced through the chains, and on c4's
+    first two passes (about 90 exact decisions, ~170 chains of 1M terms)."""
+    inst = F.survey_instance(*shape, seed=1)
+    t = F.build_distance_table(inst)
+    start = F.rank_bases(inst, t)
+    pool = F.initial_pool(start, inst)
+    vb, mv, pk, px = F._state_arrays(start.assignment, pool, inst)
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=passes)
+    monkeypatch.setenv("FLEETPLACE_FORCE_EXACT", force)
+    runs = []
+    for chains in ("1", "0"):
+        monkeypatch.setenv("FLEETPLACE_HELPED_CHAINS", chains)
+        runs.append(F.search_arrays(inst, t, cfg, vb, mv, pk, px))
+    assert runs[0].stats.exact_fallbacks > 0
+    assert _stats_key(runs[0]) == _stats_key(runs[1])
+    assert np.array_equal(runs[0].vehicle_base, runs[1].vehicle_base)
+    assert np.array_equal(runs[0].mission_vehicle, runs[1].mission_vehicle)

@@ -113,3 +113,48 @@ def test_end_to_end_pipeline_matches_reference(shape, seeds, passes):
         assert (got.mission_vehicle >= 0).all()
         fixed = inst.vehicle_kind[got.mission_vehicle] == 1
         assert not (fixed & (inst.rotary_only == 1)).any()
+
+
+@pytest.mark.parametrize("helpers", ["-1", "5"])
+def test_helper_blocks_forced(monkeypatch, helpers):
+    """Relocations shared with helper blocks (forced on a c2 instance with the
+    bitsets kept in global memory; -1 = one block per free SM slot, 5 = an
+    uneven split) follow the reference's trajectory exactly."""
+    monkeypatch.setenv("FLEETPLACE_HELPERS", helpers)
+    monkeypatch.setenv("FLEETPLACE_BITS_SMEM", "0")
+    inst = ref_survey_instance(500, 10000, 40, seed=1)
+    _check_search(inst, 1, seeds=[7], max_passes=3)
+
+
+def test_helper_blocks_default_large():
+    """M >= 32k: helper blocks are on by default."""
+    inst = ref_survey_instance(300, 40000, 60, seed=3)
+    _check_search(inst, 1, seeds=[7], max_passes=2)
+
+
+@pytest.mark.parametrize("case", ["c1", "small", "trap", "c5_prefix"])
+def test_forced_exact_decisions(monkeypatch, case):
+    """Test hook FLEETPLACE_FORCE_EXACT: the error bounds settle nothing, so
+    every takeover / reassignment and every relocation that is not certainly
+    non-improving goes through the exact fixed-order chains (exact_chain,
+    exact_reloc_quick, fresh table rows). The trajectory must not change."""
+    monkeypatch.setenv("FLEETPLACE_FORCE_EXACT", "3")
+    if case == "c1":
+        _check_search(ref_survey_instance(50, 200, 10), 1, seeds=[1, 7])
+        _check_search(ref_survey_instance(50, 200, 10), 0, seeds=[3])
+    elif case == "small":
+        for seed in range(4):
+            _check_search(ref_small_generated(16000 + seed, 15, 12, 8), 1, seeds=[seed])
+    elif case == "trap":
+        _check_search(ref_small_generated(17010, 6, 5, 3, 2, 1), 1, seeds=[6])
+    else:
+        _check_search(ref_survey_instance(200, 5000, 20, seed=1), 1, seeds=[7], max_passes=1)
+
+
+def test_forced_exact_totals_with_helper_chains(monkeypatch):
+    """M = 40k with helper blocks: every total comparison goes through the
+    helper-assisted exact chains (chunk sums in the predicted binade, walked
+    by the master) -- the trajectory must equal the reference's."""
+    monkeypatch.setenv("FLEETPLACE_FORCE_EXACT", "1")
+    inst = ref_survey_instance(300, 40000, 60, seed=3)
+    _check_search(inst, 1, seeds=[7], max_passes=1)

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -45,6 +46,9 @@ struct fp_ctx {
   // pinned staging for permutations (double-buffered)
   int32_t* h_perm[2] = {nullptr, nullptr};
   size_t perm_cap = 0;
+  // device workspace of the searches (grow-only: no allocation per call)
+  unsigned char* ws = nullptr;
+  size_t ws_cap = 0;
 };
 
 namespace {
@@ -300,12 +304,6 @@ long long resolve_tenure(const fp_search_config* cfg, int M) {
   return tenure;
 }
 
-// Device arena for n scenarios: one allocation, carved per scenario.
-struct Arena {
-  DBuf<unsigned char> mem;
-  std::vector<fpk::Scenario> scs;
-  size_t per = 0;
-};
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -366,13 +364,20 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
 
 struct SearchRun {
   std::vector<HostScenario> hs;
-  Arena arena;
-  DBuf<fpk::Scenario> d_scs;
-  DBuf<int32_t> d_active;
-  DBuf<int32_t> d_perm;  // [2*M]
-  DBuf<fpk::Counters> d_ctr;  // [n], contiguous: one copy per pass
-  DBuf<double> costT;         // row-major table copies (optional)
+  std::vector<fpk::Scenario> scs;
   std::vector<Layout> lay;
+};
+
+// FLEETPLACE_TRACE=1: host-side timestamps of a search on stderr.
+struct Trace {
+  bool on = std::getenv("FLEETPLACE_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) const {
+    if (!on) return;
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[fleetplace trace] %8.3f ms  %s\n", ms, what);
+  }
 };
 
 // Shared driver for fp_search / fp_search_batch. `tables[s]` is a device
@@ -390,27 +395,13 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   const bool tabu = cfg->mode == FP_MODE_TABU;
   const long long tenure = resolve_tenure(cfg, M);
   cudaStream_t st = ctx->stream;
+  const Trace tr;
 
   SearchRun run;
   run.hs.reserve(n);
   for (int s = 0; s < n; ++s) run.hs.push_back(prepare(&insts[s], &starts[s]));
 
   // ---- arena
-  // A row-major copy of each table (mission-major: one mission's costs at
-  // every base contiguous) serves the per-move updates that run over bases;
-  // it is made when device memory allows (FLEETPLACE_COST_T=0 disables it).
-  bool cost_t = true;
-  if (const char* e = std::getenv("FLEETPLACE_COST_T")) cost_t = std::atoi(e) != 0;
-  if (cost_t) {
-    size_t need = 0;
-    for (int s = 0; s < n; ++s) {
-      const int V = insts[s].n_vehicles, B = insts[s].n_bases;
-      need += layout(M, B, V, run.hs[s].K, run.hs[s].psize + V + 1, dev_tables[s] == nullptr).total +
-              8ull * M * B;
-    }
-    size_t free_b = 0, total_b = 0;
-    cost_t = cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && need + (2ull << 30) <= free_b;
-  }
   size_t total = 0;
   run.lay.resize(n);
   std::vector<size_t> base(n);
@@ -425,18 +416,63 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     base[s] = total;
     total += run.lay[s].total;
   }
-  run.arena.mem.alloc(std::max<size_t>(total, 256));
-  // the row-major copies: device-only, filled by launch_init, never staged
+  tr.mark("prepared");
+  // Small scenarios run many passes per launch, each block rebuilding its
+  // own mirrors/bitsets between passes (scenarios of a batch progress
+  // independently); large ones run one pass per launch after the grid-wide
+  // sweep. Permutations for a chunk of passes are generated on the host
+  // while the device runs the previous chunk.
+  const bool inkernel = n > 1 || (long long)maxV * M <= (64ll << 10);
+  // passes per host round trip: in-kernel mode runs them in one launch; the
+  // sweep mode enqueues (sweep, pass) launch pairs that exit at once when the
+  // scenario is done, so the host only synchronises once per chunk
+  int kchunk = (int)std::max<long long>(
+      1, std::min<long long>(inkernel ? 64 : 16, (16ll << 20) / (8ll * std::max(M, 1))));
+  if (const char* e = std::getenv("FLEETPLACE_KPASSES")) kchunk = std::max(1, std::atoi(e));
+  const size_t chunk_ints = 2ull * kchunk * M + 2;
+  // ---- device workspace (owned by the context, reused across calls):
+  // arena | row-major table copies | counters | scenarios | active | perms.
+  // The row-major copy of each table (mission-major: one mission's costs at
+  // every base contiguous) serves the per-move updates that run over bases;
+  // it is left out when memory is short (FLEETPLACE_COST_T=0 disables it).
+  bool cost_t = true;
+  if (const char* e = std::getenv("FLEETPLACE_COST_T")) cost_t = std::atoi(e) != 0;
+  size_t tt = 0;
   std::vector<size_t> tbase(n, 0);
-  if (cost_t) {
-    size_t tt = 0;
-    for (int s = 0; s < n; ++s) {
-      tbase[s] = tt;
-      tt += (size_t)M * insts[s].n_bases;
-    }
-    run.costT.alloc(std::max<size_t>(tt, 1));
+  for (int s = 0; s < n; ++s) {
+    tbase[s] = tt;
+    tt += (size_t)M * insts[s].n_bases;
   }
-  run.d_ctr.alloc(n);
+  const size_t o_ctr = align_up(total), o_scs = align_up(o_ctr + sizeof(fpk::Counters) * n),
+               o_act = align_up(o_scs + sizeof(fpk::Scenario) * n),
+               o_perm = align_up(o_act + 4ull * n), o_costT = align_up(o_perm + 4ull * chunk_ints);
+  auto ws_get = [&](size_t bytes) -> bool {
+    if (bytes <= ctx->ws_cap) return true;
+    if (ctx->ws) {
+      cudaStreamSynchronize(st);
+      cudaFree(ctx->ws);
+    }
+    ctx->ws = nullptr;
+    ctx->ws_cap = 0;
+    const size_t want = bytes + bytes / 8;
+    if (cudaMalloc(&ctx->ws, want) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->ws = nullptr;
+      return false;
+    }
+    ctx->ws_cap = want;
+    return true;
+  };
+  if (!(cost_t && ws_get(o_costT + 8ull * tt))) {
+    cost_t = false;
+    if (!ws_get(o_costT)) throw FpError(FP_ERR_OUT_OF_MEMORY, "search workspace");
+  }
+  unsigned char* const d0 = ctx->ws;
+  fpk::Counters* const d_ctr = reinterpret_cast<fpk::Counters*>(d0 + o_ctr);
+  fpk::Scenario* const d_scs = reinterpret_cast<fpk::Scenario*>(d0 + o_scs);
+  int32_t* const d_active = reinterpret_cast<int32_t*>(d0 + o_act);
+  int32_t* const d_perm = reinterpret_cast<int32_t*>(d0 + o_perm);
+  double* const d_costT = reinterpret_cast<double*>(d0 + o_costT);
   std::vector<fpk::Counters> ctrs(n);
   for (int s = 0; s < n; ++s) {
     ctrs[s] = fpk::Counters{};
@@ -445,9 +481,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     if (const char* e = std::getenv("FLEETPLACE_FORCE_EXACT")) ctrs[s].force_exact = std::atoi(e);
     if (const char* e = std::getenv("FLEETPLACE_HELPED_CHAINS")) ctrs[s].chain_mode = std::atoi(e) == 0;
   }
-  unsigned char* d0 = run.arena.mem.p;
   std::vector<unsigned char> stage(total, 0);
-  run.arena.scs.resize(n);
+  run.scs.resize(n);
   for (int s = 0; s < n; ++s) {
     const HostScenario& h = run.hs[s];
     const Layout& L = run.lay[s];
@@ -468,9 +503,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     if (h.psize) std::memcpy(hb + L.pidx, h.pidx.data(), 4ull * h.psize);
     if (!dev_tables[s] && (size_t)M * B)
       std::memcpy(hb + L.cost, host_tables[s], 8ull * M * B);
-    fpk::Scenario& S = run.arena.scs[s];
+    fpk::Scenario& S = run.scs[s];
     S.cost = dev_tables[s] ? dev_tables[s] : reinterpret_cast<const double*>(db + L.cost);
-    S.costT = cost_t ? run.costT.p + tbase[s] : nullptr;
+    S.costT = cost_t ? d_costT + tbase[s] : nullptr;
     S.ro = db + L.ro;
     S.vfixed = db + L.vfixed;
     S.bheli = db + L.bheli;
@@ -511,7 +546,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       for (size_t c = 0; c < nsub; ++c) he[c] = fpk::kNoBinade;
     }
     S.nwd = (M + 31) / 32;
-    S.ctr = run.d_ctr.p + s;
+    S.ctr = d_ctr + s;
     S.M = M;
     S.B = B;
     S.V = V;
@@ -523,38 +558,23 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   check(cudaEventCreate(&ev1), "event");
   check(cudaEventRecord(ev0, st), "event");
   h2d(d0, stage.data(), total, st);
-  run.d_scs.alloc(n);
-  h2d(run.d_scs.p, run.arena.scs.data(), n, st);
-  run.d_active.alloc(n);
+  h2d(d_scs, run.scs.data(), n, st);
   std::vector<int32_t> active(n, 1);
-  h2d(run.d_ctr.p, ctrs.data(), n, st);
-  // Small scenarios run many passes per launch, each block rebuilding its
-  // own mirrors/bitsets between passes (scenarios of a batch progress
-  // independently); large ones run one pass per launch after the grid-wide
-  // sweep. Permutations for a chunk of passes are generated on the host
-  // while the device runs the previous chunk.
-  const bool inkernel = n > 1 || (long long)maxV * M <= (64ll << 10);
-  // passes per host round trip: in-kernel mode runs them in one launch; the
-  // sweep mode enqueues (sweep, pass) launch pairs that exit at once when the
-  // scenario is done, so the host only synchronises once per chunk
-  int kchunk = (int)std::max<long long>(
-      1, std::min<long long>(inkernel ? 64 : 16, (16ll << 20) / (8ll * std::max(M, 1))));
-  if (const char* e = std::getenv("FLEETPLACE_KPASSES")) kchunk = std::max(1, std::atoi(e));
-  const size_t chunk_ints = 2ull * kchunk * M + 2;
+  h2d(d_ctr, ctrs.data(), n, st);
   if (ctx->perm_cap < chunk_ints) {
     for (auto& p : ctx->h_perm)
       if (p) cudaFreeHost(p), p = nullptr;
     for (auto& p : ctx->h_perm) check(cudaMallocHost(&p, sizeof(int32_t) * chunk_ints), "pinned");
     ctx->perm_cap = chunk_ints;
   }
-  run.d_perm.alloc(chunk_ints);
   double init_ms = 0.0, sweep_ms = 0.0;
   {
     EvTimer ti(st);
-    check(fpk::launch_init(run.d_scs.p, n, M, maxB, maxV, cost_t, st), "init_kernel");
+    check(fpk::launch_init(d_scs, n, M, maxB, maxV, cost_t, st), "init_kernel");
     init_ms = ti.stop_ms();
   }
   ctx->launches += 1 + (maxB > 0 ? 1 : 0) + (cost_t && M > 0 && maxB > 0 ? 1 : 0);
+  tr.mark("allocated, staged, init launched");
   std::vector<cudaEvent_t> sweep_ev;  // (start, end) pairs around grid-wide sweeps
   PermStream rng(cfg->seed);
   auto gen_chunk = [&](int32_t* buf) {
@@ -565,6 +585,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   };
   int buf = 0;
   gen_chunk(ctx->h_perm[buf]);
+  tr.mark("first permutation chunk");
   int threads = n == 1 ? 512 : 256;
   if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
   // large single scenarios share each relocation's O(M) work with helper
@@ -574,10 +595,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   unsigned epoch = 0;
   int n_active = n;
   while (n_active > 0) {
-    h2d(run.d_active.p, active.data(), n, st);
-    h2d(run.d_perm.p, ctx->h_perm[buf], 2ull * kchunk * M, st);
+    h2d(d_active, active.data(), n, st);
+    h2d(d_perm, ctx->h_perm[buf], 2ull * kchunk * M, st);
     if (inkernel) {
-      check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p, kchunk, true,
+      check(fpk::launch_pass(d_scs, d_active, n, d_perm, kchunk, true,
                              cfg->max_passes, M, tabu, tenure, cfg->debug_check_deltas != 0, maxV,
                              maxB, maxK, st, threads, 0, 0u),
             "pass_kernel");
@@ -588,12 +609,12 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
-        check(fpk::launch_sweep(run.d_scs.p, run.d_active.p, n, run.d_perm.p + 2ll * k * M, M, st),
+        check(fpk::launch_sweep(d_scs, d_active, n, d_perm + 2ll * k * M, M, st),
               "prep_kernel");
         cudaEventRecord(e1, st);
         sweep_ev.push_back(e0);
         sweep_ev.push_back(e1);
-        check(fpk::launch_pass(run.d_scs.p, run.d_active.p, n, run.d_perm.p + 2ll * k * M, 1,
+        check(fpk::launch_pass(d_scs, d_active, n, d_perm + 2ll * k * M, 1,
                                false, cfg->max_passes, M, tabu, tenure,
                                cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads,
                                helpers, ++epoch),
@@ -604,7 +625,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     // next chunk's permutations while the device works
     const int nb = buf ^ 1;
     gen_chunk(ctx->h_perm[nb]);
-    d2h(ctrs.data(), run.d_ctr.p, n, st);
+    d2h(ctrs.data(), d_ctr, n, st);
     check(cudaStreamSynchronize(st), "pass sync");
     for (size_t e = 0; e + 1 < sweep_ev.size(); e += 2) {
       float ms = 0.f;
@@ -615,6 +636,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     }
     sweep_ev.clear();
     buf = nb;
+    tr.mark("chunk synchronised");
     for (int s = 0; s < n; ++s) {
       if (!active[s]) continue;
       if (ctrs[s].done || ctrs[s].error) {
@@ -623,15 +645,16 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       }
     }
   }
-  check(fpk::launch_final(run.d_scs.p, n, st), "final_kernel");
+  check(fpk::launch_final(d_scs, n, st), "final_kernel");
   ctx->launches += 1;
   check(cudaEventRecord(ev1, st), "event");
-  d2h(ctrs.data(), run.d_ctr.p, n, st);
+  d2h(ctrs.data(), d_ctr, n, st);
   for (int s = 0; s < n; ++s) {
-    d2h(outs[s].vehicle_base, run.arena.scs[s].vbase, insts[s].n_vehicles, st);
-    d2h(outs[s].mission_vehicle, run.arena.scs[s].mv, (size_t)M, st);
+    d2h(outs[s].vehicle_base, run.scs[s].vbase, insts[s].n_vehicles, st);
+    d2h(outs[s].mission_vehicle, run.scs[s].mv, (size_t)M, st);
   }
   check(cudaStreamSynchronize(st), "final sync");
+  tr.mark("final sync");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
   cudaEventDestroy(ev0);
@@ -659,6 +682,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     for (int k = 0; k < 5; ++k) outs[s].event_counts[k] = c.counts[k];
     outs[s].kernel_launches = ctx->launches;
   }
+  tr.mark("done");
 }
 
 }  // namespace
@@ -692,6 +716,7 @@ void fp_ctx_destroy(fp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_cost) cudaFree(ctx->d_cost);
+  if (ctx->ws) cudaFree(ctx->ws);
   for (auto& p : ctx->h_perm)
     if (p) cudaFreeHost(p);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);

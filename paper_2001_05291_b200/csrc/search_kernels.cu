@@ -88,6 +88,8 @@ struct Smem {
   int helpers;         // helper blocks sharing relocations (0 = none)
   unsigned epoch;      // launch number (helper job tags)
   int32_t* gvbase;     // global vbase (helpers read the mover's new base)
+  int32_t* gmv;        // global mv / mvp when the block works on shared-memory
+  int32_t* gmvp;       //   copies (written through), else null
 };
 
 // Phase timing (thread 0's SM clock), accumulated into Counters::cycles.
@@ -1194,17 +1196,22 @@ __device__ void relocate_with_helpers(const Scenario& s, Shared& sh, const Smem&
 // ---- moves (proj/src/search.cpp:169-220) ---------------------------------
 // Thread 0 only unless noted.
 
-__device__ void set_mission(const Scenario& s, int j, int v, double c) {
+__device__ void set_mission(const Scenario& s, const Smem& sm, int j, int v, double c) {
   s.mv[j] = v;
   s.mc[j] = c;
   const int q = s.invb[j];
   s.mvp[q] = v;
   s.mcp[q] = c;
+  if (sm.gmv) {
+    sm.gmv[j] = v;
+    sm.gmvp[q] = v;
+  }
 }
 
-__device__ void apply_takeover(const Scenario& s, Shared& sh, int j, int gain, int pos) {
+__device__ void apply_takeover(const Scenario& s, Shared& sh, const Smem& sm, int j, int gain,
+                               int pos) {
   const int loser = s.mv[j];
-  set_mission(s, j, gain, cost_mb(s, j, s.vbase[gain]));
+  set_mission(s, sm, j, gain, cost_mb(s, j, s.vbase[gain]));
   s.vcount[gain] += 1;
   s.vcount[loser] -= 1;
   if (s.vcount[loser] == 0) {
@@ -1219,9 +1226,9 @@ __device__ void apply_takeover(const Scenario& s, Shared& sh, int j, int gain, i
   }
 }
 
-__device__ void apply_reassign(const Scenario& s, Shared& sh, int j, int gain) {
+__device__ void apply_reassign(const Scenario& s, Shared& sh, const Smem& sm, int j, int gain) {
   const int loser = s.mv[j];
-  set_mission(s, j, gain, cost_mb(s, j, s.vbase[gain]));
+  set_mission(s, sm, j, gain, cost_mb(s, j, s.vbase[gain]));
   s.vcount[gain] += 1;
   s.vcount[loser] -= 1;
   if (s.vcount[loser] == 0) {
@@ -1317,7 +1324,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         const int nl = s.vcount[loser], ng = s.vcount[g];
         __syncthreads();  // everyone has read the pre-move state
         if (threadIdx.x == 0) {
-          apply_takeover(s, sh, j, g, i);
+          apply_takeover(s, sh, sm, j, g, i);
           sh.c.applied += 1;
           sh.c.pass_applied += 1;
           if (acc == 3) {
@@ -1415,7 +1422,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           const int nl = s.vcount[l], ng = s.vcount[g];
           __syncthreads();
           if (threadIdx.x == 0) {
-            apply_reassign(s, sh, j, g);
+            apply_reassign(s, sh, sm, j, g);
             sh.c.applied += 1;
             sh.c.pass_applied += 1;
             if (acc == 3) {
@@ -1771,7 +1778,8 @@ template <int NT>
 __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
                 int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
-                int debug_i, int state_in_smem, int bits_in_smem, int helpers, unsigned epoch) {
+                int debug_i, int state_in_smem, int bits_in_smem, int mirrors_in_smem,
+                int helpers, unsigned epoch) {
   // with helpers the grid is one scenario: block 0 runs it, the others help
   const int scn = helpers > 0 ? 0 : blockIdx.x;
   if (!active[scn]) return;
@@ -1808,6 +1816,8 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   sm.helpers = helpers;
   sm.epoch = epoch;
   sm.gvbase = g.vbase;
+  sm.gmv = nullptr;
+  sm.gmvp = nullptr;
   if (helpers > 0 && blockIdx.x > 0) {
     helper_loop<NT>(g, sh, sm, perms + s.M, blockIdx.x - 1, helpers);
     return;
@@ -1853,6 +1863,24 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     s.imp = reinterpret_cast<uint32_t*>(take(4ull * V * s.nwd));
     s.mem = reinterpret_cast<uint32_t*>(take(4ull * V * s.nwd));
   }
+  if (mirrors_in_smem) {
+    // mission -> vehicle (both orders), the pool and the unsettled-row counts
+    // in shared memory too; mv / mvp are written through (the sweep and the
+    // helpers read them), the rest is written back at the end
+    s.mv = reinterpret_cast<int32_t*>(take(4ull * s.M));
+    s.mvp = reinterpret_cast<int32_t*>(take(4ull * s.M));
+    s.pkind = reinterpret_cast<int32_t*>(take(4ull * s.pool_cap));
+    s.pidx = reinterpret_cast<int32_t*>(take(4ull * s.pool_cap));
+    s.rcnt = reinterpret_cast<int32_t*>(take(4ull * B));
+    sm.gmv = g.mv;
+    sm.gmvp = g.mvp;
+    copy_words<NT>(reinterpret_cast<uint32_t*>(s.mv), reinterpret_cast<const uint32_t*>(g.mv), s.M);
+    for (int k = threadIdx.x; k < s.pool_cap; k += NT) {
+      s.pkind[k] = g.pkind[k];
+      s.pidx[k] = g.pidx[k];
+    }
+    for (int b = threadIdx.x; b < B; b += NT) s.rcnt[b] = g.rcnt[b];
+  }
   if (threadIdx.x == 0) {
     sh.c = *s.ctr;
     sh.jexp_max = LLONG_MIN;
@@ -1882,6 +1910,9 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       // batch of them in flight per thread before any store
       copy_words<NT>(s.imp, g.imp, (long long)V * s.nwd);
       copy_words<NT>(s.mem, g.mem, (long long)V * s.nwd);
+      if (mirrors_in_smem)
+        copy_words<NT>(reinterpret_cast<uint32_t*>(s.mvp), reinterpret_cast<const uint32_t*>(g.mvp),
+                       s.M);
       __syncthreads();
     }
     {
@@ -1999,6 +2030,13 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     }
     for (int b = threadIdx.x; b < B; b += NT) g.bveh[b] = s.bveh[b];
   }
+  if (mirrors_in_smem) {
+    for (int k = threadIdx.x; k < s.pool_cap; k += NT) {
+      g.pkind[k] = s.pkind[k];
+      g.pidx[k] = s.pidx[k];
+    }
+    for (int b = threadIdx.x; b < B; b += NT) g.rcnt[b] = s.rcnt[b];
+  }
   if (threadIdx.x == 0) *g.ctr = sh.c;
   if (helpers > 0) {
     __syncthreads();
@@ -2083,14 +2121,20 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   const size_t core = pass_smem_core(V, NT);
   const size_t state = pass_smem_state(V, B, K);
   const size_t bits = 2 * align16(4ull * V * ((M + 31) / 32));
-  const size_t limit = 200 * 1024;
+  const size_t limit = 220 * 1024;
   // 256-thread blocks run two per SM: the bitsets only join while two fit
   const size_t bits_limit = NT == 256 ? 100 * 1024 : limit;
   if (core > limit) return cudaErrorInvalidConfiguration;
   const int in_smem = core + state <= limit ? 1 : 0;
   int bits_smem = in_smem && core + state + bits <= bits_limit ? 1 : 0;
   if (const char* e = std::getenv("FLEETPLACE_BITS_SMEM")) bits_smem = bits_smem && std::atoi(e) != 0;
-  const size_t smem = core + (in_smem ? state : 0) + (bits_smem ? bits : 0);
+  // the mission mirrors join when the bitsets did (pool bound: B + 2V + 1)
+  const size_t mirrors = 2 * align16(4ull * M) + 2 * align16(4ull * (B + 2 * V + 1)) + align16(4ull * B);
+  int mirrors_smem = bits_smem && core + state + bits + mirrors <= bits_limit ? 1 : 0;
+  if (const char* e = std::getenv("FLEETPLACE_MIRRORS_SMEM"))
+    mirrors_smem = mirrors_smem && std::atoi(e) != 0;
+  const size_t smem = core + (in_smem ? state : 0) + (bits_smem ? bits : 0) +
+                      (mirrors_smem ? mirrors : 0);
   cudaFuncSetAttribute(pass_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // helper blocks: one scenario, one pass per launch, bitsets in global
   // memory, and every block co-resident (cooperative launch)
@@ -2107,13 +2151,13 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   if (helpers > 0) {
     int ip = inkernel ? 1 : 0, t = tabu ? 1 : 0, d = debug ? 1 : 0;
     void* args[] = {&d_scs, &d_active, &d_perms, &kpasses, &ip, &max_passes, &t, &tenure, &d,
-                    (void*)&in_smem, (void*)&bits_smem, &helpers, &epoch};
+                    (void*)&in_smem, (void*)&bits_smem, (void*)&mirrors_smem, &helpers, &epoch};
     return cudaLaunchCooperativeKernel((const void*)pass_kernel<NT>, dim3(1 + helpers), dim3(NT),
                                        args, smem, stream);
   }
   pass_kernel<NT><<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
                                                max_passes, tabu, tenure, debug, in_smem,
-                                               bits_smem, 0, epoch);
+                                               bits_smem, mirrors_smem, 0, epoch);
   return cudaGetLastError();
 }
 

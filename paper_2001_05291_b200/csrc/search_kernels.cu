@@ -65,6 +65,7 @@ struct Shared {
   unsigned hdone;                       // helper completions expected so far
   long long red_l[33];
   int red_i[2][33];
+  int red2[2][32][2];                   // row-run minima, double-buffered
   double red_d[3][33];
 };
 
@@ -85,6 +86,7 @@ struct Smem {
   int* jl_lim;         // [V] its live window (positions from the segment start)
   uint8_t* jl_outer;   // [V] its role is Outer
   const int32_t* pb;   // perm_b
+  int* paw;            // [2*NT] window of perm_a (row runs)
   int helpers;         // helper blocks sharing relocations (0 = none)
   unsigned epoch;      // launch number (helper job tags)
   int32_t* gvbase;     // global vbase (helpers read the mover's new base)
@@ -1766,7 +1768,7 @@ size_t pass_smem_core(int V, int NT) {
   const int NW = NT / 32;
   return align16(4ull * V) + align16(V) + align16(V) + 2 * align16(8ull * NW * V) +
          align16(8ull * NW * 32) + align16(8ull * NW * 3) + 3 * align16(4ull * V) + align16(V) +
-         align16(8ull * NT) + 64;
+         align16(8ull * NT) + align16(8ull * NT) + 64;
 }
 size_t pass_smem_state(int V, int B, int K) {
   return align16(8ull * V) * 2 + align16(8ull * K) + align16(K) + align16(4ull * V) * 3 +
@@ -1812,6 +1814,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   sm.jl_lim = reinterpret_cast<int*>(take(4ull * V));
   sm.jl_outer = take(V);
   sm.impc = reinterpret_cast<int*>(take(4ull * V));
+  sm.paw = reinterpret_cast<int*>(take(8ull * NT));
   sm.pb = perms + s.M;
   sm.helpers = helpers;
   sm.epoch = epoch;
@@ -1931,9 +1934,17 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     }
     __syncthreads();
     PH_ADD(sh, 11, ps0);
-      int r = 0;
+    int r = 0;
+    int pw = INT_MIN;  // perm_a window in shared memory: sm.paw[k] = pa[pw + k], k < 2*NT
+    int par = 0;       // parity of the double-buffered row-run reduction
+    long long T = sh.c.tick;  // every thread tracks the tick through row runs
     while (r < M && !sh.c.error) {
       const long long b0 = ph_now();
+      if (r < pw || r + NT > pw + 2 * NT) {
+        pw = r;
+        for (int k = threadIdx.x; k < 2 * NT; k += NT) sm.paw[k] = pw + k < M ? pa[pw + k] : 0;
+        __syncthreads();
+      }
       // Classify the next NT rows at the current tick T (thread d: row r+d):
       //  S: no move from its outer index can improve any mission (imp rows
       //     empty, relocation classes all POS) -- tick independent;
@@ -1943,11 +1954,10 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       // A row with S and F <= T is eventless at any later tick: all M pairs
       // are evaluated (M ticks, 3M evaluations). A row with T_d < E is
       // outer-blocked at its first pair (1 tick).
-      const long long T = sh.c.tick;
       const int d = threadIdx.x, row = r + d;
       int first_nontrivial = INT_MAX, first_nonouter = INT_MAX;
       if (row < M) {
-        const int i = pa[row];
+        const int i = sm.paw[row - pw];
         const int g0 = s.mv[i];
         bool st = sm.impc[g0] == 0;
         long long F = tabu ? max(s.exp_reas[g0], sh.jexp_max) : LLONG_MIN;
@@ -1976,7 +1986,24 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
         if (!(st && F <= T)) first_nontrivial = d;
         if (!(T + d < E)) first_nonouter = d;
       }
-      const int A = block_min<NT>(first_nontrivial, sh);
+      // both block minima with one barrier (double-buffered by parity; every
+      // warp combines the per-warp values itself)
+      {
+        const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+        const int a = __reduce_min_sync(FULL, first_nontrivial);
+        const int o = __reduce_min_sync(FULL, first_nonouter);
+        if (l == 0) {
+          sh.red2[par][w][0] = a;
+          sh.red2[par][w][1] = o;
+        }
+        __syncthreads();
+        first_nontrivial = l < NT / 32 ? sh.red2[par][l][0] : INT_MAX;
+        first_nonouter = l < NT / 32 ? sh.red2[par][l][1] : INT_MAX;
+        first_nontrivial = __reduce_min_sync(FULL, first_nontrivial);
+        first_nonouter = __reduce_min_sync(FULL, first_nonouter);
+        par ^= 1;
+      }
+      const int A = first_nontrivial;
       if (A > 0) {
         // a run of eventless rows
         const int n = A == INT_MAX ? min(NT, M - r) : A;
@@ -1985,27 +2012,28 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
           if (tabu) sh.c.tick += (long long)M * n;
           sh.c.counts[4] += (unsigned long long)n;
         }
-        __syncthreads();
+        if (tabu) T += (long long)M * n;
         r += n;
         PH_ADD(sh, 0, b0);
         continue;
       }
       if (tabu) {
         // a run of rows outer-blocked at their first pair (one tick each)
-        const int found = block_min<NT>(first_nonouter, sh);
-        const int nskip = found == INT_MAX ? min(NT, M - r) : found;
+        const int nskip = first_nonouter == INT_MAX ? min(NT, M - r) : first_nonouter;
         if (threadIdx.x == 0 && nskip > 0) {
           sh.c.tick += nskip;
           sh.c.skips_outer += (unsigned long long)nskip;
           sh.c.pass_skipped = 1;
         }
-        __syncthreads();
+        T += nskip;
         r += nskip;
         PH_ADD(sh, 0, b0);
         if (nskip > 0) continue;
       }
-      run_row<NT>(s, sh, sm, pa[r], tabu, tenure, debug);
+      __syncthreads();  // thread 0's counter updates before run_row reads them
+      run_row<NT>(s, sh, sm, sm.paw[r - pw], tabu, tenure, debug);
       __syncthreads();
+      T = sh.c.tick;
       r += 1;
     }
     // end of pass: run_search's keep_going / max_passes (search.cpp:420-428)

@@ -363,6 +363,16 @@ class DistanceTable:
         t._host = flat.reshape(B, M).T
         return t
 
+    def upload(self, cost: np.ndarray) -> None:
+        """Replaces the resident table with a host (M, B) table, reusing this
+        table's device context (its stream, workspace and buffers)."""
+        cost = np.asarray(cost, np.float64)
+        M, B = cost.shape
+        flat = np.ascontiguousarray(cost.T).reshape(-1)
+        _check(lib().fp_table_upload(self._ctx.p, M, B, A.ptr(flat, C.c_double)))
+        self.n_missions, self.n_bases = M, B
+        self._host = flat.reshape(B, M).T
+
 
 def build_distance_table(inst: Instance, radius_km: float = kEarthRadiusKm,
                          device: int = 0) -> DistanceTable:

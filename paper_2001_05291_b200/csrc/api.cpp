@@ -310,55 +310,65 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 struct Layout {
   size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
       invb, exp_take, exp_reas, exp_rel, role_rel, rA, rE, rU, rcnt, imp, mem, scratch, hc, hdelta,
-      hsum, habs, hec, hrs, hue, ctr, cost, total;
+      hsum, habs, hec, hrs, hue, impT, cost, totalA, totalB;
 };
 
+// Per-scenario layout in two regions: A holds what the host initialises
+// (inputs, tabu stamps, zeroed control blocks; staged with one copy), B the
+// device-built working arrays (never staged).
 Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   Layout L{};
-  size_t o = 0;
-  auto put = [&](size_t bytes) {
-    const size_t at = o;
-    o = align_up(o + bytes);
+  size_t a = 0, b = 0;
+  auto putA = [&](size_t bytes) {
+    const size_t at = a;
+    a = align_up(a + bytes);
     return at;
   };
-  L.ro = put(M);
-  L.vfixed = put(V);
-  L.bheli = put(B);
-  L.vrk = put(4ull * V);
-  L.brk = put(4ull * B);
-  L.mv = put(4ull * M);
-  L.mc = put(8ull * M);
-  L.vbase = put(4ull * V);
-  L.vcount = put(4ull * V);
-  L.bveh = put(4ull * B);
-  L.pkind = put(4ull * cap);
-  L.pidx = put(4ull * cap);
-  L.mvp = put(4ull * M);
-  L.mcp = put(8ull * M);
-  L.rop = put(M);
-  L.invb = put(4ull * M);
-  L.exp_take = put(8ull * V);
-  L.exp_reas = put(8ull * V);
-  L.exp_rel = put(8ull * K);
-  L.role_rel = put(K);
-  L.rA = put(8ull * B * V);
-  L.rE = put(8ull * B * V);
-  L.rU = put(8ull * B * V);
-  L.rcnt = put(4ull * B);
-  const size_t nwd = ((size_t)M + 31) / 32;
-  L.imp = put(4ull * V * nwd);
-  L.mem = put(4ull * V * nwd);
-  L.scratch = put(4ull * M + 4);
-  L.hc = put(sizeof(fpk::HelperCtl));
-  L.hdelta = put(4ull * V);
-  L.hsum = put(8ull * V);
-  L.habs = put(8ull * V);
+  auto putB = [&](size_t bytes) {
+    const size_t at = b;
+    b = align_up(b + bytes);
+    return at;
+  };
+  L.ro = putA(M);
+  L.vfixed = putA(V);
+  L.bheli = putA(B);
+  L.vrk = putA(4ull * V);
+  L.brk = putA(4ull * B);
+  L.mv = putA(4ull * M);
+  L.vbase = putA(4ull * V);
+  L.vcount = putA(4ull * V);
+  L.bveh = putA(4ull * B);
+  L.pkind = putA(4ull * cap);
+  L.pidx = putA(4ull * cap);
+  L.exp_take = putA(8ull * V);
+  L.exp_reas = putA(8ull * V);
+  L.exp_rel = putA(8ull * K);
+  L.role_rel = putA(K);
+  L.hc = putA(sizeof(fpk::HelperCtl));
+  L.hdelta = putA(4ull * V);
+  L.hsum = putA(8ull * V);
+  L.habs = putA(8ull * V);
   const size_t nsub = ((size_t)M + fpk::kChainSub - 1) / fpk::kChainSub + 1;
-  L.hec = put(4ull * nsub);
-  L.hrs = put(8ull * nsub);
-  L.hue = put(4ull * nsub);
-  L.cost = own_cost ? put(8ull * M * B + 16) : 0;
-  L.total = o;
+  L.hec = putA(4ull * nsub);
+  L.cost = own_cost ? putA(8ull * M * B + 16) : 0;
+  L.mc = putB(8ull * M);
+  L.mvp = putB(4ull * M);
+  L.mcp = putB(8ull * M);
+  L.rop = putB(M);
+  L.invb = putB(4ull * M);
+  L.rA = putB(8ull * B * V);
+  L.rE = putB(8ull * B * V);
+  L.rU = putB(8ull * B * V);
+  L.rcnt = putB(4ull * B);
+  const size_t nwd = ((size_t)M + 31) / 32;
+  L.imp = putB(4ull * V * nwd);
+  L.mem = putB(4ull * V * nwd);
+  L.scratch = putB(4ull * M + 4);
+  L.hrs = putB(8ull * nsub);
+  L.hue = putB(4ull * nsub);
+  L.impT = putB(4ull * M * ((V + 31) / 32) + 16);
+  L.totalA = a;
+  L.totalB = b;
   return L;
 }
 
@@ -402,9 +412,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   for (int s = 0; s < n; ++s) run.hs.push_back(prepare(&insts[s], &starts[s]));
 
   // ---- arena
-  size_t total = 0;
+  size_t totalA = 0, totalB = 0;
   run.lay.resize(n);
-  std::vector<size_t> base(n);
+  std::vector<size_t> baseA(n), baseB(n);
   int maxV = 0, maxB = 0, maxK = 0;
   for (int s = 0; s < n; ++s) {
     const HostScenario& h = run.hs[s];
@@ -413,8 +423,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     maxB = std::max(maxB, B);
     maxK = std::max(maxK, h.K);
     run.lay[s] = layout(M, B, V, h.K, h.psize + V + 1, dev_tables[s] == nullptr);
-    base[s] = total;
-    total += run.lay[s].total;
+    baseA[s] = totalA;
+    totalA += run.lay[s].totalA;
+    baseB[s] = totalB;
+    totalB += run.lay[s].totalB;
   }
   tr.mark("prepared");
   // Small scenarios run many passes per launch, each block rebuilding its
@@ -443,7 +455,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     tbase[s] = tt;
     tt += (size_t)M * insts[s].n_bases;
   }
-  const size_t o_ctr = align_up(total), o_scs = align_up(o_ctr + sizeof(fpk::Counters) * n),
+  const size_t o_B = align_up(totalA), o_ctr = align_up(o_B + totalB), o_scs = align_up(o_ctr + sizeof(fpk::Counters) * n),
                o_act = align_up(o_scs + sizeof(fpk::Scenario) * n),
                o_perm = align_up(o_act + 4ull * n), o_costT = align_up(o_perm + 4ull * chunk_ints);
   auto ws_get = [&](size_t bytes) -> bool {
@@ -480,16 +492,18 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     // test hook: every accept decision through the exact sums (same results)
     if (const char* e = std::getenv("FLEETPLACE_FORCE_EXACT")) ctrs[s].force_exact = std::atoi(e);
     if (const char* e = std::getenv("FLEETPLACE_HELPED_CHAINS")) ctrs[s].chain_mode = std::atoi(e) == 0;
+    if (const char* e = std::getenv("FLEETPLACE_CHECK_IMPT")) ctrs[s].check_impt = std::atoi(e);
   }
-  std::vector<unsigned char> stage(total, 0);
+  std::vector<unsigned char> stage(totalA, 0);
   run.scs.resize(n);
   for (int s = 0; s < n; ++s) {
     const HostScenario& h = run.hs[s];
     const Layout& L = run.lay[s];
     const fp_instance* in = &insts[s];
     const int V = in->n_vehicles, B = in->n_bases;
-    unsigned char* hb = stage.data() + base[s];
-    unsigned char* db = d0 + base[s];
+    unsigned char* hb = stage.data() + baseA[s];
+    unsigned char* db = d0 + baseA[s];              // region A (staged)
+    unsigned char* dw = d0 + o_B + baseB[s];        // region B (device-built)
     if (M) std::memcpy(hb + L.ro, in->rotary_only, M);
     if (V) std::memcpy(hb + L.vfixed, h.vfixed.data(), V);
     if (B) std::memcpy(hb + L.bheli, h.bheli.data(), B);
@@ -512,34 +526,36 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.vrk = reinterpret_cast<const int32_t*>(db + L.vrk);
     S.brk = reinterpret_cast<const int32_t*>(db + L.brk);
     S.mv = reinterpret_cast<int32_t*>(db + L.mv);
-    S.mc = reinterpret_cast<double*>(db + L.mc);
+    S.mc = reinterpret_cast<double*>(dw + L.mc);
     S.vbase = reinterpret_cast<int32_t*>(db + L.vbase);
     S.vcount = reinterpret_cast<int32_t*>(db + L.vcount);
     S.bveh = reinterpret_cast<int32_t*>(db + L.bveh);
     S.pkind = reinterpret_cast<int32_t*>(db + L.pkind);
     S.pidx = reinterpret_cast<int32_t*>(db + L.pidx);
-    S.mvp = reinterpret_cast<int32_t*>(db + L.mvp);
-    S.mcp = reinterpret_cast<double*>(db + L.mcp);
-    S.rop = db + L.rop;
-    S.invb = reinterpret_cast<int32_t*>(db + L.invb);
+    S.mvp = reinterpret_cast<int32_t*>(dw + L.mvp);
+    S.mcp = reinterpret_cast<double*>(dw + L.mcp);
+    S.rop = dw + L.rop;
+    S.invb = reinterpret_cast<int32_t*>(dw + L.invb);
     S.exp_take = reinterpret_cast<long long*>(db + L.exp_take);
     S.exp_reas = reinterpret_cast<long long*>(db + L.exp_reas);
     S.exp_rel = reinterpret_cast<long long*>(db + L.exp_rel);
     S.role_rel = db + L.role_rel;
-    S.rA = reinterpret_cast<double*>(db + L.rA);
-    S.rE = reinterpret_cast<double*>(db + L.rE);
-    S.rU = reinterpret_cast<double*>(db + L.rU);
-    S.rcnt = reinterpret_cast<int32_t*>(db + L.rcnt);
-    S.imp = reinterpret_cast<uint32_t*>(db + L.imp);
-    S.mem = reinterpret_cast<uint32_t*>(db + L.mem);
-    S.scratch = reinterpret_cast<int32_t*>(db + L.scratch);
+    S.rA = reinterpret_cast<double*>(dw + L.rA);
+    S.rE = reinterpret_cast<double*>(dw + L.rE);
+    S.rU = reinterpret_cast<double*>(dw + L.rU);
+    S.rcnt = reinterpret_cast<int32_t*>(dw + L.rcnt);
+    S.imp = reinterpret_cast<uint32_t*>(dw + L.imp);
+    S.mem = reinterpret_cast<uint32_t*>(dw + L.mem);
+    S.scratch = reinterpret_cast<int32_t*>(dw + L.scratch);
     S.hc = reinterpret_cast<fpk::HelperCtl*>(db + L.hc);
     S.hdelta = reinterpret_cast<int32_t*>(db + L.hdelta);
     S.hsum = reinterpret_cast<double*>(db + L.hsum);
     S.habs = reinterpret_cast<double*>(db + L.habs);
     S.hec = reinterpret_cast<int32_t*>(db + L.hec);
-    S.hrs = reinterpret_cast<long long*>(db + L.hrs);
-    S.hue = reinterpret_cast<int32_t*>(db + L.hue);
+    S.hrs = reinterpret_cast<long long*>(dw + L.hrs);
+    S.hue = reinterpret_cast<int32_t*>(dw + L.hue);
+    S.impT = reinterpret_cast<uint32_t*>(dw + L.impT);
+    S.nvw = (V + 31) / 32;
     {
       const size_t nsub = ((size_t)M + fpk::kChainSub - 1) / fpk::kChainSub + 1;
       int32_t* he = reinterpret_cast<int32_t*>(hb + L.hec);
@@ -557,7 +573,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   check(cudaEventCreate(&ev0), "event");
   check(cudaEventCreate(&ev1), "event");
   check(cudaEventRecord(ev0, st), "event");
-  h2d(d0, stage.data(), total, st);
+  h2d(d0, stage.data(), totalA, st);
   h2d(d_scs, run.scs.data(), n, st);
   std::vector<int32_t> active(n, 1);
   h2d(d_ctr, ctrs.data(), n, st);
@@ -568,12 +584,13 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     ctx->perm_cap = chunk_ints;
   }
   double init_ms = 0.0, sweep_ms = 0.0;
-  {
-    EvTimer ti(st);
-    check(fpk::launch_init(d_scs, n, M, maxB, maxV, cost_t, st), "init_kernel");
-    init_ms = ti.stop_ms();
-  }
-  ctx->launches += 1 + (maxB > 0 ? 1 : 0) + (cost_t && M > 0 && maxB > 0 ? 1 : 0);
+  cudaEvent_t ei0, ei1;
+  check(cudaEventCreate(&ei0), "event");
+  check(cudaEventCreate(&ei1), "event");
+  check(cudaEventRecord(ei0, st), "event");
+  check(fpk::launch_init(d_scs, n, M, maxB, maxV, cost_t, st), "init_kernel");
+  check(cudaEventRecord(ei1, st), "event");
+  ctx->launches += 1 + (M > 0 ? 1 : 0) + (maxB > 0 ? 1 : 0) + (cost_t && M > 0 && maxB > 0 ? 1 : 0);
   tr.mark("allocated, staged, init launched");
   std::vector<cudaEvent_t> sweep_ev;  // (start, end) pairs around grid-wide sweeps
   PermStream rng(cfg->seed);
@@ -584,7 +601,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     }
   };
   int buf = 0;
-  gen_chunk(ctx->h_perm[buf]);
+  gen_chunk(ctx->h_perm[buf]);  // overlaps the init kernels
   tr.mark("first permutation chunk");
   int threads = n == 1 ? 512 : 256;
   if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
@@ -655,6 +672,13 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   }
   check(cudaStreamSynchronize(st), "final sync");
   tr.mark("final sync");
+  {
+    float ims = 0.f;
+    cudaEventElapsedTime(&ims, ei0, ei1);
+    init_ms = ims;
+    cudaEventDestroy(ei0);
+    cudaEventDestroy(ei1);
+  }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
   cudaEventDestroy(ev0);

@@ -31,6 +31,7 @@ struct Counters {
   int force_exact;                // test hook: 1 = every total comparison through the exact
                                   // chains, 2 = every unsettled relocation delta exactly
   int chain_mode;                 // 0 = helper-assisted exact chains when possible, 1 = never
+  int check_impt;                 // test hook: verify impT against the table every pass
   double total_up;                // rigorous upper bound of the current total
   double final_total;             // exact fixed-order total (written at the end)
   double total_exact;             // exact fixed-order total of the state ...
@@ -114,6 +115,11 @@ struct Scenario {
   //  mem[v]: the position's mission is served by vehicle v
   uint32_t* imp;             // [V*NWD]
   uint32_t* mem;             // [V*NWD]
+  // the same improvement bits in natural mission order, one row of NVW words
+  // per mission (bit g of row j: moving mission j to vehicle g lowers its
+  // cost); maintained on every move, so the per-pass rebuild of imp is a
+  // gather of M rows instead of V*M table entries
+  uint32_t* impT;            // [M*NVW]
   int32_t* scratch;          // [M] per-scenario scratch (relocation position lists)
   HelperCtl* hc;             // helper work sharing (zeroed at search start)
   int32_t* hdelta;           // [V] helpers' imp-row popcount deltas
@@ -125,7 +131,7 @@ struct Scenario {
   int32_t* hue;              // [..] helpers: the binade hrs is for, kNoBinade when the
                              //   chunk holds a rounding tie / a huge term / no prediction
   Counters* ctr;
-  int32_t M, B, V, K, pool_cap, nwd;
+  int32_t M, B, V, K, pool_cap, nwd, nvw;
 };
 
 }  // namespace fpk

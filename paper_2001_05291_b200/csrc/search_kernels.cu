@@ -620,11 +620,19 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
                                         int ng) {
   const int wd = q >> 5;
   const uint32_t bit = 1u << (q & 31);
-  for (int g = threadIdx.x; g < s.V; g += NT) {
-    uint32_t* wp = s.imp + (long long)g * s.nwd + wd;
-    const bool was = (*wp & bit) != 0u, now = imp_bit(s, g, q, j);
-    put_bit(wp, bit, now);
-    sm.impc[g] += (int)now - (int)was;
+  for (int g0 = 0; g0 < s.V; g0 += NT) {
+    const int g = g0 + threadIdx.x;
+    bool now = false;
+    if (g < s.V) {
+      uint32_t* wp = s.imp + (long long)g * s.nwd + wd;
+      const bool was = (*wp & bit) != 0u;
+      now = imp_bit(s, g, q, j);
+      put_bit(wp, bit, now);
+      sm.impc[g] += (int)now - (int)was;
+    }
+    // the mission's natural-order row
+    const unsigned row = __ballot_sync(FULL, now);
+    if ((threadIdx.x & 31) == 0 && g < s.V) s.impT[(long long)j * s.nvw + (g >> 5)] = row;
   }
   if (threadIdx.x == 0 && loser != gain) {
     s.mem[(long long)loser * s.nwd + wd] &= ~bit;
@@ -661,6 +669,19 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
       b[u] = false;
       if (wd0 + u < nwd && q < M)
         b[u] = s.mvp[q] != x && compat_vm(fx, s.rop[q]) && colx[sm.pb[q]] < s.mcp[q];
+    }
+    // bit x of the natural-order rows, where it changed
+    const uint32_t xb = 1u << (x & 31);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = (wd0 + u) * 32 + l;
+      if (wd0 + u < nwd && q < M) {
+        const bool was = (s.imp[(long long)x * nwd + wd0 + u] >> l) & 1u;
+        if (b[u] != was) {
+          uint32_t* tw = s.impT + (long long)sm.pb[q] * s.nvw + (x >> 5);
+          if (b[u]) atomicOr(tw, xb); else atomicAnd(tw, ~xb);
+        }
+      }
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -707,6 +728,11 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
+        const unsigned row = __ballot_sync(FULL, on[u]);
+        if (l == 0 && g0 + u * 32 < V) s.impT[(long long)j * s.nvw + (g0 >> 5) + u] = row;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
         const int g = g0 + u * 32 + l;
         if (g >= V || g == x) continue;
         uint32_t* wp = s.imp + (long long)g * nwd + wd;
@@ -725,13 +751,21 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
         mx &= mx - 1;
         const int q = wd * 32 + bn;
         const int j = sm.pb[q];
+        uint32_t row = 0;
         for (int g = 0; g < V; ++g) {
-          if (g == x) continue;
-          uint32_t* wp = s.imp + (long long)g * nwd + wd;
-          const bool was = (*wp & (1u << bn)) != 0u;
-          const bool now = compat_vm(s.vfixed[g], s.rop[q]) && cost_mb(s, j, s.vbase[g]) < s.mcp[q];
-          put_bit(wp, 1u << bn, now);
-          if (now != was) atomicAdd(&sm.impc[g], now ? 1 : -1);
+          bool now = false;
+          if (g != x) {
+            uint32_t* wp = s.imp + (long long)g * nwd + wd;
+            const bool was = (*wp & (1u << bn)) != 0u;
+            now = compat_vm(s.vfixed[g], s.rop[q]) && cost_mb(s, j, s.vbase[g]) < s.mcp[q];
+            put_bit(wp, 1u << bn, now);
+            if (now != was) atomicAdd(&sm.impc[g], now ? 1 : -1);
+          }
+          row |= (uint32_t)now << (g & 31);
+          if ((g & 31) == 31 || g == V - 1) {
+            s.impT[(long long)j * s.nvw + (g >> 5)] = row;
+            row = 0;
+          }
         }
       }
     }
@@ -1038,6 +1072,11 @@ __device__ void helper_relocate(const Scenario& s, const Smem& sm, const int32_t
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
+          const unsigned row = __ballot_sync(FULL, on[u]);
+          if (l == 0 && g0 + u * 32 < V) s.impT[(long long)mm * s.nvw + (g0 >> 5) + u] = row;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
           const int g = g0 + u * 32 + l;
           if (g >= V || g == x) continue;
           uint32_t* wp = s.imp + (long long)g * nwd + wd;
@@ -1063,6 +1102,18 @@ __device__ void helper_relocate(const Scenario& s, const Smem& sm, const int32_t
       b[u] = false;
       if (wd0 + u < w1 && q < M)
         b[u] = s.mvp[q] != x && compat_vm(fx, s.rop[q]) && colt[pb[q]] < s.mcp[q];
+    }
+    const uint32_t xb = 1u << (x & 31);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = (wd0 + u) * 32 + l;
+      if (wd0 + u < w1 && q < M) {
+        const bool was = (s.imp[(long long)x * nwd + wd0 + u] >> l) & 1u;
+        if (b[u] != was) {
+          uint32_t* tw = s.impT + (long long)pb[q] * s.nvw + (x >> 5);
+          if (b[u]) atomicOr(tw, xb); else atomicAnd(tw, ~xb);
+        }
+      }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -1685,40 +1736,29 @@ __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) &
 }  // namespace
 
 // Per pass: the perm_b-ordered mirrors and the imp/mem bitsets, warp per
-// word, lane per position (the neighbourhood sweep: every occupied vehicle's
-// base column is gathered once, V*M table reads). Four vehicles' gathers are
-// kept in flight per lane.
+// word, lane per position: each lane gathers its mission's natural-order
+// improvement row (NVW words) and the warp transposes it into the V
+// position-order words with ballots; mem from the mirrored vehicles.
 __device__ void prep_words(const Scenario& s, const int32_t* __restrict__ pb, int wd0, int wstride) {
   const int l = threadIdx.x & 31;
   for (int wd = wd0; wd < s.nwd; wd += wstride) {
     const int q = wd * 32 + l;
     const bool valid = q < s.M;
     int j = 0, v = -1;
-    double mcq = 0.0;
-    bool ro = false;
     if (valid) {
       j = pb[q];
       v = s.mv[j];
-      mcq = s.mc[j];
-      ro = s.ro[j];
       s.mvp[q] = v;
-      s.mcp[q] = mcq;
-      s.rop[q] = ro;
+      s.mcp[q] = s.mc[j];
+      s.rop[q] = s.ro[j];
       s.invb[j] = q;
     }
-    for (int g0 = 0; g0 < s.V; g0 += 4) {
-      double c[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int g = g0 + u;
-        c[u] = (valid && g < s.V) ? s.cost[(long long)s.vbase[g] * s.M + j] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int g = g0 + u;
-        if (g >= s.V) break;
-        const bool b = valid && v != g && compat_vm(s.vfixed[g], ro) && c[u] < mcq;
-        const unsigned m = __ballot_sync(FULL, b);
+    for (int vw = 0; vw < s.nvw; ++vw) {
+      const uint32_t row = valid ? s.impT[(long long)j * s.nvw + vw] : 0u;
+      const int gend = min(32, s.V - vw * 32);
+      for (int b = 0; b < gend; ++b) {
+        const int g = vw * 32 + b;
+        const unsigned m = __ballot_sync(FULL, (row >> b) & 1u);
         const unsigned mm = __ballot_sync(FULL, v == g);
         if (l == 0) {
           s.imp[(long long)g * s.nwd + wd] = m;
@@ -1727,6 +1767,31 @@ __device__ void prep_words(const Scenario& s, const int32_t* __restrict__ pb, in
       }
     }
   }
+}
+
+// Test hook (Counters::check_impt): every natural-order improvement row
+// against the table. Block-wide; sets error 6 on a mismatch.
+template <int NT>
+__device__ void verify_impt(const Scenario& s, Shared& sh) {
+  if (threadIdx.x == 0) sh.tmp = 0;
+  __syncthreads();
+  int bad = 0;
+  for (int j = threadIdx.x; j < s.M; j += NT) {
+    for (int vw = 0; vw < s.nvw; ++vw) {
+      uint32_t row = 0;
+      for (int b = 0; b < 32 && vw * 32 + b < s.V; ++b) {
+        const int g = vw * 32 + b;
+        const bool on = s.mv[j] != g && compat_vm(s.vfixed[g], s.ro[j]) &&
+                        cost_at(s, s.vbase[g], j) < s.mc[j];
+        row |= (uint32_t)on << b;
+      }
+      bad |= row != s.impT[(long long)j * s.nvw + vw];
+    }
+  }
+  if (bad) atomicOr(&sh.tmp, 1);
+  __syncthreads();
+  if (threadIdx.x == 0 && sh.tmp) sh.c.error = 6;
+  __syncthreads();
 }
 
 // grid = (words, scenarios): the sweep for large scenarios, one launch per pass.
@@ -1905,6 +1970,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     const int32_t* pa = perms + 2ll * kp * M;
     sm.pb = pa + M;
     const long long ps0 = ph_now();
+    if (sh.c.check_impt) verify_impt<NT>(s, sh);
     if (inkernel_prep) {
       prep_words(s, sm.pb, threadIdx.x >> 5, NW);
       __syncthreads();
@@ -2110,6 +2176,29 @@ __global__ void __launch_bounds__(512) init_kernel(Scenario* scs) {
   }
 }
 
+// The natural-order improvement rows at the search start, thread per
+// mission: every occupied vehicle's base column streamed once, coalesced
+// (V*M table reads; the neighbourhood evaluation of every reassignment).
+__global__ void __launch_bounds__(256) impt_init_kernel(Scenario* scs) {
+  const Scenario s = scs[blockIdx.y];
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= s.M) return;
+  const int v = s.mv[j];
+  const double mcj = s.mc[j];
+  const bool ro = s.ro[j];
+  for (int vw = 0; vw < s.nvw; ++vw) {
+    uint32_t row = 0;
+    const int gend = min(32, s.V - vw * 32);
+#pragma unroll 8
+    for (int b = 0; b < gend; ++b) {
+      const int g = vw * 32 + b;
+      const bool on = v != g && compat_vm(s.vfixed[g], ro) && cost_at(s, s.vbase[g], j) < mcj;
+      row |= (uint32_t)on << b;
+    }
+    s.impT[(long long)j * s.nvw + vw] = row;
+  }
+}
+
 // The relocation-delta table's initial rows, one block per empty base (the
 // sweep over every empty base's column: 8*M bytes each, streamed coalesced).
 __global__ void __launch_bounds__(256) table_rows_kernel(Scenario* scs) {
@@ -2222,6 +2311,7 @@ cudaError_t launch_init(Scenario* d_scs, int n_scn, int M, int maxB, int maxV, b
   if (cost_t && M > 0 && maxB > 0)
     transpose_kernel<<<dim3((M + 31) / 32, (maxB + 31) / 32, n_scn), 256, 0, stream>>>(d_scs);
   init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
+  if (M > 0) impt_init_kernel<<<dim3((M + 255) / 256, n_scn), 256, 0, stream>>>(d_scs);
   const size_t smem = sizeof(double) * (16ull * maxV + 8 * 32);
   cudaFuncSetAttribute(table_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (maxB > 0) table_rows_kernel<<<dim3(maxB, n_scn), 256, smem, stream>>>(d_scs);

@@ -158,3 +158,22 @@ def test_forced_exact_totals_with_helper_chains(monkeypatch):
     monkeypatch.setenv("FLEETPLACE_FORCE_EXACT", "1")
     inst = ref_survey_instance(300, 40000, 60, seed=3)
     _check_search(inst, 1, seeds=[7], max_passes=1)
+
+
+@pytest.mark.parametrize("case", ["c1", "c2_sweep", "c2_forced_helpers", "helpers_40k"])
+def test_natural_order_rows_stay_exact(monkeypatch, case):
+    """Test hook FLEETPLACE_CHECK_IMPT: at every pass start the incrementally
+    maintained natural-order improvement rows (impT, the source of the
+    per-pass bitset rebuild) are compared with a fresh evaluation against the
+    table; a mismatch fails the search. Also checks the trajectory."""
+    monkeypatch.setenv("FLEETPLACE_CHECK_IMPT", "1")
+    if case == "c1":
+        _check_search(ref_survey_instance(50, 200, 10), 1, seeds=[1, 7])
+    elif case == "c2_sweep":
+        _check_search(ref_survey_instance(500, 10000, 40, seed=1), 1, seeds=[7], max_passes=4)
+    elif case == "c2_forced_helpers":
+        monkeypatch.setenv("FLEETPLACE_HELPERS", "-1")
+        monkeypatch.setenv("FLEETPLACE_BITS_SMEM", "0")
+        _check_search(ref_survey_instance(500, 10000, 40, seed=1), 1, seeds=[7], max_passes=4)
+    else:
+        _check_search(ref_survey_instance(300, 40000, 60, seed=3), 1, seeds=[7], max_passes=3)

@@ -218,13 +218,22 @@ def _kernel_rooflines(inst, t, start_ms, r, peak):
         "table_kernel": {"ms": start_ms["table"], "bytes": 8 * B * M, "bound": "fp64 ALU",
                          "note": "4 sin + 2 asin + 2 sqrt per entry; bytes are the writes"},
         "column_totals_kernel": {"ms": start_ms["totals"], "bytes": 8 * B * M, "bound": "hbm"},
-        "search_init (exact total + relocation-table sweep)": {
-            "ms": r.stats.init_ms, "bytes": 8 * P * M + 12 * M, "bound": "hbm"},
     }
+    tp, ini, imp_rows, rel_rows = r.stats.init_part_ms
+    nvw = (V + 31) // 32
+    out["transpose_table_kernel (row-major table copy, second stream)"] = {
+        "ms": start_ms["copy"] or tp, "bytes": 16 * B * M, "bound": "hbm"}
+    out["init_kernel (costs + exact total, one block)"] = {
+        "ms": ini, "bytes": 8 * M * 2 + 4 * M, "bound": "latency (one block per scenario)"}
+    out["impt_init_kernel (every reassignment scored: improvement rows)"] = {
+        "ms": imp_rows, "bytes": 8 * V * M + 17 * M + 4 * nvw * M, "bound": "hbm"}
+    out["table_rows_kernel (relocation-delta rows of the empty bases)"] = {
+        "ms": rel_rows, "bytes": 8 * P * M + 12 * M, "bound": "hbm"}
     if r.stats.sweep_ms > 0:
-        out["prep_kernel (per-pass bitset sweep, mean)"] = {
+        # gathers of M natural-order rows + mirrors, writes of imp / mem / mirrors
+        out["prep_kernel (per-pass bitset rebuild, mean)"] = {
             "ms": r.stats.sweep_ms / max(r.stats.passes, 1),
-            "bytes": 8 * V * M + 21 * M + 8 * V * nwd, "bound": "hbm (gathered columns)"}
+            "bytes": 4 * nvw * M + 25 * M + 21 * M + 8 * V * nwd, "bound": "hbm (gathered rows)"}
     for k in out.values():
         k["achieved_gbs"] = k["bytes"] / (k["ms"] / 1e3) / 1e9 if k["ms"] > 0 else None
         if k["bound"].startswith("hbm") and k["achieved_gbs"]:
@@ -246,10 +255,13 @@ def extra_workloads(device: int) -> dict:
                                 ("c4_1_pass", (5000, 1000000, 250), 1)):
         inst = F.survey_instance(*shape, seed=1)
         t = F.build_distance_table(inst, device=device)
-        ms = {"table": t._ctx.last_kernel_ms()}
+        ms = {"table": t._ctx.last_kernel_ms(), "copy": t._ctx.last_copy_ms()}
         start = F.rank_bases(inst, t)
         ms["totals"] = t._ctx.last_kernel_ms()
         vb, mv, pk, px = F._state_arrays(start.assignment, F.initial_pool(start, inst), inst)
+        # one search to size the context's workspace, then the measured one
+        F.search_arrays(inst, t, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=0),
+                        vb, mv, pk, px)
         r = F.search_arrays(inst, t, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu,
                                                     max_passes=passes), vb, mv, pk, px)
         out[name] = {

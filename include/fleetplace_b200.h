@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define FP_ABI_VERSION 2
+#define FP_ABI_VERSION 3
 
 typedef enum fp_status {
   FP_OK = 0,
@@ -134,8 +134,11 @@ typedef struct fp_search_result {
                                     table sweep (CUDA events) */
   double sweep_ms;               /* per-pass bitset sweeps (grid-wide mode) */
   uint64_t event_counts[5];      /* scenario 0: scanned rows, scan steps, row
-                                    contexts, relocation prepasses, rows settled
+                                    contexts, table-row rebuilds, rows settled
                                     by the O(1) eventless test */
+  double init_part_ms[4];        /* init_ms split: row-major table copy, costs +
+                                    exact total, improvement rows, relocation
+                                    table rows (CUDA events) */
 } fp_search_result;
 
 /* RankedStart (proj/include/fleetplace/rank.hpp:10-14) in index form. */
@@ -160,6 +163,10 @@ uint64_t fp_ctx_kernel_launches(const fp_ctx* ctx);
 /* CUDA-event time of the main kernel of the last fp_build_distance_table /
  * fp_column_totals / fp_rank_bases call on this context (ms). */
 double fp_ctx_last_kernel_ms(const fp_ctx* ctx);
+/* CUDA-event time of the last row-major copy of the resident table (made on
+ * the context's second stream after fp_build_distance_table /
+ * fp_table_upload; waits for it), or 0 if none was made. */
+double fp_ctx_last_copy_ms(fp_ctx* ctx);
 
 /* ---- instance validation / generation (host) -------------------------- */
 /* validate_instance (proj/src/model.cpp:46-74). */

@@ -49,6 +49,15 @@ struct fp_ctx {
   // device workspace of the searches (grow-only: no allocation per call)
   unsigned char* ws = nullptr;
   size_t ws_cap = 0;
+  // row-major copy of the resident table, made on a second stream as soon
+  // as the table is resident (overlapping ranking), reused by every search
+  double* d_costT = nullptr;
+  size_t costT_cap = 0;   // elements
+  bool costT_valid = false;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t table_ready = nullptr, costT_ready = nullptr;
+  cudaEvent_t copy_t0 = nullptr, copy_t1 = nullptr;  // timing of the copy
+  bool copy_timed = false;
 };
 
 namespace {
@@ -120,6 +129,7 @@ void ensure_table(const fp_ctx* ctx, int M, int B) {
 }
 
 void table_alloc(fp_ctx* ctx, int M, int B) {
+  if (ctx->aux) cudaStreamSynchronize(ctx->aux);  // a pending copy still reads the table
   const size_t need = (size_t)M * (size_t)B;
   if (need > ctx->cost_cap) {
     if (ctx->d_cost) cudaFree(ctx->d_cost);
@@ -131,6 +141,7 @@ void table_alloc(fp_ctx* ctx, int M, int B) {
   }
   ctx->M = M;
   ctx->B = B;
+  ctx->costT_valid = false;
 }
 
 bool valid_point(double lat, double lon) {
@@ -310,7 +321,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 struct Layout {
   size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
       invb, exp_take, exp_reas, exp_rel, role_rel, rA, rE, rU, rcnt, imp, mem, scratch, hc, hdelta,
-      hsum, habs, hec, hrs, hue, impT, cost, totalA, totalB;
+      hsum, habs, hec, hrs, hue, impT, vseg, vcur, vch, cost, totalA, totalB;
 };
 
 // Per-scenario layout in two regions: A holds what the host initialises
@@ -367,6 +378,9 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   L.hrs = putB(8ull * nsub);
   L.hue = putB(4ull * nsub);
   L.impT = putB(4ull * M * ((V + 31) / 32) + 16);
+  L.vseg = putB(4ull * (V + 2));
+  L.vcur = putB(4ull * V + 4);
+  L.vch = putB(12ull * ((size_t)M / fpk::kRowsChunk + V + 1));
   L.totalA = a;
   L.totalB = b;
   return L;
@@ -377,6 +391,43 @@ struct SearchRun {
   std::vector<fpk::Scenario> scs;
   std::vector<Layout> lay;
 };
+
+// Starts the row-major copy of the resident table on the context's second
+// stream (after the work already queued on the main stream). Skipped when
+// the memory is not there; searches then run without it or make their own.
+void start_costT(fp_ctx* ctx) {
+  if (const char* e = std::getenv("FLEETPLACE_COST_T"))
+    if (std::atoi(e) == 0) return;
+  const size_t need = (size_t)std::max(ctx->M, 0) * (size_t)std::max(ctx->B, 0);
+  if (need == 0) return;
+  if (ctx->costT_cap < need) {
+    if (ctx->d_costT) cudaFree(ctx->d_costT);
+    ctx->d_costT = nullptr;
+    ctx->costT_cap = 0;
+    if (cudaMalloc(&ctx->d_costT, sizeof(double) * need) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->d_costT = nullptr;
+      return;
+    }
+    ctx->costT_cap = need;
+  }
+  if (!ctx->aux) check(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking), "stream");
+  if (!ctx->table_ready)
+    check(cudaEventCreateWithFlags(&ctx->table_ready, cudaEventDisableTiming), "event");
+  if (!ctx->costT_ready)
+    check(cudaEventCreateWithFlags(&ctx->costT_ready, cudaEventDisableTiming), "event");
+  if (!ctx->copy_t0) check(cudaEventCreate(&ctx->copy_t0), "event");
+  if (!ctx->copy_t1) check(cudaEventCreate(&ctx->copy_t1), "event");
+  check(cudaEventRecord(ctx->table_ready, ctx->stream), "event");
+  check(cudaStreamWaitEvent(ctx->aux, ctx->table_ready, 0), "wait");
+  check(cudaEventRecord(ctx->copy_t0, ctx->aux), "event");
+  check(fpk::launch_transpose(ctx->d_cost, ctx->M, ctx->B, ctx->d_costT, ctx->aux), "transpose");
+  check(cudaEventRecord(ctx->copy_t1, ctx->aux), "event");
+  check(cudaEventRecord(ctx->costT_ready, ctx->aux), "event");
+  ctx->copy_timed = true;
+  ctx->launches += 1;
+  ctx->costT_valid = true;
+}
 
 // FLEETPLACE_TRACE=1: host-side timestamps of a search on stderr.
 struct Trace {
@@ -449,6 +500,26 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // it is left out when memory is short (FLEETPLACE_COST_T=0 disables it).
   bool cost_t = true;
   if (const char* e = std::getenv("FLEETPLACE_COST_T")) cost_t = std::atoi(e) != 0;
+  // a single search on the context's own table keeps its copy with the
+  // table (made once, reused by every later search on it)
+  const bool ctx_copy = cost_t && n == 1 && ctx->d_cost && dev_tables[0] == ctx->d_cost;
+  if (ctx_copy && ctx->costT_cap < (size_t)M * insts[0].n_bases) {
+    if (ctx->d_costT) {
+      cudaStreamSynchronize(st);
+      if (ctx->aux) cudaStreamSynchronize(ctx->aux);
+      cudaFree(ctx->d_costT);
+    }
+    ctx->d_costT = nullptr;
+    ctx->costT_cap = 0;
+    ctx->costT_valid = false;
+    if (cudaMalloc(&ctx->d_costT, sizeof(double) * (size_t)M * insts[0].n_bases) == cudaSuccess) {
+      ctx->costT_cap = (size_t)M * insts[0].n_bases;
+    } else {
+      cudaGetLastError();
+      ctx->d_costT = nullptr;
+      cost_t = false;
+    }
+  }
   size_t tt = 0;
   std::vector<size_t> tbase(n, 0);
   for (int s = 0; s < n; ++s) {
@@ -475,7 +546,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     ctx->ws_cap = want;
     return true;
   };
-  if (!(cost_t && ws_get(o_costT + 8ull * tt))) {
+  if (!(cost_t && ws_get(o_costT + (ctx_copy ? 0 : 8ull * tt)))) {
     cost_t = false;
     if (!ws_get(o_costT)) throw FpError(FP_ERR_OUT_OF_MEMORY, "search workspace");
   }
@@ -519,7 +590,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       std::memcpy(hb + L.cost, host_tables[s], 8ull * M * B);
     fpk::Scenario& S = run.scs[s];
     S.cost = dev_tables[s] ? dev_tables[s] : reinterpret_cast<const double*>(db + L.cost);
-    S.costT = cost_t ? d_costT + tbase[s] : nullptr;
+    S.costT = !cost_t ? nullptr : ctx_copy ? ctx->d_costT : d_costT + tbase[s];
     S.ro = db + L.ro;
     S.vfixed = db + L.vfixed;
     S.bheli = db + L.bheli;
@@ -555,6 +626,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.hrs = reinterpret_cast<long long*>(dw + L.hrs);
     S.hue = reinterpret_cast<int32_t*>(dw + L.hue);
     S.impT = reinterpret_cast<uint32_t*>(dw + L.impT);
+    S.vseg = reinterpret_cast<int32_t*>(dw + L.vseg);
+    S.vcur = reinterpret_cast<int32_t*>(dw + L.vcur);
+    S.vch = reinterpret_cast<int32_t*>(dw + L.vch);
     S.nvw = (V + 31) / 32;
     {
       const size_t nsub = ((size_t)M + fpk::kChainSub - 1) / fpk::kChainSub + 1;
@@ -584,13 +658,16 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     ctx->perm_cap = chunk_ints;
   }
   double init_ms = 0.0, sweep_ms = 0.0;
-  cudaEvent_t ei0, ei1;
-  check(cudaEventCreate(&ei0), "event");
-  check(cudaEventCreate(&ei1), "event");
-  check(cudaEventRecord(ei0, st), "event");
-  check(fpk::launch_init(d_scs, n, M, maxB, maxV, cost_t, st), "init_kernel");
-  check(cudaEventRecord(ei1, st), "event");
-  ctx->launches += 1 + (M > 0 ? 1 : 0) + (maxB > 0 ? 1 : 0) + (cost_t && M > 0 && maxB > 0 ? 1 : 0);
+  cudaEvent_t ei[5];
+  for (auto& e : ei) check(cudaEventCreate(&e), "event");
+  const bool transpose = cost_t && !(ctx_copy && ctx->costT_valid);
+  if (cost_t && ctx_copy && ctx->costT_valid) check(cudaStreamWaitEvent(st, ctx->costT_ready, 0), "wait");
+  check(fpk::launch_init(d_scs, run.scs.data(), n, M, maxB, maxV, transpose, st, ei),
+        "init_kernel");
+  if (ctx_copy && cost_t) ctx->costT_valid = true;
+  const bool rows_stream = n == 1 && cost_t && M > 0 && maxB > 0 && maxV > 0;
+  ctx->launches += 1 + (M > 0 ? 1 : 0) + (rows_stream ? 4 : (maxB > 0 ? 1 : 0)) +
+                   (transpose && M > 0 && maxB > 0 ? 1 : 0);
   tr.mark("allocated, staged, init launched");
   std::vector<cudaEvent_t> sweep_ev;  // (start, end) pairs around grid-wide sweeps
   PermStream rng(cfg->seed);
@@ -672,12 +749,16 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   }
   check(cudaStreamSynchronize(st), "final sync");
   tr.mark("final sync");
+  double init_part[4] = {0, 0, 0, 0};
   {
     float ims = 0.f;
-    cudaEventElapsedTime(&ims, ei0, ei1);
+    cudaEventElapsedTime(&ims, ei[0], ei[4]);
     init_ms = ims;
-    cudaEventDestroy(ei0);
-    cudaEventDestroy(ei1);
+    for (int k = 0; k < 4; ++k) {
+      cudaEventElapsedTime(&ims, ei[k], ei[k + 1]);
+      init_part[k] = ims;
+    }
+    for (auto& e : ei) cudaEventDestroy(e);
   }
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ev0, ev1);
@@ -701,6 +782,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     outs[s].device_ms = ms;
     outs[s].exact_fallbacks = c.fallbacks;
     outs[s].init_ms = init_ms;
+    for (int k = 0; k < 4; ++k) outs[s].init_part_ms[k] = init_part[k];
     outs[s].sweep_ms = sweep_ms;
     for (int k = 0; k < 16; ++k) outs[s].phase_cycles[k] = c.cycles[k];
     for (int k = 0; k < 5; ++k) outs[s].event_counts[k] = c.counts[k];
@@ -741,6 +823,13 @@ void fp_ctx_destroy(fp_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->d_cost) cudaFree(ctx->d_cost);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->aux) cudaStreamSynchronize(ctx->aux);
+  if (ctx->d_costT) cudaFree(ctx->d_costT);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->table_ready) cudaEventDestroy(ctx->table_ready);
+  if (ctx->costT_ready) cudaEventDestroy(ctx->costT_ready);
+  if (ctx->copy_t0) cudaEventDestroy(ctx->copy_t0);
+  if (ctx->copy_t1) cudaEventDestroy(ctx->copy_t1);
   for (auto& p : ctx->h_perm)
     if (p) cudaFreeHost(p);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -750,6 +839,15 @@ void fp_ctx_destroy(fp_ctx* ctx) {
 uint64_t fp_ctx_kernel_launches(const fp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 double fp_ctx_last_kernel_ms(const fp_ctx* ctx) { return ctx ? ctx->last_kernel_ms : 0.0; }
+
+double fp_ctx_last_copy_ms(fp_ctx* ctx) {
+  if (!ctx || !ctx->copy_timed) return 0.0;
+  cudaSetDevice(ctx->device);
+  if (cudaEventSynchronize(ctx->copy_t1) != cudaSuccess) return 0.0;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->copy_t0, ctx->copy_t1);
+  return ms;
+}
 
 fp_status fp_validate_instance(const fp_instance* inst) {
   return guarded([&] { validate(inst); });
@@ -806,6 +904,7 @@ fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* in, double rad
           "table_kernel");
     ctx->last_kernel_ms = tk.stop_ms();
     ctx->launches += 4;
+    start_costT(ctx);
     if (out_cost) d2h(out_cost, ctx->d_cost, (size_t)M * B, st);
     check(cudaStreamSynchronize(st), "table sync");
   });
@@ -845,6 +944,7 @@ fp_status fp_table_upload(fp_ctx* ctx, int32_t n_missions, int32_t n_bases,
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
     table_alloc(ctx, n_missions, n_bases);
     h2d(ctx->d_cost, cost_colmajor, (size_t)n_missions * n_bases, ctx->stream);
+    start_costT(ctx);
     check(cudaStreamSynchronize(ctx->stream), "upload sync");
   });
 }

@@ -67,6 +67,8 @@ struct HelperCtl {
 // Exact fixed-order sums are walked in chunks of kChainSub terms (see
 // exact_chain_helped).
 constexpr int kChainSub = 2048;
+// Missions per block of the row-major relocation-table build.
+constexpr int kRowsChunk = 256;
 constexpr int kNoBinade = -100000;
 
 // One search scenario: the resident distance table plus the index-based
@@ -120,6 +122,11 @@ struct Scenario {
   // cost); maintained on every move, so the per-pass rebuild of imp is a
   // gather of M rows instead of V*M table entries
   uint32_t* impT;            // [M*NVW]
+  // relocation-table build from the row-major copy: missions grouped by
+  // vehicle (in scratch), per-vehicle segment starts / cursors, chunk plan
+  int32_t* vseg;             // [V+2] segment starts, [V] = M, [V+1] = chunk count
+  int32_t* vcur;             // [V]
+  int32_t* vch;              // [3*(M/kRowsChunk + V + 1)] (vehicle, begin, end)
   int32_t* scratch;          // [M] per-scenario scratch (relocation position lists)
   HelperCtl* hc;             // helper work sharing (zeroed at search start)
   int32_t* hdelta;           // [V] helpers' imp-row popcount deltas

@@ -13,6 +13,7 @@ namespace fpk {
 struct Scenario;
 
 cudaError_t launch_point_cos(const double* lat, int n, double* out, cudaStream_t st);
+cudaError_t launch_transpose(const double* src, int M, int B, double* dst, cudaStream_t stream);
 cudaError_t launch_table(const double* blat, const double* blon, const double* bcos, int B,
                          const double* plat, const double* plon, const double* pcos,
                          const double* dlat, const double* dlon, const double* dcos, int M,
@@ -30,8 +31,8 @@ cudaError_t launch_objective(const double* cost, int M, const int32_t* vb, const
 cudaError_t launch_candidate_delta(const double* cost, int M, const int32_t* vb, const int32_t* mv,
                                    int kind, int j, int newcol, int mover, double* out,
                                    cudaStream_t st);
-cudaError_t launch_init(Scenario* d_scs, int n_scn, int M, int maxB, int maxV, bool cost_t,
-                        cudaStream_t stream);
+cudaError_t launch_init(Scenario* d_scs, const Scenario* h_scs, int n_scn, int M, int maxB,
+                        int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev);
 cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream);
 cudaError_t launch_sweep(Scenario* d_scs, const int32_t* d_active, int n_scn,
                          const int32_t* d_perms, int M, cudaStream_t stream);

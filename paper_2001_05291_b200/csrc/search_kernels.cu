@@ -2138,25 +2138,45 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   }
 }
 
-// The row-major copy of the table, 32 x 32 tiles through shared memory.
+// The row-major copy of a column-major table: 32-base x 64-mission tiles
+// through shared memory, eight 8-byte loads in flight per thread, 256-byte
+// coalesced rows on both sides.
+__device__ __forceinline__ void transpose_tile(const double* __restrict__ src, int M, int B,
+                                               double* __restrict__ dst, int m0, int b0) {
+  __shared__ double tile[32][65];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  double v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int b = b0 + ty + 8 * (r >> 1), m = m0 + tx + 32 * (r & 1);
+    v[r] = (b < B && m < M) ? src[(long long)b * M + m] : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r) tile[ty + 8 * (r >> 1)][tx + 32 * (r & 1)] = v[r];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int m = m0 + ty + 8 * r, b = b0 + tx;
+    if (m < M && b < B) dst[(long long)m * B + b] = tile[tx][ty + 8 * r];
+  }
+}
+
 __global__ void __launch_bounds__(256) transpose_kernel(Scenario* scs) {
   const Scenario s = scs[blockIdx.z];
-  const int m0 = blockIdx.x * 32, b0 = blockIdx.y * 32;
+  const int m0 = blockIdx.x * 64, b0 = blockIdx.y * 32;
   if (!s.costT || m0 >= s.M || b0 >= s.B) return;
-  __shared__ double tile[32][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {
-    const int b = b0 + r, m = m0 + tx;
-    if (b < s.B && m < s.M) tile[r][tx] = s.cost[(long long)b * s.M + m];
-  }
-  __syncthreads();
-  double* out = const_cast<double*>(s.costT);
-#pragma unroll
-  for (int r = ty; r < 32; r += 8) {
-    const int m = m0 + r, b = b0 + tx;
-    if (m < s.M && b < s.B) out[(long long)m * s.B + b] = tile[tx][r];
-  }
+  transpose_tile(s.cost, s.M, s.B, const_cast<double*>(s.costT), m0, b0);
+}
+
+__global__ void __launch_bounds__(256) transpose_table_kernel(const double* __restrict__ src, int M,
+                                                              int B, double* __restrict__ dst) {
+  transpose_tile(src, M, B, dst, blockIdx.x * 64, blockIdx.y * 32);
+}
+
+cudaError_t launch_transpose(const double* src, int M, int B, double* dst, cudaStream_t stream) {
+  if (M > 0 && B > 0)
+    transpose_table_kernel<<<dim3((M + 63) / 64, (B + 31) / 32), 256, 0, stream>>>(src, M, B, dst);
+  return cudaGetLastError();
 }
 
 // Search start: per-mission costs and the exact initial fixed-order total
@@ -2213,6 +2233,128 @@ __global__ void __launch_bounds__(256) table_rows_kernel(Scenario* scs) {
   if (threadIdx.x == 0) sh.c = *s.ctr;
   __syncthreads();
   table_row_fresh<256>(s, sh, acc_sum, acc_abs, stage, t);
+}
+
+// ---- relocation-table build from the row-major copy (single scenario) ----
+// D(t, v) for every base t at once: a block takes a chunk of vehicle v's
+// missions and streams their rows of the row-major table (B contiguous
+// costs each), thread per base with register accumulators; chunks combine
+// with fp64 atomics (any order: the table's bounds hold for any summation
+// order). HBM-bound: every table entry is read once, coalesced.
+
+// Plan: per-vehicle segment starts and the chunk list. One thread.
+__global__ void rows_plan_kernel(Scenario* scs) {
+  const Scenario s = scs[0];
+  if (threadIdx.x != 0) return;
+  int off = 0, nc = 0;
+  for (int v = 0; v < s.V; ++v) {
+    s.vseg[v] = off;
+    s.vcur[v] = off;
+    const int c = s.vcount[v];
+    for (int k = 0; k < c; k += kRowsChunk) {
+      s.vch[3 * nc] = v;
+      s.vch[3 * nc + 1] = off + k;
+      s.vch[3 * nc + 2] = off + min(c, k + kRowsChunk);
+      ++nc;
+    }
+    off += c;
+  }
+  s.vseg[s.V] = off;
+  s.vseg[s.V + 1] = nc;
+}
+
+// Missions grouped by vehicle into scratch (order inside a group is free).
+__global__ void __launch_bounds__(256) rows_group_kernel(Scenario* scs) {
+  const Scenario s = scs[0];
+  const int m = blockIdx.x * 256 + threadIdx.x;
+  if (m >= s.M) return;
+  const int pos = atomicAdd(&s.vcur[s.mv[m]], 1);
+  s.scratch[pos] = m;
+}
+
+// Block = (chunk c of a vehicle's missions, 512 consecutive bases): thread
+// per pair of bases, eight mission rows loaded before any is accumulated.
+__global__ void __launch_bounds__(256) rows_stream_kernel(Scenario* scs) {
+  constexpr int NT = 256, R = 2, U = 8;
+  const Scenario s = scs[0];
+  const int c = blockIdx.x;
+  if (c >= s.vseg[s.V + 1]) return;
+  const int v = s.vch[3 * c], k0 = s.vch[3 * c + 1], n = s.vch[3 * c + 2] - k0;
+  const int B = s.B;
+  const int tb = blockIdx.y * (NT * R) + threadIdx.x;
+  __shared__ int mk[kRowsChunk];
+  __shared__ double mck[kRowsChunk];
+  for (int k = threadIdx.x; k < n; k += NT) {
+    const int m = s.scratch[k0 + k];
+    mk[k] = m;
+    mck[k] = s.mc[m];
+  }
+  __syncthreads();
+  if (blockIdx.y * (NT * R) >= B) return;
+  double as[R], aa[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    as[i] = 0.0;
+    aa[i] = 0.0;
+  }
+  bool ok[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) ok[i] = tb + i * NT < B;
+  int k = 0;
+  for (; k + U <= n; k += U) {
+    double x[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double* row = s.costT + (long long)mk[k + u] * B + tb;
+#pragma unroll
+      for (int i = 0; i < R; ++i) x[u][i] = ok[i] ? row[i * NT] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double mcm = mck[k + u];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const double d = x[u][i] - mcm;
+        as[i] += d;
+        aa[i] += fabs(d);
+      }
+    }
+  }
+  for (; k < n; ++k) {
+    const double* row = s.costT + (long long)mk[k] * B + tb;
+    const double mcm = mck[k];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double d = (ok[i] ? row[i * NT] : 0.0) - mcm;
+      as[i] += d;
+      aa[i] += fabs(d);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const int t = tb + i * NT;
+    if (ok[i] && s.bveh[t] < 0) {
+      atomicAdd(&s.rA[tix(s, t, v)], as[i]);
+      atomicAdd(&s.rU[tix(s, t, v)], aa[i]);
+    }
+  }
+}
+
+// Bounds and classes of the streamed rows: entry (t, v), t fastest.
+__global__ void __launch_bounds__(256) rows_finish_kernel(Scenario* scs) {
+  const Scenario s = scs[0];
+  __shared__ Shared sh;
+  if (threadIdx.x == 0) sh.c = *s.ctr;
+  __syncthreads();
+  const long long e = (long long)blockIdx.x * 256 + threadIdx.x;
+  if (e >= (long long)s.B * s.V) return;
+  const int v = (int)(e / s.B), t = (int)(e % s.B);
+  if (s.bveh[t] >= 0) return;
+  const int n = s.vcount[v];
+  const double U = s.rU[e] * (1.0 + (double)(n + 2) * kTwoPowM52);
+  s.rU[e] = U;
+  s.rE[e] = (double)(n + 2) * kTwoPowM52 * U;
+  if (table_class(s, sh, t, v) != CLS_POS) atomicAdd(&s.rcnt[t], 1);
 }
 
 // Exact fixed-order final total (st.total after the last move): the cached
@@ -2306,15 +2448,35 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                              M, tabu, tenure, debug, V, B, K, helpers_req, epoch, stream);
 }
 
-cudaError_t launch_init(Scenario* d_scs, int n_scn, int M, int maxB, int maxV, bool cost_t,
-                        cudaStream_t stream) {
-  if (cost_t && M > 0 && maxB > 0)
-    transpose_kernel<<<dim3((M + 31) / 32, (maxB + 31) / 32, n_scn), 256, 0, stream>>>(d_scs);
+// ev[0..4]: events recorded around the four stages (may be null).
+cudaError_t launch_init(Scenario* d_scs, const Scenario* h_scs, int n_scn, int M, int maxB,
+                        int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev) {
+  if (ev) cudaEventRecord(ev[0], stream);
+  if (transpose && M > 0 && maxB > 0)
+    transpose_kernel<<<dim3((M + 63) / 64, (maxB + 31) / 32, n_scn), 256, 0, stream>>>(d_scs);
+  if (ev) cudaEventRecord(ev[1], stream);
   init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
+  if (ev) cudaEventRecord(ev[2], stream);
   if (M > 0) impt_init_kernel<<<dim3((M + 255) / 256, n_scn), 256, 0, stream>>>(d_scs);
-  const size_t smem = sizeof(double) * (16ull * maxV + 8 * 32);
-  cudaFuncSetAttribute(table_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (maxB > 0) table_rows_kernel<<<dim3(maxB, n_scn), 256, smem, stream>>>(d_scs);
+  if (ev) cudaEventRecord(ev[3], stream);
+  const Scenario& h = h_scs[0];
+  if (n_scn == 1 && h.costT && M > 0 && maxB > 0 && maxV > 0) {
+    // single scenario with the row-major copy: stream it by vehicle chunks
+    const size_t bv = (size_t)h.B * h.V;
+    cudaMemsetAsync(h.rA, 0, sizeof(double) * bv, stream);
+    cudaMemsetAsync(h.rU, 0, sizeof(double) * bv, stream);
+    cudaMemsetAsync(h.rcnt, 0, sizeof(int32_t) * h.B, stream);
+    rows_plan_kernel<<<1, 32, 0, stream>>>(d_scs);
+    rows_group_kernel<<<(M + 255) / 256, 256, 0, stream>>>(d_scs);
+    const int chunks = M / kRowsChunk + maxV + 1;
+    rows_stream_kernel<<<dim3(chunks, (maxB + 511) / 512), 256, 0, stream>>>(d_scs);
+    rows_finish_kernel<<<(unsigned)((bv + 255) / 256), 256, 0, stream>>>(d_scs);
+  } else {
+    const size_t smem = sizeof(double) * (16ull * maxV + 8 * 32);
+    cudaFuncSetAttribute(table_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (maxB > 0) table_rows_kernel<<<dim3(maxB, n_scn), 256, smem, stream>>>(d_scs);
+  }
+  if (ev) cudaEventRecord(ev[4], stream);
   return cudaGetLastError();
 }
 

@@ -323,6 +323,9 @@ class _Ctx:
     def last_kernel_ms(self) -> float:
         return float(lib().fp_ctx_last_kernel_ms(self.p))
 
+    def last_copy_ms(self) -> float:
+        return float(lib().fp_ctx_last_copy_ms(self.p))
+
     def __del__(self):
         try:
             if getattr(self, "p", None):
@@ -498,6 +501,7 @@ class SearchStats:
     event_counts: tuple = ()
     init_ms: float = 0.0
     sweep_ms: float = 0.0
+    init_part_ms: tuple = ()
 
 
 @dataclass
@@ -565,7 +569,7 @@ def _stats(r: A.fp_search_result) -> SearchStats:
                        int(s.tabu_skips_outer), int(s.tabu_skips_inner), float(s.final_objective_km),
                        float(r.device_ms), int(r.exact_fallbacks), tuple(int(x) for x in r.phase_cycles),
                        tuple(int(x) for x in r.event_counts), float(r.init_ms),
-                       float(r.sweep_ms))
+                       float(r.sweep_ms), tuple(float(x) for x in r.init_part_ms))
 
 
 def search_arrays(inst: Instance, t: DistanceTable, cfg: SearchConfig, vehicle_base: np.ndarray,

@@ -217,7 +217,8 @@ def _kernel_rooflines(inst, t, start_ms, r, peak):
     out = {
         "table_kernel": {"ms": start_ms["table"], "bytes": 8 * B * M, "bound": "fp64 ALU",
                          "note": "4 sin + 2 asin + 2 sqrt per entry; bytes are the writes"},
-        "column_totals_kernel": {"ms": start_ms["totals"], "bytes": 8 * B * M, "bound": "hbm"},
+        "column_chain_kernel (fixed-order column totals)": {"ms": start_ms["totals"], "bytes": 8 * B * M,
+                                                            "bound": "hbm"},
     }
     tp, ini, imp_rows, rel_rows = r.stats.init_part_ms
     nvw = (V + 31) // 32

@@ -80,49 +80,6 @@ __global__ void haversine_pairs_kernel(int n, const double* __restrict__ alat,
   out[k] = r;
 }
 
-// Column totals: one warp owns 32 columns and keeps, per lane, the single
-// sequential fp64 chain of its column in row order (bit-identical to the
-// reference by construction). The chains are fed through an S-stage cp.async
-// ring of 32x32 tiles in shared memory: lane l copies row r0+l of each of the
-// 32 columns (coalesced 256 B per column), so the loads of tiles t+1..t+S-1
-// are in flight while the lanes add tile t. Rows are padded to 33 doubles so
-// the transposed reads are conflict-free.
-constexpr int kTotStages = 8;
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-
-__global__ void __launch_bounds__(32)
-    column_totals_kernel(const double* __restrict__ cost, int M, int B, double* __restrict__ out) {
-  extern __shared__ __align__(16) double ring[];  // [kTotStages][32][33]
-  const int l = threadIdx.x;
-  const int c0 = blockIdx.x * 32;
-  const int ntiles = (M + 31) / 32;
-  auto issue = [&](int t) {
-    if (t < ntiles) {
-      double* tile = ring + (t % kTotStages) * 32 * 33;
-      const int r = t * 32 + l;
-      if (r < M)
-        for (int k = 0; k < 32 && c0 + k < B; ++k)
-          cp_async8(&tile[k * 33 + l], &cost[(long long)(c0 + k) * M + r]);
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  for (int t = 0; t < kTotStages - 1; ++t) issue(t);
-  double sum = 0.0;
-  for (int t = 0; t < ntiles; ++t) {
-    issue(t + kTotStages - 1);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(kTotStages - 1) : "memory");
-    __syncwarp();
-    const double* tile = ring + (t % kTotStages) * 32 * 33;
-    const int n = min(32, M - t * 32);
-    for (int k = 0; k < n; ++k) sum = __dadd_rn(sum, tile[l * 33 + k]);
-    __syncwarp();
-  }
-  if (c0 + l < B) out[c0 + l] = sum;
-}
 
 // Per-mission argmin over the chosen (occupied) bases whose vehicle may fly
 // the mission; ties fall to the lower base id (proj/src/rank.cpp:92-116).
@@ -225,11 +182,102 @@ cudaError_t launch_haversine_pairs(int n, const double* alat, const double* alon
   return cudaGetLastError();
 }
 
+// rn(x / u) for u = 2^(e-52), exact power-of-two scaling; tie flag; a term
+// >= 4e15 u leaves the binade by itself.
+__device__ __forceinline__ long long col_round(double x, double inv_u, bool& tie) {
+  const double y = x * inv_u;
+  tie = false;
+  if (y >= 4.0e15) return 1ll << 53;
+  const double f = floor(y);
+  const double fr = y - f;
+  tie = fr == 0.5;
+  return (long long)f + (fr >= 0.5 ? 1 : 0);
+}
+
+// Kernel (2), warp per column: the fixed-order fp64 column sum, bit-exact,
+// without a sequential add chain. While the running sum S stays in one
+// binade [2^e, 2^(e+1)) every partial sum is a multiple of u = 2^(e-52), so
+// fl(S + c) = S + u rn(c/u) unless c/u is an exact tie; a step of 32*UE terms
+// (lanes coalesced over consecutive missions) is an integer sum, and the
+// first step that leaves the binade or holds a tie is resolved exactly by one
+// lane scan per 32 terms and one true fp64 add (the same algorithm as the
+// search's exact_chain). HBM-bound: each entry read once.
+__global__ void __launch_bounds__(256)
+    column_chain_kernel(const double* __restrict__ cost, int M, int B, double* __restrict__ out) {
+  constexpr int UE = 32;
+  constexpr long long LIM = 1ll << 53;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int l = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const double* col = cost + (long long)b * M;
+  double S = 0.0;
+  int k = 0;
+  if (l == 0)
+    while (k < M && !(S >= 0x1p-900)) S = __dadd_rn(S, col[k++]);  // leading zeros / tiny values
+  S = __shfl_sync(FULL, S, 0);
+  k = __shfl_sync(FULL, k, 0);
+  while (k < M) {
+    const int e = ilogb(S);
+    const double u = ldexp(1.0, e - 52), inv_u = ldexp(1.0, 52 - e);
+    const long long N0 = (long long)(S * inv_u);
+    // the whole step's terms in flight before any is used
+    double xv[UE];
+#pragma unroll
+    for (int q = 0; q < UE; ++q) {
+      const int kk = k + q * 32 + l;
+      xv[q] = kk < M ? col[kk] : 0.0;
+    }
+    long long local = 0;
+    bool any_tie = false;
+#pragma unroll
+    for (int q = 0; q < UE; ++q) {
+      bool tie;
+      local = min(local + col_round(xv[q], inv_u, tie), LIM);
+      any_tie |= tie;  // padding zeros never tie
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(FULL, local, o);
+    if (N0 + local < LIM && !__any_sync(FULL, any_tie)) {
+      S = (double)(N0 + local) * u;
+      k = min(M, k + 32 * UE);
+      continue;
+    }
+    // the first event of the step: one lane scan per 32 terms
+    long long run = N0;
+    bool found = false;
+    int ev = 0;
+    long long before = 0;
+#pragma unroll
+    for (int q = 0; q < UE; ++q) {
+      if (!found) {
+        const int kk = k + q * 32 + l;
+        bool tq;
+        const long long r = col_round(xv[q], inv_u, tq);
+        long long incl = r;
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long y = __shfl_up_sync(FULL, incl, o);
+          if (l >= o) incl += y;
+        }
+        const unsigned hit = __ballot_sync(FULL, kk < M && (tq || run + incl >= LIM));
+        if (hit) {
+          const int f = __ffs(hit) - 1;
+          before = run + __shfl_sync(FULL, incl - r, f);
+          ev = k + q * 32 + f;
+          found = true;
+        } else {
+          run += __shfl_sync(FULL, incl, 31);
+        }
+      }
+    }
+    S = __dadd_rn((double)before * u, col[ev]);
+    k = ev + 1;
+  }
+  if (l == 0) out[b] = S;
+}
+
 cudaError_t launch_column_totals(const double* cost, int M, int B, double* out, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * kTotStages * 32 * 33;
-  cudaFuncSetAttribute(column_totals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  column_totals_kernel<<<(B + 31) / 32, 32, smem, st>>>(cost, M, B, out);
+  column_chain_kernel<<<(B + 7) / 8, 256, 0, st>>>(cost, M, B, out);
   return cudaGetLastError();
 }
 

@@ -240,3 +240,35 @@ def test_helper_assisted_exact_chains_match_single_block_chains(monkeypatch, sha
     assert _stats_key(runs[0]) == _stats_key(runs[1])
     assert np.array_equal(runs[0].vehicle_base, runs[1].vehicle_base)
     assert np.array_equal(runs[0].mission_vehicle, runs[1].mission_vehicle)
+
+
+def _seq_sum(col):
+    s = 0.0
+    for x in col.tolist():
+        s += x  # IEEE fp64, left to right
+    return s
+
+
+def test_column_totals_exact_on_adversarial_columns():
+    """Kernel (2)'s integer-binade chains against left-to-right fp64 sums on
+    columns built to hit every path: leading zeros and tiny values, exact
+    rounding ties (power-of-two multiples), terms that cross several binades
+    at once, long runs inside one binade, a single huge term late, and
+    random costs; M not a multiple of the 1024-term step."""
+    rng = np.random.default_rng(5)
+    M = 5000 + 37
+    cols = [
+        np.concatenate([np.zeros(100), rng.uniform(0, 1e-300, 50), rng.uniform(1, 2, M - 150)]),
+        np.full(M, 0.75),                                    # ties once S is large
+        np.ldexp(1.0, rng.integers(-3, 4, M)).astype(np.float64) * 1.5,
+        np.concatenate([rng.uniform(0, 1e3, M - 1), [1e12]]),
+        rng.uniform(0, 2e4, M),
+        np.where(rng.random(M) < 0.5, 0.5, 3.0 * 2.0 ** -20),
+        np.concatenate([[1e15], rng.uniform(0, 1, M - 1)]),
+        rng.integers(0, 5, M).astype(np.float64) * 0.125,
+    ]
+    table = np.stack(cols, axis=1)  # (M, B) column-major semantics
+    t = F.DistanceTable.from_host(table)
+    got = F.column_totals(t)
+    want = np.array([_seq_sum(table[:, b]) for b in range(table.shape[1])])
+    assert np.array_equal(got.view(np.int64), want.view(np.int64)), (got, want)

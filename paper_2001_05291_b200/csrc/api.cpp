@@ -485,6 +485,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // independently); large ones run one pass per launch after the grid-wide
   // sweep. Permutations for a chunk of passes are generated on the host
   // while the device runs the previous chunk.
+  // (single scenarios: one block rebuilding its bitsets is slower than the
+  // grid-wide sweep plus a relaunch once V*M passes 64K)
   const bool inkernel = n > 1 || (long long)maxV * M <= (64ll << 10);
   // passes per host round trip: in-kernel mode runs them in one launch; the
   // sweep mode enqueues (sweep, pass) launch pairs that exit at once when the

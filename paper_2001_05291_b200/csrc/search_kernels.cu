@@ -1735,34 +1735,77 @@ __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) &
 
 }  // namespace
 
+// 32 x 32 bit-matrix transpose across a warp: lane r holds row r (bit c =
+// column c); afterwards lane c holds column c (bit r = row r). Five
+// shuffle-exchange stages swapping the off-diagonal j x j blocks.
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
+  uint32_t m = 0x0000FFFFu;
+#pragma unroll
+  for (int j = 16; j != 0; j >>= 1, m ^= (m << j)) {
+    const uint32_t y = __shfl_xor_sync(FULL, x, j);
+    if ((lane & j) == 0) {
+      x ^= (((x >> j) ^ y) & m) << j;
+    } else {
+      x ^= ((y >> j) ^ x) & m;
+    }
+  }
+  return x;
+}
+
 // Per pass: the perm_b-ordered mirrors and the imp/mem bitsets, warp per
 // word, lane per position: each lane gathers its mission's natural-order
 // improvement row (NVW words) and the warp transposes it into the V
 // position-order words with ballots; mem from the mirrored vehicles.
 __device__ void prep_words(const Scenario& s, const int32_t* __restrict__ pb, int wd0, int wstride) {
+  constexpr int UW = 4;  // words per warp iteration: their loads in flight together
   const int l = threadIdx.x & 31;
-  for (int wd = wd0; wd < s.nwd; wd += wstride) {
-    const int q = wd * 32 + l;
-    const bool valid = q < s.M;
-    int j = 0, v = -1;
-    if (valid) {
-      j = pb[q];
-      v = s.mv[j];
-      s.mvp[q] = v;
-      s.mcp[q] = s.mc[j];
-      s.rop[q] = s.ro[j];
-      s.invb[j] = q;
+  const int nvw = s.nvw, V = s.V;
+  for (int wb = wd0; wb < s.nwd; wb += wstride * UW) {
+    int j[UW], v[UW];
+    bool valid[UW];
+#pragma unroll
+    for (int u = 0; u < UW; ++u) {
+      const int wd = wb + u * wstride;
+      const int q = wd * 32 + l;
+      valid[u] = wd < s.nwd && q < s.M;
+      j[u] = valid[u] ? pb[q] : 0;
     }
-    for (int vw = 0; vw < s.nvw; ++vw) {
-      const uint32_t row = valid ? s.impT[(long long)j * s.nvw + vw] : 0u;
-      const int gend = min(32, s.V - vw * 32);
-      for (int b = 0; b < gend; ++b) {
-        const int g = vw * 32 + b;
-        const unsigned m = __ballot_sync(FULL, (row >> b) & 1u);
-        const unsigned mm = __ballot_sync(FULL, v == g);
-        if (l == 0) {
-          s.imp[(long long)g * s.nwd + wd] = m;
-          s.mem[(long long)g * s.nwd + wd] = mm;
+    double mcv[UW];
+    uint8_t rov[UW];
+#pragma unroll
+    for (int u = 0; u < UW; ++u) {
+      v[u] = valid[u] ? s.mv[j[u]] : -1;
+      mcv[u] = valid[u] ? s.mc[j[u]] : 0.0;
+      rov[u] = valid[u] ? s.ro[j[u]] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < UW; ++u) {
+      if (valid[u]) {
+        const int q = (wb + u * wstride) * 32 + l;
+        s.mvp[q] = v[u];
+        s.mcp[q] = mcv[u];
+        s.rop[q] = rov[u];
+        s.invb[j[u]] = q;
+      }
+    }
+    // per vehicle word: the 32 lanes' rows form a 32 x 32 bit matrix; its
+    // transpose gives lane b the position word of vehicle 32*vw + b
+    for (int vw = 0; vw < nvw; ++vw) {
+      const int g = vw * 32 + l;
+      uint32_t rows[UW];
+#pragma unroll
+      for (int u = 0; u < UW; ++u) rows[u] = valid[u] ? s.impT[(long long)j[u] * nvw + vw] : 0u;
+#pragma unroll
+      for (int u = 0; u < UW; ++u) {
+        const int wd = wb + u * wstride;
+        if (wd >= s.nwd) break;
+        const uint32_t row = rows[u];
+        const int dv = v[u] - vw * 32;
+        const uint32_t one = (dv >= 0 && dv < 32) ? 1u << dv : 0u;
+        const uint32_t it = transpose32(row, l), mt = transpose32(one, l);
+        if (g < V) {
+          s.imp[(long long)g * s.nwd + wd] = it;
+          s.mem[(long long)g * s.nwd + wd] = mt;
         }
       }
     }

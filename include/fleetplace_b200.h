@@ -168,6 +168,13 @@ double fp_ctx_last_kernel_ms(const fp_ctx* ctx);
  * fp_table_upload; waits for it), or 0 if none was made. */
 double fp_ctx_last_copy_ms(fp_ctx* ctx);
 
+/* The search's permutation stream (perm_a, perm_b of every pass: std::
+ * mt19937_64(seed), Fisher-Yates with uniform_below; proj/src/search.cpp:
+ * 401-413) drawn on the device: 2*passes permutations of n into out
+ * [2*passes*n]. Used by searches whose passes run in one launch; exposed for
+ * tests. n >= 2. */
+fp_status fp_permutations(fp_ctx* ctx, uint64_t seed, int32_t n, int32_t passes, int32_t* out);
+
 /* ---- instance validation / generation (host) -------------------------- */
 /* validate_instance (proj/src/model.cpp:46-74). */
 fp_status fp_validate_instance(const fp_instance* inst);

@@ -16,7 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libfleetplace_b200.so"
-SOURCES = ["api.cpp", "generator.cpp", "table_rank_kernels.cu", "search_kernels.cu"]
+SOURCES = ["api.cpp", "generator.cpp", "table_rank_kernels.cu", "search_kernels.cu", "perm_kernels.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -20,6 +20,7 @@ EXPORTS = (
     "fp_build_distance_table", "fp_table_upload", "fp_table_download",
     "fp_column_totals", "fp_rank_bases", "fp_initial_pool", "fp_search",
     "fp_search_batch", "fp_enumerate_moves", "fp_objective_km", "fp_haversine_batch",
+    "fp_permutations",
 )
 
 _lib: C.CDLL | None = None
@@ -50,6 +51,8 @@ def lib() -> C.CDLL:
     l.fp_ctx_last_kernel_ms.restype = f64
     l.fp_ctx_last_copy_ms.argtypes = [p]
     l.fp_ctx_last_copy_ms.restype = f64
+    l.fp_permutations.argtypes = [p, u64, i32, i32, i32p]
+    l.fp_permutations.restype = i32
     l.fp_validate_instance.argtypes = [inst_p]
     l.fp_validate_instance.restype = i32
     l.fp_generate_instance.argtypes = [u64, f64p, i32, i32, i32, i32, f64, u64, i32, i32,

@@ -361,7 +361,7 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   L.habs = putA(8ull * V);
   const size_t nsub = ((size_t)M + fpk::kChainSub - 1) / fpk::kChainSub + 1;
   L.hec = putA(4ull * nsub);
-  L.cost = own_cost ? putA(8ull * M * B + 16) : 0;
+  L.cost = own_cost ? putB(8ull * M * B + 16) : 0;
   L.mc = putB(8ull * M);
   L.mvp = putB(4ull * M);
   L.mcp = putB(8ull * M);
@@ -491,10 +491,14 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // passes per host round trip: in-kernel mode runs them in one launch; the
   // sweep mode enqueues (sweep, pass) launch pairs that exit at once when the
   // scenario is done, so the host only synchronises once per chunk
-  int kchunk = (int)std::max<long long>(
-      1, std::min<long long>(inkernel ? 64 : 16, (16ll << 20) / (8ll * std::max(M, 1))));
-  if (const char* e = std::getenv("FLEETPLACE_KPASSES")) kchunk = std::max(1, std::atoi(e));
-  const size_t chunk_ints = 2ull * kchunk * M + 2;
+  // In-kernel chunks hold up to 1024 passes (64 MB of permutations); a
+  // single scenario's chunks grow 32, 64, ... so a short search generates
+  // few permutations.
+  int kmax = (int)std::max<long long>(
+      1, std::min<long long>(inkernel ? 1024 : 16,
+                             ((inkernel ? 64ll : 16ll) << 20) / (8ll * std::max(M, 1))));
+  if (const char* e = std::getenv("FLEETPLACE_KPASSES")) kmax = std::max(1, std::atoi(e));
+  const size_t chunk_ints = 2ull * kmax * M + 2;
   // ---- device workspace (owned by the context, reused across calls):
   // arena | row-major table copies | counters | scenarios | active | perms.
   // The row-major copy of each table (mission-major: one mission's costs at
@@ -530,7 +534,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   }
   const size_t o_B = align_up(totalA), o_ctr = align_up(o_B + totalB), o_scs = align_up(o_ctr + sizeof(fpk::Counters) * n),
                o_act = align_up(o_scs + sizeof(fpk::Scenario) * n),
-               o_perm = align_up(o_act + 4ull * n), o_costT = align_up(o_perm + 4ull * chunk_ints);
+               o_perm = align_up(o_act + 4ull * n), o_mt = align_up(o_perm + 4ull * chunk_ints),
+               o_pbad = align_up(o_mt + sizeof(fpk::MtState)),
+               o_draws = align_up(o_pbad + sizeof(int)),
+               o_costT = align_up(o_draws + (inkernel ? 16ull * kmax * (size_t)std::max(M - 1, 0) : 0));
   auto ws_get = [&](size_t bytes) -> bool {
     if (bytes <= ctx->ws_cap) return true;
     if (ctx->ws) {
@@ -558,6 +565,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   int32_t* const d_active = reinterpret_cast<int32_t*>(d0 + o_act);
   int32_t* const d_perm = reinterpret_cast<int32_t*>(d0 + o_perm);
   double* const d_costT = reinterpret_cast<double*>(d0 + o_costT);
+  fpk::MtState* const d_mt = reinterpret_cast<fpk::MtState*>(d0 + o_mt);
+  int* const d_pbad = reinterpret_cast<int*>(d0 + o_pbad);
+  unsigned long long* const d_draws = reinterpret_cast<unsigned long long*>(d0 + o_draws);
   std::vector<fpk::Counters> ctrs(n);
   for (int s = 0; s < n; ++s) {
     ctrs[s] = fpk::Counters{};
@@ -588,10 +598,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     if (B) std::memcpy(hb + L.bveh, h.bveh.data(), 4ull * B);
     if (h.psize) std::memcpy(hb + L.pkind, h.pkind.data(), 4ull * h.psize);
     if (h.psize) std::memcpy(hb + L.pidx, h.pidx.data(), 4ull * h.psize);
-    if (!dev_tables[s] && (size_t)M * B)
-      std::memcpy(hb + L.cost, host_tables[s], 8ull * M * B);
+
     fpk::Scenario& S = run.scs[s];
-    S.cost = dev_tables[s] ? dev_tables[s] : reinterpret_cast<const double*>(db + L.cost);
+    S.cost = dev_tables[s] ? dev_tables[s] : reinterpret_cast<const double*>(dw + L.cost);
     S.costT = !cost_t ? nullptr : ctx_copy ? ctx->d_costT : d_costT + tbase[s];
     S.ro = db + L.ro;
     S.vfixed = db + L.vfixed;
@@ -648,6 +657,11 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   cudaEvent_t ev0, ev1;
   check(cudaEventCreate(&ev0), "event");
   check(cudaEventCreate(&ev1), "event");
+  // host tables (batches): straight from the caller's buffers into the
+  // device region, before the timed search
+  for (int s = 0; s < n; ++s)
+    if (!dev_tables[s] && (size_t)M * insts[s].n_bases)
+      h2d(const_cast<double*>(run.scs[s].cost), host_tables[s], (size_t)M * insts[s].n_bases, st);
   check(cudaEventRecord(ev0, st), "event");
   h2d(d0, stage.data(), totalA, st);
   h2d(d_scs, run.scs.data(), n, st);
@@ -673,14 +687,37 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   tr.mark("allocated, staged, init launched");
   std::vector<cudaEvent_t> sweep_ev;  // (start, end) pairs around grid-wide sweeps
   PermStream rng(cfg->seed);
-  auto gen_chunk = [&](int32_t* buf) {
-    for (int k = 0; k < kchunk; ++k) {
+  auto gen_chunk = [&](int32_t* buf, int kk) {
+    for (int k = 0; k < kk; ++k) {
       rng.perm(M, buf + 2ll * k * M);
       rng.perm(M, buf + (2ll * k + 1) * M);
     }
   };
+  long long launched = 0;  // passes whose permutations went to the device
+  // batches: one launch for (nearly) every search — a chunk boundary makes
+  // every scenario wait for the slowest; single scenarios start small
+  int kfirst = inkernel && n == 1 ? std::min(kmax, 32) : kmax;
+  if (const char* e = std::getenv("FLEETPLACE_KFIRST")) kfirst = std::max(1, std::min(kmax, std::atoi(e)));
+  auto next_chunk = [&](int prev) {
+    int k = prev == 0 ? kfirst : std::min(kmax, 2 * prev);
+    if (cfg->max_passes >= 0) k = (int)std::max<long long>(1, std::min<long long>(k, cfg->max_passes - launched));
+    return k;
+  };
+  // In-kernel mode draws the permutations on the device (perm_kernels.cu):
+  // the host stream is the bottleneck of batches. The host generator stays
+  // the fallback (a rejected draw, FLEETPLACE_DEVICE_PERMS=0).
+  bool dev_perm = inkernel && M >= 2 && fpk::fy_smem_bytes(M) <= (200u << 10);
+  if (const char* e = std::getenv("FLEETPLACE_DEVICE_PERMS")) dev_perm = dev_perm && std::atoi(e) != 0;
+  bool force_bad = std::getenv("FLEETPLACE_PERM_FORCE_BAD") != nullptr;  // test hook
+  if (dev_perm) {
+    fpk::MtState seeded;
+    fpk::mt_seed_host(&seeded, cfg->seed);
+    h2d(d_mt, &seeded, 1, st);
+    check(cudaMemsetAsync(d_pbad, 0, sizeof(int), st), "memset");
+  }
+  int kchunk = next_chunk(0);
   int buf = 0;
-  gen_chunk(ctx->h_perm[buf]);  // overlaps the init kernels
+  if (!dev_perm) gen_chunk(ctx->h_perm[buf], kchunk);  // overlaps the init kernels
   tr.mark("first permutation chunk");
   int threads = n == 1 ? 512 : 256;
   if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
@@ -692,11 +729,18 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   int n_active = n;
   while (n_active > 0) {
     h2d(d_active, active.data(), n, st);
-    h2d(d_perm, ctx->h_perm[buf], 2ull * kchunk * M, st);
+    if (dev_perm) {
+      check(fpk::launch_permutations(d_mt, M, 2 * kchunk, d_draws, d_perm, d_pbad, st),
+            "permutations");
+      ctx->launches += 2;
+      if (force_bad) check(cudaMemsetAsync(d_pbad, 1, 1, st), "memset");
+    } else {
+      h2d(d_perm, ctx->h_perm[buf], 2ull * kchunk * M, st);
+    }
     if (inkernel) {
       check(fpk::launch_pass(d_scs, d_active, n, d_perm, kchunk, true,
                              cfg->max_passes, M, tabu, tenure, cfg->debug_check_deltas != 0, maxV,
-                             maxB, maxK, st, threads, 0, 0u),
+                             maxB, maxK, st, threads, 0, 0u, dev_perm ? d_pbad : nullptr),
             "pass_kernel");
       ctx->launches += 1;
     } else {
@@ -713,15 +757,19 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
         check(fpk::launch_pass(d_scs, d_active, n, d_perm + 2ll * k * M, 1,
                                false, cfg->max_passes, M, tabu, tenure,
                                cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads,
-                               helpers, ++epoch),
+                               helpers, ++epoch, nullptr),
               "pass_kernel");
         ctx->launches += M > 0 ? 2 : 1;
       }
     }
     // next chunk's permutations while the device works
+    launched += kchunk;
+    const int knext = next_chunk(kchunk);
     const int nb = buf ^ 1;
-    gen_chunk(ctx->h_perm[nb]);
+    if (!dev_perm) gen_chunk(ctx->h_perm[nb], knext);
     d2h(ctrs.data(), d_ctr, n, st);
+    int pbad = 0;
+    if (dev_perm) d2h(&pbad, d_pbad, 1, st);
     check(cudaStreamSynchronize(st), "pass sync");
     for (size_t e = 0; e + 1 < sweep_ev.size(); e += 2) {
       float ms = 0.f;
@@ -731,7 +779,21 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       cudaEventDestroy(sweep_ev[e + 1]);
     }
     sweep_ev.clear();
+    if (pbad) {
+      // a rejected draw (or the test hook): the pass kernel did not run this
+      // chunk; regenerate the stream exactly on the host and redo the chunk
+      dev_perm = false;
+      force_bad = false;
+      launched -= kchunk;
+      rng = PermStream(cfg->seed);
+      std::vector<int32_t> skip((size_t)std::max(M, 1));
+      for (long long p = 0; p < 2 * launched; ++p) rng.perm(M, skip.data());
+      gen_chunk(ctx->h_perm[buf], kchunk);
+      tr.mark("device permutation chunk rejected: host stream");
+      continue;
+    }
     buf = nb;
+    kchunk = knext;
     tr.mark("chunk synchronised");
     for (int s = 0; s < n; ++s) {
       if (!active[s]) continue;
@@ -841,6 +903,35 @@ void fp_ctx_destroy(fp_ctx* ctx) {
 uint64_t fp_ctx_kernel_launches(const fp_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 double fp_ctx_last_kernel_ms(const fp_ctx* ctx) { return ctx ? ctx->last_kernel_ms : 0.0; }
+
+fp_status fp_permutations(fp_ctx* ctx, uint64_t seed, int32_t n, int32_t passes, int32_t* out) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (n < 2 || passes < 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "need n >= 2, passes >= 0");
+    if (fpk::fy_smem_bytes(n) > (200u << 10)) throw FpError(FP_ERR_INVALID_ARGUMENT, "n too large");
+    const int np = 2 * passes;
+    if (np == 0) return;
+    cudaStream_t st = ctx->stream;
+    DBuf<fpk::MtState> d_mt(1);
+    DBuf<int> d_bad(1);
+    DBuf<unsigned long long> d_draws((size_t)np * (n - 1));
+    DBuf<int32_t> d_perms((size_t)np * n);
+    fpk::MtState seeded;
+    fpk::mt_seed_host(&seeded, seed);
+    h2d(d_mt.p, &seeded, 1, st);
+    check(cudaMemsetAsync(d_bad.p, 0, sizeof(int), st), "memset");
+    check(fpk::launch_permutations(d_mt.p, n, np, d_draws.p, d_perms.p, d_bad.p, st), "perms");
+    ctx->launches += 2;
+    int bad = 0;
+    d2h(&bad, d_bad.p, 1, st);
+    d2h(out, d_perms.p, (size_t)np * n, st);
+    check(cudaStreamSynchronize(st), "perm sync");
+    if (bad) {  // a rejected draw: the exact host stream
+      PermStream rng(seed);
+      for (int p = 0; p < np; ++p) rng.perm(n, out + (size_t)p * n);
+    }
+  });
+}
 
 double fp_ctx_last_copy_ms(fp_ctx* ctx) {
   if (!ctx || !ctx->copy_timed) return 0.0;

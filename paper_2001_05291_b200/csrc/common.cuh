@@ -71,6 +71,12 @@ constexpr int kChainSub = 2048;
 constexpr int kRowsChunk = 256;
 constexpr int kNoBinade = -100000;
 
+// std::mt19937_64 state (the search's permutation stream, perm_kernels.cu).
+struct MtState {
+  unsigned long long mt[312];
+  int idx;
+};
+
 // One search scenario: the resident distance table plus the index-based
 // SearchState of proj/src/search_state.hpp:20-31 in structure-of-arrays
 // form, the perm_b-ordered mirrors the scan streams, and the expiry-stamp

@@ -11,6 +11,12 @@
 
 namespace fpk {
 struct Scenario;
+struct MtState;
+
+void mt_seed_host(MtState* st, unsigned long long seed);
+size_t fy_smem_bytes(int n);
+cudaError_t launch_permutations(MtState* st, int n, int nperm, unsigned long long* draws,
+                                int32_t* perms, int* bad, cudaStream_t stream);
 
 cudaError_t launch_point_cos(const double* lat, int n, double* out, cudaStream_t st);
 cudaError_t launch_transpose(const double* src, int M, int B, double* dst, cudaStream_t stream);
@@ -39,7 +45,8 @@ cudaError_t launch_sweep(Scenario* d_scs, const int32_t* d_active, int n_scn,
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,
                         bool tabu, long long tenure, bool debug, int V, int B, int K,
-                        cudaStream_t stream, int threads, int helpers_req, unsigned epoch);
+                        cudaStream_t stream, int threads, int helpers_req, unsigned epoch,
+                        const int* perm_bad);
 }  // namespace fpk
 
 namespace fpk_host {

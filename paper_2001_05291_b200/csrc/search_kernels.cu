@@ -1889,7 +1889,9 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
                 int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
                 int debug_i, int state_in_smem, int bits_in_smem, int mirrors_in_smem,
-                int helpers, unsigned epoch) {
+                int helpers, unsigned epoch, const int* __restrict__ perm_bad) {
+  // a rejected draw in the device permutation stream: the host redoes the chunk
+  if (perm_bad && *perm_bad) return;
   // with helpers the grid is one scenario: block 0 runs it, the others help
   const int scn = helpers > 0 ? 0 : blockIdx.x;
   if (!active[scn]) return;
@@ -2419,7 +2421,7 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
                                   const int32_t* d_perms, int kpasses, bool inkernel,
                                   int max_passes, int M, bool tabu, long long tenure, bool debug,
                                   int V, int B, int K, int helpers_req, unsigned epoch,
-                                  cudaStream_t stream) {
+                                  const int* perm_bad, cudaStream_t stream) {
   const size_t core = pass_smem_core(V, NT);
   const size_t state = pass_smem_state(V, B, K);
   const size_t bits = 2 * align16(4ull * V * ((M + 31) / 32));
@@ -2453,13 +2455,14 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   if (helpers > 0) {
     int ip = inkernel ? 1 : 0, t = tabu ? 1 : 0, d = debug ? 1 : 0;
     void* args[] = {&d_scs, &d_active, &d_perms, &kpasses, &ip, &max_passes, &t, &tenure, &d,
-                    (void*)&in_smem, (void*)&bits_smem, (void*)&mirrors_smem, &helpers, &epoch};
+                    (void*)&in_smem, (void*)&bits_smem, (void*)&mirrors_smem, &helpers, &epoch,
+                    (void*)&perm_bad};
     return cudaLaunchCooperativeKernel((const void*)pass_kernel<NT>, dim3(1 + helpers), dim3(NT),
                                        args, smem, stream);
   }
   pass_kernel<NT><<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
                                                max_passes, tabu, tenure, debug, in_smem,
-                                               bits_smem, mirrors_smem, 0, epoch);
+                                               bits_smem, mirrors_smem, 0, epoch, perm_bad);
   return cudaGetLastError();
 }
 
@@ -2480,15 +2483,16 @@ cudaError_t launch_sweep(Scenario* d_scs, const int32_t* d_active, int n_scn,
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,
                         bool tabu, long long tenure, bool debug, int V, int B, int K,
-                        cudaStream_t stream, int threads, int helpers_req, unsigned epoch) {
+                        cudaStream_t stream, int threads, int helpers_req, unsigned epoch,
+                        const int* perm_bad) {
   if (threads == 1024)
     return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                                M, tabu, tenure, debug, V, B, K, helpers_req, epoch, stream);
+                                M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream);
   if (threads == 512)
     return launch_pass_nt<512>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                               M, tabu, tenure, debug, V, B, K, helpers_req, epoch, stream);
+                               M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream);
   return launch_pass_nt<256>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                             M, tabu, tenure, debug, V, B, K, helpers_req, epoch, stream);
+                             M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream);
 }
 
 // ev[0..4]: events recorded around the four stages (may be null).

@@ -410,6 +410,16 @@ class RankedStart:
     unused_index: np.ndarray = None
 
 
+def device_permutations(seed: int, n: int, passes: int, device: int = 0) -> np.ndarray:
+    """The search's permutation stream drawn on the device (fp_permutations):
+    shape (2*passes, n), rows perm_a, perm_b of pass 0, 1, ..."""
+    out = np.empty(2 * passes * n, np.int32)
+    ctx = _Ctx(device)
+    _check(lib().fp_permutations(ctx.p, int(seed) & 0xFFFFFFFFFFFFFFFF, n, passes,
+                                 A.ptr(out, C.c_int32)))
+    return out.reshape(2 * passes, n)
+
+
 def column_totals(t: DistanceTable) -> np.ndarray:
     """proj/src/rank.cpp:10-23 (bit-identical fixed-order column sums)."""
     out = np.empty(t.n_bases, np.float64)

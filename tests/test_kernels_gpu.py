@@ -272,3 +272,36 @@ def test_column_totals_exact_on_adversarial_columns():
     got = F.column_totals(t)
     want = np.array([_seq_sum(table[:, b]) for b in range(table.shape[1])])
     assert np.array_equal(got.view(np.int64), want.view(np.int64)), (got, want)
+
+
+@pytest.mark.parametrize("seed,n,passes", [(7, 2, 3), (7, 200, 40), (0, 5000, 3), (123, 10000, 2),
+                                           (2**64 - 1, 313, 7)])
+def test_device_permutation_stream_matches_reference(seed, n, passes):
+    """perm_kernels.cu (parallel MT19937-64 twist + tempering, Fisher-Yates
+    in shared memory) reproduces the reference's std::mt19937_64 +
+    uniform_below stream bit for bit (the oracle restatement, itself pinned
+    to the reference and the standard's 10000th-output value)."""
+    got = F.device_permutations(seed, n, passes)
+    want = np.empty(2 * passes * n, np.int32)
+    H.ORC.or_permutations(seed, n, passes, want.ctypes.data_as(H.C.POINTER(H.C.c_int32)))
+    assert np.array_equal(got.reshape(-1), want)
+
+
+def test_device_permutation_rejection_fallback(monkeypatch):
+    """Test hook FLEETPLACE_PERM_FORCE_BAD marks the first device chunk as
+    holding a rejected draw: the pass kernels skip it, the host regenerates
+    the stream and the batch result is unchanged."""
+    insts = [F.survey_instance(50, 200, 10, seed=s) for s in (1, 2, 3)]
+    starts, tabs = [], []
+    for inst in insts:
+        t = F.build_distance_table(inst)
+        st = F.rank_bases(inst, t)
+        starts.append(F._state_arrays(st.assignment, F.initial_pool(st, inst), inst))
+        tabs.append(np.ascontiguousarray(t.cost.T).reshape(-1))
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu)
+    base = F.search_batch(insts, starts, cfg, tabs)
+    monkeypatch.setenv("FLEETPLACE_PERM_FORCE_BAD", "1")
+    forced = F.search_batch(insts, starts, cfg, tabs)
+    for a, b in zip(base, forced):
+        assert _stats_key(a) == _stats_key(b)
+        assert np.array_equal(a.mission_vehicle, b.mission_vehicle)

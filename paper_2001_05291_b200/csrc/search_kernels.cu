@@ -1884,7 +1884,10 @@ size_t pass_smem_state(int V, int B, int K) {
 }
 
 // One pass over perm_a for every active scenario (blockIdx.x = scenario).
-template <int NT>
+// INK: the block rebuilds its own mirrors / bitsets between passes (a
+// separate instantiation, so the grid-wide-sweep variant carries none of
+// that code's registers).
+template <int NT, bool INK>
 __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
                 int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
@@ -2016,7 +2019,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     sm.pb = pa + M;
     const long long ps0 = ph_now();
     if (sh.c.check_impt) verify_impt<NT>(s, sh);
-    if (inkernel_prep) {
+    if (INK) {
       prep_words(s, sm.pb, threadIdx.x >> 5, NW);
       __syncthreads();
     } else if (bits_in_smem) {
@@ -2439,7 +2442,8 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
     mirrors_smem = mirrors_smem && std::atoi(e) != 0;
   const size_t smem = core + (in_smem ? state : 0) + (bits_smem ? bits : 0) +
                       (mirrors_smem ? mirrors : 0);
-  cudaFuncSetAttribute(pass_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = inkernel ? pass_kernel<NT, true> : pass_kernel<NT, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // helper blocks: one scenario, one pass per launch, bitsets in global
   // memory, and every block co-resident (cooperative launch)
   int helpers = 0;
@@ -2447,7 +2451,7 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_kernel<NT>, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
     helpers = per_sm * sms - 1;
     if (helpers_req > 0 && helpers_req < helpers) helpers = helpers_req;
     if (helpers < 0) helpers = 0;
@@ -2457,10 +2461,10 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
     void* args[] = {&d_scs, &d_active, &d_perms, &kpasses, &ip, &max_passes, &t, &tenure, &d,
                     (void*)&in_smem, (void*)&bits_smem, (void*)&mirrors_smem, &helpers, &epoch,
                     (void*)&perm_bad};
-    return cudaLaunchCooperativeKernel((const void*)pass_kernel<NT>, dim3(1 + helpers), dim3(NT),
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(1 + helpers), dim3(NT),
                                        args, smem, stream);
   }
-  pass_kernel<NT><<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
+  kern<<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
                                                max_passes, tabu, tenure, debug, in_smem,
                                                bits_smem, mirrors_smem, 0, epoch, perm_bad);
   return cudaGetLastError();

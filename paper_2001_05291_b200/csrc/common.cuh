@@ -53,7 +53,15 @@ struct Counters {
 // relocation. The master posts a job by publishing seq = (epoch << 32) | k
 // (epoch = launch number, k = job number within the launch); every helper
 // adds one to `done` when its share is finished.
-enum : int { HJOB_QUIT = 0, HJOB_RELOCATE = 1, HJOB_CHAIN = 2 };
+enum : int { HJOB_QUIT = 0, HJOB_RELOCATE = 1, HJOB_CHAIN = 2, HJOB_LOG = 3 };
+
+// A reassignment / takeover for the relocation-delta table, applied by the
+// helper blocks in the background (each helper owns a slice of the bases).
+struct SubRec {
+  int j, loser, gain, nl, ng, pad;
+  double mc_old, mc_new;
+};
+constexpr int kLogCap = 1024;
 struct HelperCtl {
   unsigned long long seq;
   unsigned done;
@@ -62,6 +70,8 @@ struct HelperCtl {
   int impc_x;        // out: set bits of the mover's new imp row
   int ckind, cj, cmover, ct;  // chain: term kind, mission, mover, base (-1)
   double cnewc;               // chain: the substituted cost (kind 1)
+  unsigned long long log_tail;  // (launch << 32) | records published in the launch
+  unsigned log_done;            // helper-record completions, cumulative
 };
 
 // Exact fixed-order sums are walked in chunks of kChainSub terms (see
@@ -141,6 +151,7 @@ struct Scenario {
   int32_t* hec;              // [ceil(M/kChainSub)] binade of the running sum at each chunk
                              //   start in the latest exact chain (kNoBinade: unknown)
   long long* hrs;            // [..] helpers: chunk sums of rn(term / ulp) in binade hue
+  SubRec* hlog;              // [kLogCap] substitution records for the helpers
   int32_t* hue;              // [..] helpers: the binade hrs is for, kNoBinade when the
                              //   chunk holds a rounding tie / a huge term / no prediction
   Counters* ctr;

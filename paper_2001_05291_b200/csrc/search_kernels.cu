@@ -63,6 +63,7 @@ struct Shared {
   int xk;                               // ... after this many terms
   unsigned hk;                          // helper jobs posted in this launch
   unsigned hdone;                       // helper completions expected so far
+  unsigned lt, lsync, ldone0;           // substitution log: published, applied, base
   long long red_l[33];
   int red_i[2][33];
   int red2[2][32][2];                   // row-run minima, double-buffered
@@ -237,6 +238,50 @@ __device__ long long block_inclusive_scan(long long x, Shared& sh) {
   for (int k = 0; k < w; ++k) before += sh.red_l[k];
   __syncthreads();
   return before + incl;
+}
+
+// Master, thread 0: publish a substitution record for the helpers' table
+// patches (back-pressure: a full log is drained first).
+__device__ void log_wait(const Scenario& s, Shared& sh, const Smem& sm) {
+  const long long t0 = clock64();
+  const unsigned want = (unsigned)sm.helpers * sh.lt;
+  while ((int)(ld_acquire_u32(&s.hc->log_done) - sh.ldone0 - want) < 0) {
+    if (clock64() - t0 > kSpinLimit) {
+      sh.c.error = 8;
+      break;
+    }
+    __nanosleep(32);
+  }
+  sh.c.cycles[14] += (unsigned long long)(clock64() - t0);
+  sh.lsync = sh.lt;
+}
+
+__device__ void log_append(const Scenario& s, Shared& sh, const Smem& sm, int j, int loser,
+                           int gain, int nl, int ng, double mc_old, double mc_new) {
+  if (sh.lt - sh.lsync >= (unsigned)kLogCap) log_wait(s, sh, sm);
+  SubRec r;
+  r.j = j;
+  r.loser = loser;
+  r.gain = gain;
+  r.nl = nl;
+  r.ng = ng;
+  r.pad = 0;
+  r.mc_old = mc_old;
+  r.mc_new = mc_new;
+  s.hlog[sh.lt % kLogCap] = r;
+  sh.lt += 1;
+  __threadfence();
+  st_release_u64(&s.hc->log_tail, ((unsigned long long)sm.epoch << 32) | sh.lt);
+}
+
+// Block-wide: every published record applied to the table (before any read
+// of rA / rE / rU / rcnt in helper mode). Uniform: sh.lt / sh.lsync are only
+// written by thread 0 before a barrier.
+template <int NT>
+__device__ void table_sync(const Scenario& s, Shared& sh, const Smem& sm) {
+  if (sm.helpers == 0 || sh.lt == sh.lsync) return;
+  if (threadIdx.x == 0) log_wait(s, sh, sm);
+  __syncthreads();
 }
 
 // rn(x / u) for u = 2^(e-52) (an exact power-of-two scaling), with the
@@ -639,7 +684,11 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     s.mem[(long long)gain * s.nwd + wd] |= bit;
   }
   const long long tp0 = ph_now();
-  table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, s.mcp[q], nl, ng);
+  if (sm.helpers > 0) {
+    if (threadIdx.x == 0) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, s.mcp[q]);
+  } else {
+    table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, s.mcp[q], nl, ng);
+  }
   PH_ADD(sh, 10, tp0);
   __syncthreads();
 }
@@ -901,6 +950,7 @@ __device__ void table_row_fresh(const Scenario& s, Shared& sh, double* acc_sum, 
 // row with an unsettled class is rebuilt exactly first.
 template <int NT>
 __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm, int t) {
+  table_sync<NT>(s, sh, sm);
   int amb = 0;
   for (int v = threadIdx.x; v < s.V; v += NT) {
     const uint8_t c = table_class(s, sh, t, v);
@@ -1140,17 +1190,66 @@ __device__ void helper_relocate(const Scenario& s, const Smem& sm, const int32_t
   }
 }
 
-// Helper block main loop: wait for a job of this launch, do its share,
-// count done; return on QUIT (or on the hang guard).
+// Helper share of substitution records [from, to): the bases of slice `part`
+// (thread per base; records in order, each entry patched as in
+// table_after_substitution). Rows of occupied bases are patched too -- they
+// are never read, and a base that empties gets a fresh row.
+template <int NT>
+__device__ void helper_log(const Scenario& s, unsigned from, unsigned to, int part, int parts) {
+  const int per = (s.B + parts - 1) / parts;
+  const int t0 = part * per, t1 = min(s.B, t0 + per);
+  for (int t = t0 + threadIdx.x; t < t1; t += NT) {
+    const bool heli = s.bheli[t];
+    for (unsigned r = from; r < to; ++r) {
+      const SubRec& rec = s.hlog[r % kLogCap];
+      const int j = __ldcg(&rec.j), loser = __ldcg(&rec.loser), gain = __ldcg(&rec.gain);
+      const int nl = __ldcg(&rec.nl), ng = __ldcg(&rec.ng);
+      const double mc_old = __ldcg(&rec.mc_old), mc_new = __ldcg(&rec.mc_new);
+      const bool fl = s.vfixed[loser], fg = s.vfixed[gain];
+      const double c = cost_mb(s, j, t);
+      const long long kl = tix(s, t, loser), kg = tix(s, t, gain);
+      double Al = s.rA[kl], El = s.rE[kl], Ul = s.rU[kl];
+      double Ag = s.rA[kg], Eg = s.rE[kg], Ug = s.rU[kg];
+      int delta = 0;
+      if (!(fl && heli)) delta -= table_unsettled(Al, El, Ul, nl, 0.0);
+      if (!(fg && heli)) delta -= table_unsettled(Ag, Eg, Ug, ng, 0.0);
+      const double dl = c - mc_old, dg = c - mc_new;
+      Al -= dl;
+      El += 2.0 * kTwoPowM52 * (fabs(dl) + fabs(Al));
+      Ul = fmax(0.0, Ul - fabs(dl)) + 2.0 * kTwoPowM52 * Ul;
+      Ag += dg;
+      Eg += 2.0 * kTwoPowM52 * (fabs(dg) + fabs(Ag));
+      Ug = (Ug + fabs(dg)) * (1.0 + 2.0 * kTwoPowM52);
+      if (!(fl && heli)) delta += table_unsettled(Al, El, Ul, nl - 1, 0.0);
+      if (!(fg && heli)) delta += table_unsettled(Ag, Eg, Ug, ng + 1, 0.0);
+      s.rA[kl] = Al;
+      s.rE[kl] = El;
+      s.rU[kl] = Ul;
+      s.rA[kg] = Ag;
+      s.rE[kg] = Eg;
+      s.rU[kg] = Ug;
+      if (delta) s.rcnt[t] += delta;
+    }
+  }
+}
+
+// Helper block main loop: wait for a job of this launch (or new substitution
+// records), do its share, count done; return on QUIT (or on the hang guard).
 template <int NT>
 __device__ void helper_loop(const Scenario& s, Shared& sh, const Smem& sm, const int32_t* pb,
                             int part, int parts) {
-  unsigned seen = 0;
+  unsigned seen = 0, applied = 0;
   while (true) {
     if (threadIdx.x == 0) {
       const long long t0 = clock64();
       int kind = -1;
       while (true) {
+        const unsigned long long lt = ld_acquire_u64(&s.hc->log_tail);
+        if ((unsigned)(lt >> 32) == sm.epoch && (unsigned)lt > applied) {
+          kind = HJOB_LOG;
+          sh.bi[1] = (int)(unsigned)lt;
+          break;
+        }
         const unsigned long long v = ld_acquire_u64(&s.hc->seq);
         if ((unsigned)(v >> 32) == sm.epoch && (unsigned)v > seen) {
           seen = (unsigned)v;
@@ -1172,6 +1271,17 @@ __device__ void helper_loop(const Scenario& s, Shared& sh, const Smem& sm, const
     }
     __syncthreads();
     const int kind = sh.bi[0];
+    if (kind == HJOB_LOG) {
+      const unsigned to = (unsigned)sh.bi[1];
+      helper_log<NT>(s, applied, to, part, parts);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(&s.hc->log_done, to - applied);
+      }
+      applied = to;
+      continue;
+    }
     if (kind == HJOB_RELOCATE)
       helper_relocate<NT>(s, sm, pb, sh.bi[2], sh.bi[3], sh.bi[4], part, parts);
     else if (kind == HJOB_CHAIN)
@@ -1191,6 +1301,7 @@ __device__ void helper_loop(const Scenario& s, Shared& sh, const Smem& sm, const
 template <int NT>
 __device__ void relocate_with_helpers(const Scenario& s, Shared& sh, const Smem& sm, int x, int t,
                                       int pos, int b_old) {
+  table_sync<NT>(s, sh, sm);
   __syncthreads();  // everyone has read the pre-move state
   if (threadIdx.x == 0) {
     s.bveh[b_old] = -1;
@@ -2002,6 +2113,9 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     sh.jexp_max = LLONG_MIN;
     sh.hk = 0;
     sh.hdone = helpers > 0 ? s.hc->done : 0u;
+    sh.lt = 0;
+    sh.lsync = 0;
+    sh.ldone0 = helpers > 0 ? s.hc->log_done : 0u;
   }
   __syncthreads();
   {
@@ -2054,6 +2168,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     long long T = sh.c.tick;  // every thread tracks the tick through row runs
     while (r < M && !sh.c.error) {
       const long long b0 = ph_now();
+      table_sync<NT>(s, sh, sm);  // the eventless test reads rcnt
       if (r < pw || r + NT > pw + 2 * NT) {
         pw = r;
         for (int k = threadIdx.x; k < 2 * NT; k += NT) sm.paw[k] = pw + k < M ? pa[pw + k] : 0;
@@ -2150,6 +2265,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       T = sh.c.tick;
       r += 1;
     }
+    table_sync<NT>(s, sh, sm);  // the next launch starts from a complete table
     // end of pass: run_search's keep_going / max_passes (search.cpp:420-428)
     if (threadIdx.x == 0) {
       sh.c.passes += 1;

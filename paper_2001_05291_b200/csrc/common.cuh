@@ -31,6 +31,8 @@ struct Counters {
   int force_exact;                // test hook: 1 = every total comparison through the exact
                                   // chains, 2 = every unsettled relocation delta exactly
   int chain_mode;                 // 0 = helper-assisted exact chains when possible, 1 = never
+  int hp_valid;                   // chunk boundaries [0, hp_valid] of hP hold the current state's
+                                  //   exact running sums (helper-assisted chains)
   int check_impt;                 // test hook: verify impT against the table every pass
   double total_up;                // rigorous upper bound of the current total
   double final_total;             // exact fixed-order total (written at the end)
@@ -70,6 +72,8 @@ struct HelperCtl {
   int impc_x;        // out: set bits of the mover's new imp row
   int ckind, cj, cmover, ct;  // chain: term kind, mission, mover, base (-1)
   double cnewc;               // chain: the substituted cost (kind 1)
+  int cstart;                 // chain: first chunk
+  int minm;                   // relocation: smallest mission index of the mover
   unsigned long long log_tail;  // (launch << 32) | records published in the launch
   unsigned log_done;            // helper-record completions, cumulative
 };
@@ -152,6 +156,7 @@ struct Scenario {
                              //   start in the latest exact chain (kNoBinade: unknown)
   long long* hrs;            // [..] helpers: chunk sums of rn(term / ulp) in binade hue
   SubRec* hlog;              // [kLogCap] substitution records for the helpers
+  double* hP;                // [nsub+1] exact running sum at each chunk start (current state)
   int32_t* hue;              // [..] helpers: the binade hrs is for, kNoBinade when the
                              //   chunk holds a rounding tie / a huge term / no prediction
   Counters* ctr;

@@ -431,7 +431,8 @@ __device__ void helper_chain(const Scenario& s, Shared& sh, int kind, int j, dou
   const int M = s.M;
   const double* col = t >= 0 ? s.cost + (long long)t * M : nullptr;
   const int nsub = (M + kChainSub - 1) / kChainSub;
-  for (int c = part; c < nsub; c += parts) {
+  const int c0 = __ldcg(&s.hc->cstart);
+  for (int c = c0 + part; c < nsub; c += parts) {
     const int e = __ldcg(&s.hec[c]);
     if (e == kNoBinade) {
       if (threadIdx.x == 0) s.hue[c] = kNoBinade;
@@ -480,7 +481,7 @@ __device__ void helper_chain(const Scenario& s, Shared& sh, int kind, int j, dou
 // and runs chain_steps on every other chunk. Block-wide.
 template <int NT>
 __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& sm, int kind,
-                                     int j, double newc, int mover, int t) {
+                                     int j, double newc, int mover, int t, int c0, bool record) {
   constexpr long long LIM = 1ll << 53;
   const int M = s.M;
   const double* col = t >= 0 ? s.cost + (long long)t * M : nullptr;
@@ -492,12 +493,15 @@ __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& 
     hc->cmover = mover;
     hc->ct = t;
     hc->cnewc = newc;
+    hc->cstart = c0;
     post_job(s, sh, sm, HJOB_CHAIN, 0, 0, 0);
   }
   wait_helpers<NT>(s, sh, sm);
+  // the chain is the current state's up to chunk c0: start from its
+  // recorded exact running sum there
   if (threadIdx.x == 0) {
-    sh.xs = 0.0;
-    sh.xk = 0;
+    sh.xs = c0 > 0 ? s.hP[c0] : 0.0;
+    sh.xk = c0 * kChainSub;
   }
   __syncthreads();
   const int nsub = (M + kChainSub - 1) / kChainSub;
@@ -506,6 +510,7 @@ __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& 
     const double S = sh.xs;
     if (k >= M || sh.c.error) break;
     if (k % kChainSub != 0 || !(S >= 0x1p-900)) {
+      if (record && k % kChainSub == 0 && threadIdx.x == 0) s.hP[k / kChainSub] = S;
       chain_steps<NT>(s, sh, kind, j, newc, mover, col, min(M, (k / kChainSub + 1) * kChainSub));
       continue;
     }
@@ -521,13 +526,20 @@ __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& 
     const bool good = ok && N + incl < LIM;
     const int bad = block_min<NT>(good ? INT_MAX : (int)threadIdx.x, sh);
     const int nok = bad == INT_MAX ? NT : bad;
+    if (record && (int)threadIdx.x < nok) s.hP[cc] = (double)(N + incl - v) * u;
     if (nok > 0 && (int)threadIdx.x == nok - 1) {
       sh.xs = (double)(N + incl) * u;
       sh.xk = min(M, (c + nok) * kChainSub);
     }
     __syncthreads();
-    if (nok < NT && sh.xk < M)
+    if (nok < NT && sh.xk < M) {
+      if (record && threadIdx.x == 0) s.hP[sh.xk / kChainSub] = sh.xs;
       chain_steps<NT>(s, sh, kind, j, newc, mover, col, min(M, (c + nok + 1) * kChainSub));
+    }
+  }
+  if (record && threadIdx.x == 0 && !sh.c.error) {
+    s.hP[nsub] = sh.xs;  // (a start at c0 = nsub returns the total itself)
+    sh.c.hp_valid = nsub;
   }
   const double r = sh.xs;
   __syncthreads();
@@ -535,11 +547,15 @@ __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& 
 }
 
 // Exact chain, with the helpers when there are any and M is large.
+// c0: first chunk whose terms may differ from the current state's (the chain
+// resumes from hP[c0] when helper-assisted); record: the chain is the
+// current state's (kind 0) and refreshes hP.
 template <int NT>
 __device__ double exact_chain_any(const Scenario& s, Shared& sh, const Smem& sm, int kind, int j,
-                                  double newc, int mover, int t) {
+                                  double newc, int mover, int t, int c0, bool record) {
   if (sm.helpers > 0 && s.M >= 8 * kChainSub && sh.c.chain_mode == 0)
-    return exact_chain_helped<NT>(s, sh, sm, kind, j, newc, mover, t);
+    return exact_chain_helped<NT>(s, sh, sm, kind, j, newc, mover, t, min(c0, sh.c.hp_valid),
+                                  record);
   return exact_chain<NT>(s, sh, kind, j, newc, mover,
                          t >= 0 ? s.cost + (long long)t * s.M : nullptr);
 }
@@ -549,7 +565,7 @@ template <int NT>
 __device__ double exact_total(const Scenario& s, Shared& sh, const Smem& sm) {
   if (sh.c.total_ver == (long long)sh.c.applied) return sh.c.total_exact;
   const long long e0 = ph_now();
-  const double t = exact_chain_any<NT>(s, sh, sm, 0, -1, 0.0, -1, -1);
+  const double t = exact_chain_any<NT>(s, sh, sm, 0, -1, 0.0, -1, -1, INT_MAX, true);
   PH_ADD(sh, 9, e0);
   if (threadIdx.x == 0) {
     sh.c.total_exact = t;
@@ -1062,6 +1078,7 @@ __device__ void helper_relocate(const Scenario& s, const Smem& sm, const int32_t
   double* st = sm.stage + w * 32;
   int* list = sm.xidx;  // [2*NT]
   int* cnt = sm.wsum;
+  int my_min = INT_MAX;  // smallest mission index of the mover seen by this thread
   for (int v = l; v < V; v += 32) {
     as[v] = 0.0;
     aa[v] = 0.0;
@@ -1086,6 +1103,7 @@ __device__ void helper_relocate(const Scenario& s, const Smem& sm, const int32_t
         s.mc[m] = c;
         s.mcp[s.invb[m]] = c;
         list[atomicAdd(cnt, 1)] = m;
+        my_min = min(my_min, m);
       }
       term = colo[m] - c;
     }
@@ -1175,6 +1193,8 @@ __device__ void helper_relocate(const Scenario& s, const Smem& sm, const int32_t
     }
   }
   if (l == 0 && cb) atomicAdd(&s.hc->impc_x, cb);
+  my_min = __reduce_min_sync(FULL, my_min);
+  if (l == 0 && my_min != INT_MAX) atomicMin(&s.hc->minm, my_min);
   __syncthreads();
   for (int v = threadIdx.x; v < V; v += NT) {
     double sum = 0.0, abs = 0.0;
@@ -1310,6 +1330,7 @@ __device__ void relocate_with_helpers(const Scenario& s, Shared& sh, const Smem&
     sm.gvbase[x] = t;
     s.pkind[pos] = POOL_EMPTY;
     s.pidx[pos] = b_old;
+    s.hc->minm = INT_MAX;
     post_job(s, sh, sm, HJOB_RELOCATE, x, t, b_old);
   }
   // meanwhile every other empty row shifts by -D(t, x)
@@ -1353,6 +1374,8 @@ __device__ void relocate_with_helpers(const Scenario& s, Shared& sh, const Smem&
     s.rcnt[b_old] = sh.tmp;
     sm.impc[x] = __ldcg(&s.hc->impc_x);
     s.hc->impc_x = 0;
+    // the chain's terms changed from the mover's first mission on
+    sh.c.hp_valid = min(sh.c.hp_valid, __ldcg(&s.hc->minm) / kChainSub);
   }
   __syncthreads();
 }
@@ -1455,7 +1478,7 @@ __device__ bool exact_accept_single(const Scenario& s, Shared& sh, const Smem& s
   const long long f0 = ph_now();
   const double S = exact_total<NT>(s, sh, sm);
   const long long c0 = ph_now();
-  const double S2 = exact_chain_any<NT>(s, sh, sm, 1, j, newc, -1, -1);
+  const double S2 = exact_chain_any<NT>(s, sh, sm, 1, j, newc, -1, -1, j / kChainSub, false);
   PH_ADD(sh, 13, c0);
   if (threadIdx.x == 0) {
     sh.c.fallbacks += 1;
@@ -1489,6 +1512,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         __syncthreads();  // everyone has read the pre-move state
         if (threadIdx.x == 0) {
           apply_takeover(s, sh, sm, j, g, i);
+          sh.c.hp_valid = min(sh.c.hp_valid, j / kChainSub);
           sh.c.applied += 1;
           sh.c.pass_applied += 1;
           if (acc == 3) {
@@ -1527,7 +1551,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         if (neg) {
           const double S = exact_total<NT>(s, sh, sm);
           const long long c0 = ph_now();
-          after = exact_chain_any<NT>(s, sh, sm, 2, -1, 0.0, mover, t);
+          after = exact_chain_any<NT>(s, sh, sm, 2, -1, 0.0, mover, t, 0, false);
           PH_ADD(sh, 13, c0);
           acc = after < S;
           exact_known = true;
@@ -1544,6 +1568,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         } else {
           const long long a0 = ph_now();
           apply_relocate<NT>(s, sh, mover, t, i);
+          if (threadIdx.x == 0) sh.c.hp_valid = 0;
           PH_ADD(sh, 8, a0);
           const long long a1 = ph_now();
           bits_after_relocation<NT>(s, sh, sm, mover, sm.xlist, sm.xlist_cap);
@@ -1587,6 +1612,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           __syncthreads();
           if (threadIdx.x == 0) {
             apply_reassign(s, sh, sm, j, g);
+            sh.c.hp_valid = min(sh.c.hp_valid, j / kChainSub);
             sh.c.applied += 1;
             sh.c.pass_applied += 1;
             if (acc == 3) {

@@ -321,7 +321,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 struct Layout {
   size_t ro, vfixed, bheli, vrk, brk, mv, mc, vbase, vcount, bveh, pkind, pidx, mvp, mcp, rop,
       invb, exp_take, exp_reas, exp_rel, role_rel, rA, rE, rU, rcnt, imp, mem, scratch, hc, hdelta,
-      hsum, habs, hec, hrs, hue, impT, vseg, vcur, vch, hlog, hP, cost, totalA, totalB;
+      hsum, habs, hec, hrs, hue, impT, vseg, vcur, vch, hlog, hP, hP2, cost, totalA, totalB;
 };
 
 // Per-scenario layout in two regions: A holds what the host initialises
@@ -383,6 +383,7 @@ Layout layout(int M, int B, int V, int K, int cap, bool own_cost) {
   L.vch = putB(12ull * ((size_t)M / fpk::kRowsChunk + V + 1));
   L.hlog = putB(sizeof(fpk::SubRec) * fpk::kLogCap);
   L.hP = putB(8ull * (nsub + 1));
+  L.hP2 = putB(8ull * (nsub + 1));
   L.totalA = a;
   L.totalB = b;
   return L;
@@ -644,6 +645,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.vch = reinterpret_cast<int32_t*>(dw + L.vch);
     S.hlog = reinterpret_cast<fpk::SubRec*>(dw + L.hlog);
     S.hP = reinterpret_cast<double*>(dw + L.hP);
+    S.hP2 = reinterpret_cast<double*>(dw + L.hP2);
     S.nvw = (V + 31) / 32;
     {
       const size_t nsub = ((size_t)M + fpk::kChainSub - 1) / fpk::kChainSub + 1;

@@ -157,6 +157,7 @@ struct Scenario {
   long long* hrs;            // [..] helpers: chunk sums of rn(term / ulp) in binade hue
   SubRec* hlog;              // [kLogCap] substitution records for the helpers
   double* hP;                // [nsub+1] exact running sum at each chunk start (current state)
+  double* hP2;               // [nsub+1] the same for the last candidate chain (adopted if accepted)
   int32_t* hue;              // [..] helpers: the binade hrs is for, kNoBinade when the
                              //   chunk holds a rounding tie / a huge term / no prediction
   Counters* ctr;

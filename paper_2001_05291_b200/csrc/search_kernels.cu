@@ -64,6 +64,7 @@ struct Shared {
   unsigned hk;                          // helper jobs posted in this launch
   unsigned hdone;                       // helper completions expected so far
   unsigned lt, lsync, ldone0;           // substitution log: published, applied, base
+  int hp2_from;                         // hP2 holds the last candidate chain from this chunk (-1: none)
   long long red_l[33];
   int red_i[2][33];
   int red2[2][32][2];                   // row-run minima, double-buffered
@@ -481,7 +482,9 @@ __device__ void helper_chain(const Scenario& s, Shared& sh, int kind, int j, dou
 // and runs chain_steps on every other chunk. Block-wide.
 template <int NT>
 __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& sm, int kind,
-                                     int j, double newc, int mover, int t, int c0, bool record) {
+                                     int j, double newc, int mover, int t, int c0, int rec) {
+  double* const hp = rec == 1 ? s.hP : s.hP2;
+  const bool record = rec != 0;
   constexpr long long LIM = 1ll << 53;
   const int M = s.M;
   const double* col = t >= 0 ? s.cost + (long long)t * M : nullptr;
@@ -510,7 +513,7 @@ __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& 
     const double S = sh.xs;
     if (k >= M || sh.c.error) break;
     if (k % kChainSub != 0 || !(S >= 0x1p-900)) {
-      if (record && k % kChainSub == 0 && threadIdx.x == 0) s.hP[k / kChainSub] = S;
+      if (record && k % kChainSub == 0 && threadIdx.x == 0) hp[k / kChainSub] = S;
       chain_steps<NT>(s, sh, kind, j, newc, mover, col, min(M, (k / kChainSub + 1) * kChainSub));
       continue;
     }
@@ -526,20 +529,21 @@ __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& 
     const bool good = ok && N + incl < LIM;
     const int bad = block_min<NT>(good ? INT_MAX : (int)threadIdx.x, sh);
     const int nok = bad == INT_MAX ? NT : bad;
-    if (record && (int)threadIdx.x < nok) s.hP[cc] = (double)(N + incl - v) * u;
+    if (record && (int)threadIdx.x < nok) hp[cc] = (double)(N + incl - v) * u;
     if (nok > 0 && (int)threadIdx.x == nok - 1) {
       sh.xs = (double)(N + incl) * u;
       sh.xk = min(M, (c + nok) * kChainSub);
     }
     __syncthreads();
     if (nok < NT && sh.xk < M) {
-      if (record && threadIdx.x == 0) s.hP[sh.xk / kChainSub] = sh.xs;
+      if (record && threadIdx.x == 0) hp[sh.xk / kChainSub] = sh.xs;
       chain_steps<NT>(s, sh, kind, j, newc, mover, col, min(M, (c + nok + 1) * kChainSub));
     }
   }
   if (record && threadIdx.x == 0 && !sh.c.error) {
-    s.hP[nsub] = sh.xs;  // (a start at c0 = nsub returns the total itself)
-    sh.c.hp_valid = nsub;
+    hp[nsub] = sh.xs;  // (a start at c0 = nsub returns the total itself)
+    if (rec == 1) sh.c.hp_valid = nsub;
+    else sh.hp2_from = c0;
   }
   const double r = sh.xs;
   __syncthreads();
@@ -548,16 +552,34 @@ __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& 
 
 // Exact chain, with the helpers when there are any and M is large.
 // c0: first chunk whose terms may differ from the current state's (the chain
-// resumes from hP[c0] when helper-assisted); record: the chain is the
-// current state's (kind 0) and refreshes hP.
+// resumes from hP[c0] when helper-assisted); rec: 1 = the chain is the
+// current state's (kind 0) and refreshes hP, 2 = a candidate's, recorded in
+// hP2 (adopt_candidate_sums makes it current when the move is applied).
 template <int NT>
 __device__ double exact_chain_any(const Scenario& s, Shared& sh, const Smem& sm, int kind, int j,
-                                  double newc, int mover, int t, int c0, bool record) {
+                                  double newc, int mover, int t, int c0, int rec) {
+  if (threadIdx.x == 0 && rec == 2) sh.hp2_from = -1;
   if (sm.helpers > 0 && s.M >= 8 * kChainSub && sh.c.chain_mode == 0)
     return exact_chain_helped<NT>(s, sh, sm, kind, j, newc, mover, t, min(c0, sh.c.hp_valid),
-                                  record);
+                                  rec);
   return exact_chain<NT>(s, sh, kind, j, newc, mover,
                          t >= 0 ? s.cost + (long long)t * s.M : nullptr);
+}
+
+// The applied move is the last candidate chain's state: its recorded running
+// sums become the current ones. Block-wide.
+template <int NT>
+__device__ void adopt_candidate_sums(const Scenario& s, Shared& sh) {
+  const int from = sh.hp2_from;
+  if (from < 0) return;
+  const int nsub = (s.M + kChainSub - 1) / kChainSub;
+  for (int c = from + threadIdx.x; c <= nsub; c += NT) s.hP[c] = s.hP2[c];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sh.c.hp_valid = nsub;
+    sh.hp2_from = -1;
+  }
+  __syncthreads();
 }
 
 // Exact current total, cached per applied-move count.
@@ -565,7 +587,7 @@ template <int NT>
 __device__ double exact_total(const Scenario& s, Shared& sh, const Smem& sm) {
   if (sh.c.total_ver == (long long)sh.c.applied) return sh.c.total_exact;
   const long long e0 = ph_now();
-  const double t = exact_chain_any<NT>(s, sh, sm, 0, -1, 0.0, -1, -1, INT_MAX, true);
+  const double t = exact_chain_any<NT>(s, sh, sm, 0, -1, 0.0, -1, -1, INT_MAX, 1);
   PH_ADD(sh, 9, e0);
   if (threadIdx.x == 0) {
     sh.c.total_exact = t;
@@ -1478,7 +1500,7 @@ __device__ bool exact_accept_single(const Scenario& s, Shared& sh, const Smem& s
   const long long f0 = ph_now();
   const double S = exact_total<NT>(s, sh, sm);
   const long long c0 = ph_now();
-  const double S2 = exact_chain_any<NT>(s, sh, sm, 1, j, newc, -1, -1, j / kChainSub, false);
+  const double S2 = exact_chain_any<NT>(s, sh, sm, 1, j, newc, -1, -1, j / kChainSub, 2);
   PH_ADD(sh, 13, c0);
   if (threadIdx.x == 0) {
     sh.c.fallbacks += 1;
@@ -1525,6 +1547,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         __syncthreads();
         const long long a2 = ph_now();
         bits_after_substitution<NT>(s, sh, sm, q, j, loser, g, mcj, nl, ng);
+        if (acc == 3) adopt_candidate_sums<NT>(s, sh);
         PH_ADD(sh, 7, a2);
       }
     }
@@ -1551,7 +1574,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         if (neg) {
           const double S = exact_total<NT>(s, sh, sm);
           const long long c0 = ph_now();
-          after = exact_chain_any<NT>(s, sh, sm, 2, -1, 0.0, mover, t, 0, false);
+          after = exact_chain_any<NT>(s, sh, sm, 2, -1, 0.0, mover, t, 0, 2);
           PH_ADD(sh, 13, c0);
           acc = after < S;
           exact_known = true;
@@ -1595,6 +1618,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           if (debug) debug_check(s, sh);
         }
         __syncthreads();
+        if (exact_known) adopt_candidate_sums<NT>(s, sh);
       }
     }
   }
@@ -1625,6 +1649,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           __syncthreads();
           const long long a2 = ph_now();
           bits_after_substitution<NT>(s, sh, sm, q, j, l, g, mcj, nl, ng);
+          if (acc == 3) adopt_candidate_sums<NT>(s, sh);
           PH_ADD(sh, 7, a2);
         }
       }
@@ -2141,6 +2166,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     sh.hdone = helpers > 0 ? s.hc->done : 0u;
     sh.lt = 0;
     sh.lsync = 0;
+    sh.hp2_from = -1;
     sh.ldone0 = helpers > 0 ? s.hc->log_done : 0u;
   }
   __syncthreads();

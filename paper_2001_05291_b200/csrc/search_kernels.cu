@@ -278,9 +278,9 @@ __device__ void log_append(const Scenario& s, Shared& sh, const Smem& sm, int j,
 // Block-wide: every published record applied to the table (before any read
 // of rA / rE / rU / rcnt in helper mode). Uniform: sh.lt / sh.lsync are only
 // written by thread 0 before a barrier.
-template <int NT>
+template <int NT, bool HELP>
 __device__ void table_sync(const Scenario& s, Shared& sh, const Smem& sm) {
-  if (sm.helpers == 0 || sh.lt == sh.lsync) return;
+  if (!HELP || sm.helpers == 0 || sh.lt == sh.lsync) return;
   if (threadIdx.x == 0) log_wait(s, sh, sm);
   __syncthreads();
 }
@@ -555,11 +555,11 @@ __device__ double exact_chain_helped(const Scenario& s, Shared& sh, const Smem& 
 // resumes from hP[c0] when helper-assisted); rec: 1 = the chain is the
 // current state's (kind 0) and refreshes hP, 2 = a candidate's, recorded in
 // hP2 (adopt_candidate_sums makes it current when the move is applied).
-template <int NT>
+template <int NT, bool HELP>
 __device__ double exact_chain_any(const Scenario& s, Shared& sh, const Smem& sm, int kind, int j,
                                   double newc, int mover, int t, int c0, int rec) {
   if (threadIdx.x == 0 && rec == 2) sh.hp2_from = -1;
-  if (sm.helpers > 0 && s.M >= 8 * kChainSub && sh.c.chain_mode == 0)
+  if (HELP && sm.helpers > 0 && s.M >= 8 * kChainSub && sh.c.chain_mode == 0)
     return exact_chain_helped<NT>(s, sh, sm, kind, j, newc, mover, t, min(c0, sh.c.hp_valid),
                                   rec);
   return exact_chain<NT>(s, sh, kind, j, newc, mover,
@@ -583,11 +583,11 @@ __device__ void adopt_candidate_sums(const Scenario& s, Shared& sh) {
 }
 
 // Exact current total, cached per applied-move count.
-template <int NT>
+template <int NT, bool HELP>
 __device__ double exact_total(const Scenario& s, Shared& sh, const Smem& sm) {
   if (sh.c.total_ver == (long long)sh.c.applied) return sh.c.total_exact;
   const long long e0 = ph_now();
-  const double t = exact_chain_any<NT>(s, sh, sm, 0, -1, 0.0, -1, -1, INT_MAX, 1);
+  const double t = exact_chain_any<NT, HELP>(s, sh, sm, 0, -1, 0.0, -1, -1, INT_MAX, 1);
   PH_ADD(sh, 9, e0);
   if (threadIdx.x == 0) {
     sh.c.total_exact = t;
@@ -697,7 +697,7 @@ __device__ void table_after_substitution(const Scenario& s, const Shared& sh, in
 // to `gain` (new cost in mcp[q], ng missions): refresh bit q of every imp
 // row, move its mem bit, and patch the relocation-delta table, in one
 // block-wide phase with a single barrier.
-template <int NT>
+template <int NT, bool HELP>
 __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Smem& sm, int q,
                                         int j, int loser, int gain, double mc_old, int nl,
                                         int ng) {
@@ -722,7 +722,7 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     s.mem[(long long)gain * s.nwd + wd] |= bit;
   }
   const long long tp0 = ph_now();
-  if (sm.helpers > 0) {
+  if (HELP && sm.helpers > 0) {
     if (threadIdx.x == 0) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, s.mcp[q]);
   } else {
     table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, s.mcp[q], nl, ng);
@@ -986,9 +986,9 @@ __device__ void table_row_fresh(const Scenario& s, Shared& sh, double* acc_sum, 
 
 // Relocation classes of every vehicle towards empty base t into sm.cls; a
 // row with an unsettled class is rebuilt exactly first.
-template <int NT>
+template <int NT, bool HELP>
 __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm, int t) {
-  table_sync<NT>(s, sh, sm);
+  table_sync<NT, HELP>(s, sh, sm);
   int amb = 0;
   for (int v = threadIdx.x; v < s.V; v += NT) {
     const uint8_t c = table_class(s, sh, t, v);
@@ -1343,7 +1343,7 @@ __device__ void helper_loop(const Scenario& s, Shared& sh, const Smem& sm, const
 template <int NT>
 __device__ void relocate_with_helpers(const Scenario& s, Shared& sh, const Smem& sm, int x, int t,
                                       int pos, int b_old) {
-  table_sync<NT>(s, sh, sm);
+  table_sync<NT, true>(s, sh, sm);
   __syncthreads();  // everyone has read the pre-move state
   if (threadIdx.x == 0) {
     s.bveh[b_old] = -1;
@@ -1494,13 +1494,13 @@ __device__ void debug_check(const Scenario& s, Shared& sh) {
 // Exact accept of a single-substitution candidate (takeover/reassign):
 // candidate_total < total, both fixed-order fp64 sums. Block-wide; the new
 // exact total is cached when the move is accepted.
-template <int NT>
+template <int NT, bool HELP>
 __device__ bool exact_accept_single(const Scenario& s, Shared& sh, const Smem& sm, int j,
                                     double newc) {
   const long long f0 = ph_now();
-  const double S = exact_total<NT>(s, sh, sm);
+  const double S = exact_total<NT, HELP>(s, sh, sm);
   const long long c0 = ph_now();
-  const double S2 = exact_chain_any<NT>(s, sh, sm, 1, j, newc, -1, -1, j / kChainSub, 2);
+  const double S2 = exact_chain_any<NT, HELP>(s, sh, sm, 1, j, newc, -1, -1, j / kChainSub, 2);
   PH_ADD(sh, 13, c0);
   if (threadIdx.x == 0) {
     sh.c.fallbacks += 1;
@@ -1515,7 +1515,7 @@ __device__ bool exact_accept_single(const Scenario& s, Shared& sh, const Smem& s
 // 333-341). Block-cooperative; every thread screens each move redundantly
 // from the (block-uniform) state, so barriers are only needed around state
 // changes and exact sums. Returns with the block synchronised.
-template <int NT>
+template <int NT, bool HELP>
 __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int i, int q,
                              bool tabu, long long tenure, bool debug) {
   const int j = sm.pb[q];
@@ -1527,7 +1527,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
     const double mcj = s.mc[j];
     if (compat_vm(s.vfixed[g], s.ro[j]) && newc - mcj < 0.0) {
       int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
-      if (!acc) acc = exact_accept_single<NT>(s, sh, sm, j, newc) ? 3 : 0;
+      if (!acc) acc = exact_accept_single<NT, HELP>(s, sh, sm, j, newc) ? 3 : 0;
       if (acc) {
         const int loser = s.mv[j];
         const int nl = s.vcount[loser], ng = s.vcount[g];
@@ -1546,8 +1546,8 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         }
         __syncthreads();
         const long long a2 = ph_now();
-        bits_after_substitution<NT>(s, sh, sm, q, j, loser, g, mcj, nl, ng);
-        if (acc == 3) adopt_candidate_sums<NT>(s, sh);
+        bits_after_substitution<NT, HELP>(s, sh, sm, q, j, loser, g, mcj, nl, ng);
+        if (HELP && acc == 3) adopt_candidate_sums<NT>(s, sh);
         PH_ADD(sh, 7, a2);
       }
     }
@@ -1557,7 +1557,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
     const int t = s.pidx[i];
     const int mover = s.mv[j];
     if (!(s.vfixed[mover] && s.bheli[t])) {
-      relocation_classes<NT>(s, sh, sm, t);
+      relocation_classes<NT, HELP>(s, sh, sm, t);
       const uint8_t cls = sm.cls[mover];
       bool acc = cls == CLS_ACC;
       bool exact_known = false;
@@ -1572,9 +1572,9 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           PH_ADD(sh, 12, q0);
         }
         if (neg) {
-          const double S = exact_total<NT>(s, sh, sm);
+          const double S = exact_total<NT, HELP>(s, sh, sm);
           const long long c0 = ph_now();
-          after = exact_chain_any<NT>(s, sh, sm, 2, -1, 0.0, mover, t, 0, 2);
+          after = exact_chain_any<NT, HELP>(s, sh, sm, 2, -1, 0.0, mover, t, 0, 2);
           PH_ADD(sh, 13, c0);
           acc = after < S;
           exact_known = true;
@@ -1584,7 +1584,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       }
       if (acc) {
         const int b_old = s.vbase[mover];
-        if (sm.helpers > 0) {
+        if (HELP && sm.helpers > 0) {
           const long long a1 = ph_now();
           relocate_with_helpers<NT>(s, sh, sm, mover, t, i, b_old);
           PH_ADD(sh, 6, a1);
@@ -1618,7 +1618,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           if (debug) debug_check(s, sh);
         }
         __syncthreads();
-        if (exact_known) adopt_candidate_sums<NT>(s, sh);
+        if (HELP && exact_known) adopt_candidate_sums<NT>(s, sh);
       }
     }
   }
@@ -1630,7 +1630,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
       const double mcj = s.mc[j];
       if (newc - mcj < 0.0) {
         int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
-        if (!acc) acc = exact_accept_single<NT>(s, sh, sm, j, newc) ? 3 : 0;
+        if (!acc) acc = exact_accept_single<NT, HELP>(s, sh, sm, j, newc) ? 3 : 0;
         if (acc) {
           const int nl = s.vcount[l], ng = s.vcount[g];
           __syncthreads();
@@ -1648,8 +1648,8 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           }
           __syncthreads();
           const long long a2 = ph_now();
-          bits_after_substitution<NT>(s, sh, sm, q, j, l, g, mcj, nl, ng);
-          if (acc == 3) adopt_candidate_sums<NT>(s, sh);
+          bits_after_substitution<NT, HELP>(s, sh, sm, q, j, l, g, mcj, nl, ng);
+          if (HELP && acc == 3) adopt_candidate_sums<NT>(s, sh);
           PH_ADD(sh, 7, a2);
         }
       }
@@ -1663,7 +1663,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
 }
 
 // Row context after any state change (thread 0 writes, all read after sync).
-template <int NT>
+template <int NT, bool HELP>
 __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int i, bool tabu) {
   if (threadIdx.x == 0) {
     sh.c.counts[2] += 1;
@@ -1737,7 +1737,7 @@ __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int 
     sh.nj = 0;
   }
   const int t = sh.rel_t;
-  if (t >= 0) relocation_classes<NT>(s, sh, sm, t);
+  if (t >= 0) relocation_classes<NT, HELP>(s, sh, sm, t);
   __syncthreads();
 }
 
@@ -1751,7 +1751,7 @@ __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int 
 // is the first set bit of outer | (candidates & ~blocked); the positions
 // before it are either inner-blocked (tick + skip) or evaluated (3
 // evaluations each), counted with popc.
-template <int NT>
+template <int NT, bool HELP>
 __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bool tabu,
                         long long tenure, bool debug) {
   constexpr int NW = NT / 32;
@@ -1762,7 +1762,7 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
   if (threadIdx.x == 0) sh.c.counts[0] += 1;
   while (p < M) {
     const long long c0 = ph_now();
-    make_context<NT>(s, sh, sm, i, tabu);
+    make_context<NT, HELP>(s, sh, sm, i, tabu);
     PH_ADD(sh, 1, c0);
     const long long c1 = ph_now();
     const int p_seg = p;
@@ -1886,7 +1886,7 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
       return;
     }
     const long long c2 = ph_now();
-    process_pair<NT>(s, sh, sm, i, p, tabu, tenure, debug);
+    process_pair<NT, HELP>(s, sh, sm, i, p, tabu, tenure, debug);
     PH_ADD(sh, 3, c2);
     if (sh.c.error) return;
     p += 1;
@@ -2049,7 +2049,7 @@ size_t pass_smem_state(int V, int B, int K) {
 // INK: the block rebuilds its own mirrors / bitsets between passes (a
 // separate instantiation, so the grid-wide-sweep variant carries none of
 // that code's registers).
-template <int NT, bool INK>
+template <int NT, bool INK, bool HELP>
 __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
                 int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
@@ -2096,7 +2096,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   sm.gvbase = g.vbase;
   sm.gmv = nullptr;
   sm.gmvp = nullptr;
-  if (helpers > 0 && blockIdx.x > 0) {
+  if (HELP && helpers > 0 && blockIdx.x > 0) {
     helper_loop<NT>(g, sh, sm, perms + s.M, blockIdx.x - 1, helpers);
     return;
   }
@@ -2220,7 +2220,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     long long T = sh.c.tick;  // every thread tracks the tick through row runs
     while (r < M && !sh.c.error) {
       const long long b0 = ph_now();
-      table_sync<NT>(s, sh, sm);  // the eventless test reads rcnt
+      table_sync<NT, HELP>(s, sh, sm);  // the eventless test reads rcnt
       if (r < pw || r + NT > pw + 2 * NT) {
         pw = r;
         for (int k = threadIdx.x; k < 2 * NT; k += NT) sm.paw[k] = pw + k < M ? pa[pw + k] : 0;
@@ -2312,12 +2312,12 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
         if (nskip > 0) continue;
       }
       __syncthreads();  // thread 0's counter updates before run_row reads them
-      run_row<NT>(s, sh, sm, sm.paw[r - pw], tabu, tenure, debug);
+      run_row<NT, HELP>(s, sh, sm, sm.paw[r - pw], tabu, tenure, debug);
       __syncthreads();
       T = sh.c.tick;
       r += 1;
     }
-    table_sync<NT>(s, sh, sm);  // the next launch starts from a complete table
+    table_sync<NT, HELP>(s, sh, sm);  // the next launch starts from a complete table
     // end of pass: run_search's keep_going / max_passes (search.cpp:420-428)
     if (threadIdx.x == 0) {
       sh.c.passes += 1;
@@ -2610,7 +2610,11 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
     mirrors_smem = mirrors_smem && std::atoi(e) != 0;
   const size_t smem = core + (in_smem ? state : 0) + (bits_smem ? bits : 0) +
                       (mirrors_smem ? mirrors : 0);
-  auto kern = inkernel ? pass_kernel<NT, true> : pass_kernel<NT, false>;
+  // HELP: the variant that can share work with helper blocks (large single
+  // scenarios); the others compile none of that code
+  const bool help_possible = helpers_req != 0 && n_scn == 1 && kpasses == 1 && !inkernel && !bits_smem;
+  auto kern = inkernel ? pass_kernel<NT, true, false>
+                       : (help_possible ? pass_kernel<NT, false, true> : pass_kernel<NT, false, false>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // helper blocks: one scenario, one pass per launch, bitsets in global
   // memory, and every block co-resident (cooperative launch)

@@ -2633,8 +2633,14 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
     void* args[] = {&d_scs, &d_active, &d_perms, &kpasses, &ip, &max_passes, &t, &tenure, &d,
                     (void*)&in_smem, (void*)&bits_smem, (void*)&mirrors_smem, &helpers, &epoch,
                     (void*)&perm_bad};
-    return cudaLaunchCooperativeKernel((const void*)kern, dim3(1 + helpers), dim3(NT),
-                                       args, smem, stream);
+    const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(1 + helpers),
+                                                      dim3(NT), args, smem, stream);
+    if (e == cudaSuccess) return e;
+    // the blocks could not all be resident (another tenant, MPS limits): the
+    // same pass without helpers, which is only an execution strategy
+    cudaGetLastError();
+    kern = pass_kernel<NT, false, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   kern<<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
                                                max_passes, tabu, tenure, debug, in_smem,

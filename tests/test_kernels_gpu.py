@@ -305,3 +305,23 @@ def test_device_permutation_rejection_fallback(monkeypatch):
     for a, b in zip(base, forced):
         assert _stats_key(a) == _stats_key(b)
         assert np.array_equal(a.mission_vehicle, b.mission_vehicle)
+
+
+def test_table_upload_into_a_live_context():
+    """DistanceTable.upload (fp_table_upload into an existing context, as the
+    bench's e2e leg and a long-lived solver use it) replaces the table and the
+    context's row-major copy: a search after re-uploading another instance's
+    table equals a search on a fresh context."""
+    a = F.survey_instance(200, 5000, 20, seed=1)
+    b = F.survey_instance(200, 5000, 20, seed=2)
+    ta, tb = F.build_distance_table(a), F.build_distance_table(b)
+    sb = F.rank_bases(b, tb)
+    vb, mv, pk, px = F._state_arrays(sb.assignment, F.initial_pool(sb, b), b)
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=3)
+    want = F.search_arrays(b, tb, cfg, vb, mv, pk, px)
+    F.search_arrays(a, ta, cfg, *F._state_arrays(F.rank_bases(a, ta).assignment,
+                                                   F.initial_pool(F.rank_bases(a, ta), a), a))
+    ta.upload(np.asarray(tb.cost))
+    got = F.search_arrays(b, ta, cfg, vb, mv, pk, px)
+    assert _stats_key(got) == _stats_key(want)
+    assert np.array_equal(got.mission_vehicle, want.mission_vehicle)

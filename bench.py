@@ -180,6 +180,10 @@ def run_ours(args) -> None:
         "search_stats": {k: getattr(st, k) for k in ("passes", "evaluations", "applied_moves",
                                                        "tabu_skips_outer", "tabu_skips_inner",
                                                        "final_objective_km", "exact_fallbacks")},
+        # SURVEY.md §8(d) coverage / distance: missions served by a compatible
+        # placed vehicle (must be M) and the distance of the final assignment
+        "coverage": _coverage(inst, results[0]), "missions": inst.n_missions,
+        "distance_km": st.final_objective_km,
         "phase_ms": dict(zip(("row_runs", "row_context", "scan_steps", "event_pairs",
                               "exact_fallbacks", "table_row_rebuilds", "reloc_bits", "subst_bits",
                               "reloc_apply", "exact_totals", "table_patches", "pass_setup",
@@ -207,6 +211,20 @@ def run_ours(args) -> None:
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def _coverage(inst, r) -> int:
+    """Missions served by a placed, compatible vehicle (no fixed wing on a
+    rotary-only mission, no fixed wing on a helipad)."""
+    mv = np.asarray(r.mission_vehicle)
+    vb = np.asarray(r.vehicle_base)
+    ok = mv >= 0
+    v = np.where(ok, mv, 0)
+    placed = vb[v] >= 0
+    fixed = inst.vehicle_kind[v] == 1
+    heli = inst.base_kind[np.where(placed, vb[v], 0)] == 1
+    ok &= placed & ~(fixed & (inst.rotary_only == 1)) & ~(fixed & heli)
+    return int(ok.sum())
 
 
 def _traffic():
@@ -317,6 +335,19 @@ def extra_workloads(device: int) -> dict:
                 "exact_fallbacks": rq.stats.exact_fallbacks,
                 "move_evals_per_s": rq.stats.evaluations / (rq.stats.device_ms / 1e3)}
         del t
+    # c1 (the reference's own CPU-runnable case) completes the c1 -> c4 sweep
+    i1 = F.survey_instance(50, 200, 10, seed=1)
+    t1 = F.build_distance_table(i1, device=device)
+    s1 = F.rank_bases(i1, t1)
+    a1 = F._state_arrays(s1.assignment, F.initial_pool(s1, i1), i1)
+    F.search_arrays(i1, t1, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu), *a1)  # warm
+    r1 = F.search_arrays(i1, t1, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu), *a1)
+    out["c1_to_quiescence"] = {
+        "workload": "50 bases x 200 missions x 10 vehicles, tabu seed 7 to quiescence",
+        "search_ms": r1.stats.device_ms, "passes": r1.stats.passes,
+        "evaluations": r1.stats.evaluations, "applied_moves": r1.stats.applied_moves,
+        "final_objective_km": r1.stats.final_objective_km}
+    del t1
     n = 512
     insts, starts, tabs = [], [], []
     for k in range(n):

@@ -56,6 +56,7 @@ struct Shared {
   int bi[8];
   int ev;                               // scan step result broadcast
   int nj;                               // live j-keys in sm.jl_*
+  int nrl;                              // vehicles whose relocation class is not POS (sm.rlist)
   long long jexp_max;                   // latest expiry of any vehicle's {Relocate, id} key
   int tmp;
   double bd0;
@@ -84,6 +85,7 @@ struct Smem {
   int* xlist;          // position buffer for relocation bitset updates (global scratch)
   int xlist_cap;
   int* impc;           // [V] set bits of imp[g] (0 = no reassign/takeover to g improves)
+  int* rlist;          // [V] vehicles whose relocation to the row's empty base may improve
   int* jl_v;           // [V] vehicles whose {Relocate, id} j-key is live
   int* jl_lim;         // [V] its live window (positions from the segment start)
   uint8_t* jl_outer;   // [V] its role is Outer
@@ -1737,7 +1739,23 @@ __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int 
     sh.nj = 0;
   }
   const int t = sh.rel_t;
-  if (t >= 0) relocation_classes<NT, HELP>(s, sh, sm, t);
+  if (t >= 0) {
+    relocation_classes<NT, HELP>(s, sh, sm, t);
+    // the movers that can relocate with gain: the scan's relocation mask is
+    // then the OR of their membership words
+    if (threadIdx.x < 32) {
+      const int l = threadIdx.x;
+      int n = 0;
+      for (int v0 = 0; v0 < s.V; v0 += 32) {
+        const int v = v0 + l;
+        const bool on = v < s.V && sm.cls[v] != CLS_POS;
+        const unsigned m = __ballot_sync(FULL, on);
+        if (on) sm.rlist[n + __popc(m & ((1u << l) - 1u))] = v;
+        n += __popc(m);
+      }
+      if (l == 0) sh.nrl = n;
+    }
+  }
   __syncthreads();
 }
 
@@ -1768,6 +1786,7 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
     const int p_seg = p;
     const int gain_r = sh.gain_r, gain_t = sh.gain_t, rel_t = sh.rel_t;
     const int lim_ro = sh.lim_ro, lim_ra = sh.lim_ra, nj = sh.nj;
+    const int nrl = rel_t >= 0 ? sh.nrl : 0;
     const uint32_t* imp_r = s.imp + (long long)gain_r * nwd;
     const uint32_t* imp_t = s.imp + (long long)(gain_t >= 0 ? gain_t : 0) * nwd;
     int ev = INT_MAX;
@@ -1776,9 +1795,13 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
       const int wd = w0 + w * 32 + l;
       const long long base = (long long)wd * 32;
       uint32_t relw = 0;
-      if (rel_t >= 0) {
-        // relocation candidates need the vehicle of every position: one
-        // coalesced pass over the warp's 32 words, lane = position
+      if (rel_t >= 0 && nrl <= 8) {
+        // relocation candidates: the positions of the few movers that can gain
+        if (wd < nwd)
+          for (int k = 0; k < nrl; ++k) relw |= s.mem[(long long)sm.rlist[k] * nwd + wd];
+      } else if (rel_t >= 0) {
+        // many movers: the vehicle of every position, one coalesced pass over
+        // the warp's 32 words, lane = position
         for (int k = 0; k < 32; ++k) {
           const long long q = (long long)(w0 + w * 32 + k) * 32 + l;
           bool b = false;
@@ -2038,7 +2061,7 @@ size_t pass_smem_core(int V, int NT) {
   const int NW = NT / 32;
   return align16(4ull * V) + align16(V) + align16(V) + 2 * align16(8ull * NW * V) +
          align16(8ull * NW * 32) + align16(8ull * NW * 3) + 3 * align16(4ull * V) + align16(V) +
-         align16(8ull * NT) + align16(8ull * NT) + 64;
+         align16(8ull * NT) + align16(8ull * NT) + align16(4ull * V) + 64;
 }
 size_t pass_smem_state(int V, int B, int K) {
   return align16(8ull * V) * 2 + align16(8ull * K) + align16(K) + align16(4ull * V) * 3 +
@@ -2089,6 +2112,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   sm.jl_lim = reinterpret_cast<int*>(take(4ull * V));
   sm.jl_outer = take(V);
   sm.impc = reinterpret_cast<int*>(take(4ull * V));
+  sm.rlist = reinterpret_cast<int*>(take(4ull * V));
   sm.paw = reinterpret_cast<int*>(take(8ull * NT));
   sm.pb = perms + s.M;
   sm.helpers = helpers;

@@ -47,12 +47,6 @@ constexpr unsigned FULL = 0xffffffffu;
 
 struct Shared {
   Counters c;                 // block copy of the counters
-  // row context (written by thread 0, read by all)
-  int gain_r, col_r, fixed_r;           // reassignment gainer = vehicle of mission i
-  int gain_t, col_t, fixed_t;           // takeover gainer (pool[i] idle) or -1
-  int rel_t, heli_t;                    // relocation target (pool[i] empty) or -1
-  int lim_ro, lim_ra;                   // row keys: live-positions (outer / any)
-  long long t0;                         // tick at the start of the scan segment
   int bi[8];
   int ev;                               // scan step result broadcast
   int nj;                               // live j-keys in sm.jl_*
@@ -1664,53 +1658,53 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
   __syncthreads();
 }
 
-// Row context after any state change (thread 0 writes, all read after sync).
+// Row context after any state change, computed by every thread from the
+// block-uniform state (no barrier unless a j-key is live or the row
+// relocates; those phases publish through shared memory).
+struct RowCtx {
+  int gain_r, gain_t, rel_t, lim_ro, lim_ra, nj, nrl;
+};
+
 template <int NT, bool HELP>
-__device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int i, bool tabu) {
-  if (threadIdx.x == 0) {
-    sh.c.counts[2] += 1;
-    const int g = s.mv[i];
-    sh.gain_r = g;
-    sh.col_r = s.vbase[g];
-    sh.fixed_r = s.vfixed[g];
-    sh.gain_t = -1;
-    sh.rel_t = -1;
-    int lim_ro = 0, lim_ra = 0;
-    const long long T = sh.c.tick;
-    sh.t0 = T;
-    if (i < sh.c.psize) {
-      const int k = s.pkind[i], x = s.pidx[i];
-      if (k == POOL_IDLE) {
-        sh.gain_t = x;
-        sh.col_t = s.vbase[x];
-        sh.fixed_t = s.vfixed[x];
-        if (tabu) {
-          const int lim = clamp_lim(s.exp_take[x] - T, s.M);
-          lim_ro = lim;
-          lim_ra = lim;
-        }
-      } else {
-        sh.rel_t = x;
-        sh.heli_t = s.bheli[x];
-        if (tabu) {
-          const int kk = s.brk[x];
-          const int lim = clamp_lim(s.exp_rel[kk] - T, s.M);
-          if (s.role_rel[kk] == ROLE_OUTER) lim_ro = lim;
-          lim_ra = lim;
-        }
+__device__ RowCtx make_context(const Scenario& s, Shared& sh, const Smem& sm, int i, bool tabu) {
+  RowCtx c;
+  const long long T = sh.c.tick;
+  const int g = s.mv[i];
+  c.gain_r = g;
+  c.gain_t = -1;
+  c.rel_t = -1;
+  int lim_ro = 0, lim_ra = 0;
+  if (i < sh.c.psize) {
+    const int k = s.pkind[i], x = s.pidx[i];
+    if (k == POOL_IDLE) {
+      c.gain_t = x;
+      if (tabu) {
+        const int lim = clamp_lim(s.exp_take[x] - T, s.M);
+        lim_ro = lim;
+        lim_ra = lim;
+      }
+    } else {
+      c.rel_t = x;
+      if (tabu) {
+        const int kk = s.brk[x];
+        const int lim = clamp_lim(s.exp_rel[kk] - T, s.M);
+        if (s.role_rel[kk] == ROLE_OUTER) lim_ro = lim;
+        lim_ra = lim;
       }
     }
-    if (tabu) {
-      const int lim = clamp_lim(s.exp_reas[g] - T, s.M);
-      lim_ro = max(lim_ro, lim);
-      lim_ra = max(lim_ra, lim);
-    }
-    sh.lim_ro = lim_ro;
-    sh.lim_ra = lim_ra;
   }
-  __syncthreads();
-  if (tabu && sh.jexp_max > sh.t0) {
-    const long long T = sh.t0;
+  if (tabu) {
+    const int lim = clamp_lim(s.exp_reas[g] - T, s.M);
+    lim_ro = max(lim_ro, lim);
+    lim_ra = max(lim_ra, lim);
+  }
+  c.lim_ro = lim_ro;
+  c.lim_ra = lim_ra;
+  c.nj = 0;
+  c.nrl = 0;
+  __syncwarp();
+  if (threadIdx.x == 0) sh.c.counts[2] += 1;
+  if (tabu && sh.jexp_max > T) {
     for (int v = threadIdx.x; v < s.V; v += NT) {
       const int k = s.vrk[v];
       sm.lim_j[v] = clamp_lim(s.exp_rel[k] - T, s.M);
@@ -1735,12 +1729,11 @@ __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int 
       }
       if (l == 0) sh.nj = n;
     }
-  } else if (threadIdx.x == 0) {
-    sh.nj = 0;
+    __syncthreads();
+    c.nj = sh.nj;
   }
-  const int t = sh.rel_t;
-  if (t >= 0) {
-    relocation_classes<NT, HELP>(s, sh, sm, t);
+  if (c.rel_t >= 0) {
+    relocation_classes<NT, HELP>(s, sh, sm, c.rel_t);
     // the movers that can relocate with gain: the scan's relocation mask is
     // then the OR of their membership words
     if (threadIdx.x < 32) {
@@ -1755,8 +1748,10 @@ __device__ void make_context(const Scenario& s, Shared& sh, const Smem& sm, int 
       }
       if (l == 0) sh.nrl = n;
     }
+    __syncthreads();
+    c.nrl = sh.nrl;
   }
-  __syncthreads();
+  return c;
 }
 
 // One outer-index row, proj/src/search.cpp:307-346.
@@ -1780,13 +1775,13 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
   if (threadIdx.x == 0) sh.c.counts[0] += 1;
   while (p < M) {
     const long long c0 = ph_now();
-    make_context<NT, HELP>(s, sh, sm, i, tabu);
+    const RowCtx cx = make_context<NT, HELP>(s, sh, sm, i, tabu);
     PH_ADD(sh, 1, c0);
     const long long c1 = ph_now();
     const int p_seg = p;
-    const int gain_r = sh.gain_r, gain_t = sh.gain_t, rel_t = sh.rel_t;
-    const int lim_ro = sh.lim_ro, lim_ra = sh.lim_ra, nj = sh.nj;
-    const int nrl = rel_t >= 0 ? sh.nrl : 0;
+    const int gain_r = cx.gain_r, gain_t = cx.gain_t, rel_t = cx.rel_t;
+    const int lim_ro = cx.lim_ro, lim_ra = cx.lim_ra, nj = cx.nj;
+    const int nrl = cx.nrl;
     const uint32_t* imp_r = s.imp + (long long)gain_r * nwd;
     const uint32_t* imp_t = s.imp + (long long)(gain_t >= 0 ? gain_t : 0) * nwd;
     int ev = INT_MAX;

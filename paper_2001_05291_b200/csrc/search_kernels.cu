@@ -2330,7 +2330,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
         PH_ADD(sh, 0, b0);
         if (nskip > 0) continue;
       }
-      __syncthreads();  // thread 0's counter updates before run_row reads them
+      // (the reduction barrier above published thread 0's counter updates)
       run_row<NT, HELP>(s, sh, sm, sm.paw[r - pw], tabu, tenure, debug);
       __syncthreads();
       T = sh.c.tick;

@@ -223,6 +223,28 @@ fp_status fp_column_totals(fp_ctx* ctx, double* out_totals);
 fp_status fp_rank_bases(fp_ctx* ctx, const fp_instance* inst,
                         fp_ranked_start* out);
 
+/* ---- missions sharded across GPUs ---------------------- */
+/* A mission shard's context holds the table of a contiguous mission range
+ * (fp_build_distance_table / fp_table_upload on an instance carrying all
+ * bases and vehicles and that range's missions).
+ *
+ * column_totals (proj/src/rank.cpp:10-23) continued across shards: for the
+ * columns [b0, b0 + nb), out[k] = the fixed-order fp64 chain over this
+ * shard's rows starting at carry[k] (NULL: 0.0). Feeding shard g's `out` as
+ * shard g+1's `carry` gives, on the last shard, the reference's totals bit
+ * for bit (the sum is never reassociated; rank.hpp:16-18's bit-identity
+ * contract). device_ptrs = 1: carry/out are device pointers on ctx's device
+ * (e.g. NCCL buffers), 0: host pointers. Synchronous at return. */
+fp_status fp_column_totals_chain(fp_ctx* ctx, int32_t b0, int32_t nb,
+                                 const double* carry, double* out,
+                                 int32_t device_ptrs);
+/* rank_bases steps (2)-(6) (proj/src/rank.cpp:35-121) from given totals of
+ * all bases (host, n_bases): rank order, helipad cap, placement, and the
+ * per-mission argmin for the resident table's missions (those of `inst`,
+ * e.g. one shard). out->base_totals receives a copy of totals. */
+fp_status fp_rank_from_totals(fp_ctx* ctx, const fp_instance* inst,
+                              const double* totals, fp_ranked_start* out);
+
 /* ---- kernels (3)+(4): search ------------------------------------------- */
 /* initial_pool (proj/src/search.cpp:364-377): unused bases in the given
  * order, then placed vehicles serving no mission, in vehicle-id order.

@@ -20,7 +20,7 @@ EXPORTS = (
     "fp_build_distance_table", "fp_table_upload", "fp_table_download",
     "fp_column_totals", "fp_rank_bases", "fp_initial_pool", "fp_search",
     "fp_search_batch", "fp_enumerate_moves", "fp_objective_km", "fp_haversine_batch",
-    "fp_permutations",
+    "fp_permutations", "fp_column_totals_chain", "fp_rank_from_totals",
 )
 
 _lib: C.CDLL | None = None
@@ -69,6 +69,10 @@ def lib() -> C.CDLL:
     l.fp_column_totals.restype = i32
     l.fp_rank_bases.argtypes = [p, inst_p, C.POINTER(A.fp_ranked_start)]
     l.fp_rank_bases.restype = i32
+    l.fp_column_totals_chain.argtypes = [p, i32, i32, p, p, i32]
+    l.fp_column_totals_chain.restype = i32
+    l.fp_rank_from_totals.argtypes = [p, inst_p, f64p, C.POINTER(A.fp_ranked_start)]
+    l.fp_rank_from_totals.restype = i32
     l.fp_initial_pool.argtypes = [inst_p, i32p, i32p, i32p, i32, i32p, i32p, i32p]
     l.fp_initial_pool.restype = i32
     l.fp_search.argtypes = [p, inst_p, C.POINTER(A.fp_search_config),

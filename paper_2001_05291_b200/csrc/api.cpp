@@ -1071,11 +1071,17 @@ fp_status fp_column_totals(fp_ctx* ctx, double* out_totals) {
   });
 }
 
+namespace {
+// rank_bases steps (2)-(6) (rank.cpp:35-121) from the base totals `tot` on
+// the resident table (the whole instance, or one mission shard of it).
+void rank_from_totals(fp_ctx* ctx, const fp_instance* in, const double* tot, fp_ranked_start* out);
+}  // namespace
+
 fp_status fp_rank_bases(fp_ctx* ctx, const fp_instance* in, fp_ranked_start* out) {
   return guarded([&] {
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
     validate(in);
-    const int M = in->n_missions, B = in->n_bases, V = in->n_vehicles;
+    const int M = in->n_missions, B = in->n_bases;
     ensure_table(ctx, M, B);
     cudaStream_t st = ctx->stream;
     // (1) fixed-order column totals on the device
@@ -1086,7 +1092,57 @@ fp_status fp_rank_bases(fp_ctx* ctx, const fp_instance* in, fp_ranked_start* out
     ctx->launches += 1;
     d2h(out->base_totals, d_tot.p, B, st);
     check(cudaStreamSynchronize(st), "totals sync");
-    const double* tot = out->base_totals;
+    rank_from_totals(ctx, in, out->base_totals, out);
+  });
+}
+
+fp_status fp_column_totals_chain(fp_ctx* ctx, int32_t b0, int32_t nb, const double* carry,
+                                 double* out, int32_t device_ptrs) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (ctx->M < 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "no resident table");
+    if (b0 < 0 || nb < 0 || (int64_t)b0 + nb > ctx->B || !out)
+      throw FpError(FP_ERR_INVALID_ARGUMENT, "column range outside the resident table");
+    if (nb == 0) return;
+    cudaStream_t st = ctx->stream;
+    const double* d_carry = carry;
+    double* d_out = out;
+    DBuf<double> tmp(device_ptrs ? 0 : 2 * (size_t)nb);
+    if (!device_ptrs) {
+      d_out = tmp.p;
+      if (carry) {
+        h2d(tmp.p + nb, carry, nb, st);
+        d_carry = tmp.p + nb;
+      }
+    }
+    EvTimer tk(st);
+    check(fpk::launch_column_totals_chain(ctx->d_cost + (size_t)b0 * ctx->M, ctx->M, nb, d_carry,
+                                          d_out, st),
+          "totals chain");
+    ctx->last_kernel_ms = tk.stop_ms();
+    ctx->launches += 1;
+    if (!device_ptrs) d2h(out, d_out, nb, st);
+    check(cudaStreamSynchronize(st), "totals chain sync");
+  });
+}
+
+fp_status fp_rank_from_totals(fp_ctx* ctx, const fp_instance* in, const double* totals,
+                              fp_ranked_start* out) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    validate(in);
+    ensure_table(ctx, in->n_missions, in->n_bases);
+    if (!totals) throw FpError(FP_ERR_INVALID_ARGUMENT, "totals is NULL");
+    if (out->base_totals && out->base_totals != totals)
+      std::copy(totals, totals + in->n_bases, out->base_totals);
+    rank_from_totals(ctx, in, totals, out);
+  });
+}
+
+namespace {
+void rank_from_totals(fp_ctx* ctx, const fp_instance* in, const double* tot, fp_ranked_start* out) {
+    const int M = in->n_missions, B = in->n_bases, V = in->n_vehicles;
+    cudaStream_t st = ctx->stream;
     // (2) rank order: total ascending, lower id on ties (rank.cpp:35-43)
     std::vector<int> order(B);
     std::iota(order.begin(), order.end(), 0);
@@ -1172,8 +1228,8 @@ fp_status fp_rank_bases(fp_ctx* ctx, const fp_instance* in, fp_ranked_start* out
     for (int bi : order)
       if (base_vehicle[bi] < 0) out->unused_bases[nu++] = bi;
     out->n_unused = nu;
-  });
 }
+}  // namespace
 
 fp_status fp_initial_pool(const fp_instance* in, const int32_t* vehicle_base,
                           const int32_t* mission_vehicle, const int32_t* unused_bases,

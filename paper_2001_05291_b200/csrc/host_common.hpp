@@ -29,6 +29,8 @@ cudaError_t launch_haversine_pairs(int n, const double* alat, const double* alon
                                    const double* clon, double radius_km, double* out,
                                    cudaStream_t st);
 cudaError_t launch_column_totals(const double* cost, int M, int B, double* out, cudaStream_t st);
+cudaError_t launch_column_totals_chain(const double* cost, int M, int B, const double* carry,
+                                       double* out, cudaStream_t st);
 cudaError_t launch_mission_argmin(const double* cost, int M, const int32_t* cb, const int32_t* cbid,
                                   const uint8_t* cf, const int32_t* cv, int n, const uint8_t* ro,
                                   int32_t* mv, int32_t* first_bad, cudaStream_t st);

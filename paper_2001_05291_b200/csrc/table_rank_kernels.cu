@@ -203,7 +203,8 @@ __device__ __forceinline__ long long col_round(double x, double inv_u, bool& tie
 // lane scan per 32 terms and one true fp64 add (the same algorithm as the
 // search's exact_chain). HBM-bound: each entry read once.
 __global__ void __launch_bounds__(256)
-    column_chain_kernel(const double* __restrict__ cost, int M, int B, double* __restrict__ out) {
+    column_chain_kernel(const double* __restrict__ cost, int M, int B, const double* __restrict__ carry,
+                        double* __restrict__ out) {
   constexpr int UE = 32;
   constexpr long long LIM = 1ll << 53;
   constexpr unsigned FULL = 0xffffffffu;
@@ -211,7 +212,8 @@ __global__ void __launch_bounds__(256)
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (b >= B) return;
   const double* col = cost + (long long)b * M;
-  double S = 0.0;
+  // a mission shard continues the chain of the shards before it
+  double S = carry ? carry[b] : 0.0;
   int k = 0;
   if (l == 0)
     while (k < M && !(S >= 0x1p-900)) S = __dadd_rn(S, col[k++]);  // leading zeros / tiny values
@@ -275,10 +277,17 @@ __global__ void __launch_bounds__(256)
   if (l == 0) out[b] = S;
 }
 
-cudaError_t launch_column_totals(const double* cost, int M, int B, double* out, cudaStream_t st) {
+// Columns [0, B) of `cost` (pre-offset by the caller for a column range),
+// each chain starting at carry[b] (NULL: 0.0).
+cudaError_t launch_column_totals_chain(const double* cost, int M, int B, const double* carry,
+                                       double* out, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  column_chain_kernel<<<(B + 7) / 8, 256, 0, st>>>(cost, M, B, out);
+  column_chain_kernel<<<(B + 7) / 8, 256, 0, st>>>(cost, M, B, carry, out);
   return cudaGetLastError();
+}
+
+cudaError_t launch_column_totals(const double* cost, int M, int B, double* out, cudaStream_t st) {
+  return launch_column_totals_chain(cost, M, B, nullptr, out, st);
 }
 
 cudaError_t launch_mission_argmin(const double* cost, int M, const int32_t* cb, const int32_t* cbid,

@@ -179,6 +179,15 @@ class Instance:
         self._cstruct = None
         self._maps = None
 
+    def mission_slice(self, lo: int, hi: int) -> "Instance":
+        """All bases and vehicles with the missions [lo, hi) in load order:
+        one mission shard of a single instance."""
+        return Instance.from_arrays(
+            self.base_id, self.base_kind, self.base_lat, self.base_lon, self.vehicle_id,
+            self.vehicle_kind, self.mission_id[lo:hi], self.pickup_lat[lo:hi],
+            self.pickup_lon[lo:hi], self.delivery_lat[lo:hi], self.delivery_lon[lo:hi],
+            self.rotary_only[lo:hi])
+
     # -- views in the reference's AoS vocabulary
     @property
     def bases(self) -> list[Base]:

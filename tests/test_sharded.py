@@ -1,0 +1,105 @@
+"""CPU: the mission-sharded single-instance path's host logic
+with world sizes 2 and 3 over gloo. Each rank holds a contiguous mission
+slice of the table and continues the column-total chains of the ranks before
+it, column batch by column batch; the last rank's sums must be the
+reference's fixed-order totals bit for bit. The per-rank chain here is a
+numpy sequential sum (test infrastructure standing in for the device kernel,
+which the GPU tests run through the same protocol)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import oracle_harness as H
+from paper_2001_05291_b200.dist import shard
+from paper_2001_05291_b200.sharded import chained_totals, column_batches
+
+
+def _seq_totals(T):
+    """Column sums strictly in row order (proj/src/rank.cpp:10-23)."""
+    s = np.zeros(T.shape[1])
+    for m in range(T.shape[0]):
+        s = s + T[m]
+    return s
+
+
+def _np_chain(T):
+    def chain(b0, nb, carry, out):
+        s = carry.numpy().copy() if carry is not None else np.zeros(nb)
+        for m in range(T.shape[0]):
+            s = s + T[m, b0:b0 + nb]
+        out.copy_(torch.from_numpy(s))
+    return chain
+
+
+def _wide_table(M=1500, B=37, seed=3):
+    """Terms spread over many binades (reassociation changes the sums)."""
+    rng = np.random.default_rng(seed)
+    return np.exp(rng.uniform(-20, 12, size=(M, B)))
+
+
+def test_column_batches_partition():
+    for B in (1, 5, 37, 5000):
+        for k in (1, 3, 8, 64):
+            parts = column_batches(B, k)
+            assert [b for b0, nb in parts for b in range(b0, b0 + nb)] == list(range(B))
+            assert all(nb > 0 for _, nb in parts)
+
+
+def _worker(rank, world, port, table, batches, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rg = shard(table.shape[0], rank, world)
+    tot = chained_totals(table.shape[1], _np_chain(table[rg.start:rg.stop]), batches=batches)
+    q.put((rank, tot.numpy().copy()))
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(table, world, batches):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_worker, args=(world, _free_port(), table, batches, q), nprocs=world,
+                       start_method="spawn")
+    return dict(q.get(timeout=60) for _ in range(world))
+
+
+@pytest.mark.parametrize("world,batches", [(2, 1), (3, 7)])
+def test_chained_totals_bit_identical_across_ranks(world, batches):
+    T = _wide_table()
+    want = _seq_totals(T)
+    # the test is meaningful: summing per-shard partials would not match
+    naive = sum(_seq_totals(T[r.start:r.stop]) for r in (shard(len(T), g, world) for g in range(world)))
+    assert (naive != want).any()
+    got = _run(T, world, batches)
+    for g in range(world):
+        assert got[g].tobytes() == want.tobytes(), g
+
+
+@pytest.mark.skipif(H.REF is None, reason="reference not built")
+def test_chained_totals_equal_reference_rank_totals():
+    """On the reference's own table of a survey instance, the 3-rank chain
+    reproduces the reference's rank_bases base_totals bit for bit."""
+    inst = H.ref_survey_instance(50, 700, 10, seed=2)
+    cost = H.ref_table(inst)
+    T = cost.reshape(inst.n_bases, inst.n_missions).T.copy()
+    want = H.ref_rank(inst, cost).totals
+    got = _run(T, 3, 5)
+    for g in range(3):
+        assert got[g].tobytes() == want.tobytes()
+
+
+def test_single_process_no_exchange():
+    T = _wide_table(200, 9)
+    assert chained_totals(9, _np_chain(T), batches=4).numpy().tobytes() == _seq_totals(T).tobytes()

@@ -1,0 +1,108 @@
+"""GPU: the mission-sharded single-instance path on one
+device. The shards run one after another in this process (each its own
+context holding its mission slice of the table), handing the running column
+sums on through `fp_column_totals_chain` exactly as the ranks do over NCCL;
+the concatenated result must equal the unsharded device path and the
+reference bit for bit."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import oracle_harness as H
+from paper_2001_05291_b200 import _abi as A
+from paper_2001_05291_b200 import fleetplace as F
+from paper_2001_05291_b200 import sharded as S
+from paper_2001_05291_b200._native import lib
+from paper_2001_05291_b200.dist import shard
+
+pytestmark = pytest.mark.gpu
+
+
+def _shard_tables(inst, world, host_cost=None):
+    parts = []
+    for g in range(world):
+        rg = shard(inst.n_missions, g, world)
+        sub = inst.mission_slice(rg.start, rg.stop)
+        if host_cost is None:
+            t = F.build_distance_table(sub)
+        else:
+            t = F.DistanceTable.from_host(host_cost[rg.start:rg.stop])
+        parts.append((rg, sub, t))
+    return parts
+
+
+def _chain_host(parts, B, batches):
+    """Rank after rank, batch after batch, through host pointers."""
+    carry = None
+    for _, _, t in parts:
+        out = np.empty(B)
+        for b0, nb in S.column_batches(B, batches):
+            cp = A.ptr(carry[b0:b0 + nb], C.c_double) if carry is not None else None
+            F._check(lib().fp_column_totals_chain(t._ctx.p, b0, nb, cp,
+                                                  A.ptr(out[b0:b0 + nb], C.c_double), 0))
+        carry = out
+    return carry
+
+
+@pytest.mark.parametrize("world,batches", [(2, 1), (3, 4), (8, 8)])
+def test_sharded_totals_and_ranking_equal_reference(world, batches):
+    inst = F.survey_instance(500, 10000, 40, seed=1)
+    cost = H.ref_table(inst)
+    T = cost.reshape(inst.n_bases, inst.n_missions).T
+    want = H.ref_rank(inst, cost)
+    parts = _shard_tables(inst, world, T)
+    tot = _chain_host(parts, inst.n_bases, batches)
+    assert tot.tobytes() == want.totals.tobytes()
+    mv = np.concatenate([S.rank_from_totals(sub, t, tot, rg.start).mission_vehicle
+                         for rg, sub, t in parts])
+    last = S.rank_from_totals(parts[-1][1], parts[-1][2], tot)
+    assert np.array_equal(last.vehicle_base, want.vehicle_base)
+    assert np.array_equal(last.unused_index, want.unused)
+    assert np.array_equal(mv, want.mission_vehicle)
+
+
+def test_sharded_device_tables_equal_unsharded_device_path():
+    """Own kernel (1) tables per shard: same totals bits and same RankedStart
+    as the single-GPU path, with device-pointer chains (the NCCL buffers'
+    path) and an empty shard (more ranks than missions in the last slices)."""
+    inst = F.survey_instance(200, 5000, 20, seed=4)
+    t = F.build_distance_table(inst)
+    rs = F.rank_bases(inst, t)
+    parts = _shard_tables(inst, 3)
+    carry = None
+    for _, _, tp in parts:
+        out = torch.empty(inst.n_bases, dtype=torch.float64, device="cuda:0")
+        for b0, nb in S.column_batches(inst.n_bases, 3):
+            S.device_chain(tp)(b0, nb, None if carry is None else carry[b0:b0 + nb], out[b0:b0 + nb])
+        carry = out
+    tot = carry.cpu().numpy()
+    assert tot.tobytes() == rs.base_totals.tobytes()
+    mv = np.concatenate([S.rank_from_totals(sub, tp, tot, rg.start).mission_vehicle
+                         for rg, sub, tp in parts])
+    assert np.array_equal(mv, rs.mission_vehicle)
+    tiny = F.small_generated(5, missions=3)
+    tt = F.build_distance_table(tiny)
+    ptiny = _shard_tables(tiny, 5)
+    assert any(rg.stop == rg.start for rg, _, _ in ptiny)
+    assert _chain_host(ptiny, tiny.n_bases, 2).tobytes() == F.column_totals(tt).tobytes()
+
+
+def test_rank_bases_sharded_world_one():
+    inst = F.survey_instance(50, 200, 10, seed=1)
+    part, _ = S.rank_bases_sharded(inst)
+    full = S.gather_start(inst, part)
+    rs = F.rank_bases(inst, F.build_distance_table(inst))
+    assert full.assignment == rs.assignment
+    assert full.unused_bases == rs.unused_bases
+    assert full.base_totals.tobytes() == rs.base_totals.tobytes()
+
+
+def test_chain_rejects_bad_ranges():
+    inst = F.survey_instance(50, 200, 10, seed=1)
+    t = F.build_distance_table(inst)
+    out = np.empty(60)
+    for b0, nb in ((-1, 5), (45, 10), (0, -1)):
+        rc = lib().fp_column_totals_chain(t._ctx.p, b0, nb, None, A.ptr(out, C.c_double), 0)
+        assert rc == A.FP_ERR_INVALID_ARGUMENT

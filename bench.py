@@ -202,6 +202,10 @@ def run_ours(args) -> None:
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if not args.no_extras:
+        sh = sharded_rank_workload(ws, rank, local)  # every rank takes part
+        if rank == 0:
+            line["c4_sharded_table_rank"] = sh
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(inst, host_cost, start, pk, px)
     if rank == 0 and not args.no_extras:
@@ -271,6 +275,56 @@ def _kernel_rooflines(inst, t, start_ms, r, peak):
         if k["bound"].startswith("hbm") and k["achieved_gbs"]:
             k["frac_of_measured_hbm"] = k["achieved_gbs"] / peak
     return out
+
+
+def sharded_rank_workload(ws: int, rank: int, local: int, reps: int = 2) -> dict:
+    """c4 (5k x 1M x 250) build_distance_table + rank_bases with the missions
+    sharded across the ws ranks (paper_2001_05291_b200/
+    sharded.py): each rank builds its 1M/ws-mission slice of the 40 GB table,
+    the column-total chains pass rank to rank over NCCL, every rank ranks the
+    bases and resolves its missions. Timed with CUDA events bracketing the
+    synchronous calls (host orchestration and the NCCL hand-offs included),
+    after one warm-up call, max over ranks. `totals_sha256` must be the same
+    at every N (the totals are the reference's fixed-order sums)."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+    from paper_2001_05291_b200 import fleetplace as F
+    from paper_2001_05291_b200 import sharded as S
+
+    shape = (5000, 1000000, 250)
+    inst = F.survey_instance(*shape, seed=1)
+    part, table = S.rank_bases_sharded(inst, device=local)
+    ms = []
+    for _ in range(reps):
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        part, table = S.rank_bases_sharded(inst, device=local, table=table)
+        e1.record()
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    v = torch.tensor([float(np.mean(ms)), float((part.mission_vehicle >= 0).sum())],
+                     dtype=torch.float64, device="cuda")
+    if ws > 1:
+        mx = v.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+        v[0] = mx[0]
+    del table
+    torch.cuda.empty_cache()
+    B, M = shape[0], shape[1]
+    return {"workload": "c4 5000 bases x 1M missions x 250 vehicles: build_distance_table + "
+                        f"rank_bases, missions sharded over {ws} GPU(s)",
+            "ms": float(v[0]), "n_gpus": ws, "missions_per_gpu": -(-M // ws),
+            "assigned_missions": int(v[1]), "missions": M,
+            "table_bytes_per_gpu": 8 * B * -(-M // ws),
+            "totals_sha256": hashlib.sha256(part.base_totals.tobytes()).hexdigest(),
+            "timing": "CUDA events around the synchronous calls, mean of 2 after 1 warm-up, "
+                      "max over ranks"}
 
 
 def _c4_sweep_roofline(extra: dict, peak: float) -> dict:

@@ -119,7 +119,7 @@ def rank_from_totals(shard_inst: F.Instance, table: F.DistanceTable, totals: np.
 
 
 def rank_bases_sharded(inst: F.Instance, *, group=None, device: int = 0, batches: int = 8,
-                       radius_km: float = F.kEarthRadiusKm):
+                       radius_km: float = F.kEarthRadiusKm, table: F.DistanceTable = None):
     """build_distance_table + rank_bases (proj/src/model.cpp:76-90,
     proj/src/rank.cpp:25-124) with the missions sharded across the ranks of
     `group`, one GPU per rank. Returns (this rank's ShardStart, its table
@@ -130,7 +130,11 @@ def rank_bases_sharded(inst: F.Instance, *, group=None, device: int = 0, batches
     g = dist.get_rank(group) if dist.is_initialized() else 0
     rg = shard(inst.n_missions, g, world)
     part = inst.mission_slice(rg.start, rg.stop)
-    table = F.build_distance_table(part, radius_km, device=device)
+    if table is None:
+        table = F.build_distance_table(part, radius_km, device=device)
+    else:
+        F._check(lib().fp_build_distance_table(table._ctx.p, C.byref(part.c()), radius_km, None))
+        table.n_missions, table.n_bases, table._host = part.n_missions, part.n_bases, None
     nccl = dist.is_initialized() and dist.get_backend(group) == "nccl"
     totals = chained_totals(inst.n_bases, device_chain(table), group=group, batches=batches,
                             device=f"cuda:{device}" if nccl else "cpu")

@@ -91,7 +91,8 @@ def test_sharded_device_tables_equal_unsharded_device_path():
 
 def test_rank_bases_sharded_world_one():
     inst = F.survey_instance(50, 200, 10, seed=1)
-    part, _ = S.rank_bases_sharded(inst)
+    part, tp = S.rank_bases_sharded(inst)
+    part, _ = S.rank_bases_sharded(inst, table=tp)  # rebuilt in place
     full = S.gather_start(inst, part)
     rs = F.rank_bases(inst, F.build_distance_table(inst))
     assert full.assignment == rs.assignment

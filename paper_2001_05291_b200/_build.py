@@ -33,17 +33,27 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
     LIB_DIR.mkdir(exist_ok=True)
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v", f"-I{ROOT / 'include'}", f"-I{CSRC}",
-           *[str(CSRC / s) for s in SOURCES], "-o", str(LIB)]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    (LIB_DIR / "build.log").write_text(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError(f"nvcc failed ({r.returncode}); see {LIB_DIR / 'build.log'}")
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+    # one nvcc per source in parallel, then one link
+    cmds = [[NVCC, *flags, "-c", str(CSRC / s), "-o", str(LIB_DIR / (s + ".o"))] for s in SOURCES]
+    cmds.append([NVCC, *ARCH, "-shared", *[str(LIB_DIR / (s + ".o")) for s in SOURCES],
+                 "-o", str(LIB)])
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        rs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds[:-1]))
+    if all(r.returncode == 0 for r in rs):
+        rs.append(subprocess.run(cmds[-1], capture_output=True, text=True))
+    log = "".join(" ".join(c) + "\n" + r.stdout + r.stderr for c, r in zip(cmds, rs))
+    (LIB_DIR / "build.log").write_text(log)
+    bad = [r for r in rs if r.returncode != 0]
+    if bad or len(rs) < len(cmds):
+        sys.stderr.write("".join(r.stdout + r.stderr for r in bad))
+        raise RuntimeError(f"nvcc failed; see {LIB_DIR / 'build.log'}")
     if verbose:
-        sys.stdout.write(r.stderr)
+        sys.stdout.write(log)
     return LIB
 
 

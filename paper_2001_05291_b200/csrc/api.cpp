@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -173,10 +174,28 @@ void validate(const fp_instance* in) {
                                              std::to_string(in->vehicle_id[v]) + ": duplicate id");
   }
   {
+    // first repeated id in load order: a bitmap over the id range when it is
+    // compact (generated ids are dense, proj/src/data.cpp:156-174), else a map
+    const int M = in->n_missions;
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int m = 0; m < M; ++m) {
+      lo = std::min(lo, in->mission_id[m]);
+      hi = std::max(hi, in->mission_id[m]);
+    }
+    const int64_t span = M ? (int64_t)hi - lo + 1 : 0;
+    std::vector<uint64_t> bits(span <= 8 * (int64_t)M + 4096 ? (size_t)((span + 63) / 64) : 0);
     std::unordered_map<int, int> seen;
-    seen.reserve((size_t)in->n_missions * 2);
-    for (int m = 0; m < in->n_missions; ++m) {
-      if (!seen.emplace(in->mission_id[m], m).second)
+    if (bits.empty()) seen.reserve((size_t)M * 2);
+    for (int m = 0; m < M; ++m) {
+      bool dup;
+      if (!bits.empty()) {
+        const uint64_t k = (uint64_t)((int64_t)in->mission_id[m] - lo);
+        dup = (bits[k >> 6] >> (k & 63)) & 1;
+        bits[k >> 6] |= 1ull << (k & 63);
+      } else {
+        dup = !seen.emplace(in->mission_id[m], m).second;
+      }
+      if (dup)
         throw FpError(FP_ERR_VALIDATION, "validation failed for mission " +
                                              std::to_string(in->mission_id[m]) + ": duplicate id");
       if (!valid_point(in->pickup_lat[m], in->pickup_lon[m]) ||

@@ -76,6 +76,17 @@ def test_validate_instance_contract():
     bad._cstruct = None
     with pytest.raises(F.ValidationError, match="duplicate id"):
         F.validate_instance(bad)
+    # duplicate mission ids: the first repeat in load order is reported, for
+    # compact id ranges (bitmap) and sparse ones (hash map)
+    for ids in ([5, 6, 7, 6, 5], [5, 2_000_000_000, -7, 2_000_000_000, 5]):
+        dup = F.Instance(bases=[(1, 0, (45.0, -75.0))], fleet=[(0, 0)],
+                         missions=[(i, (45.0, -75.0), (45.5, -75.5), False) for i in ids])
+        with pytest.raises(F.ValidationError, match=f"mission {ids[3]}: duplicate id"):
+            F.validate_instance(dup)
+    ok = F.Instance(bases=[(1, 0, (45.0, -75.0))], fleet=[(0, 0)],
+                    missions=[(i, (45.0, -75.0), (45.5, -75.5), False)
+                              for i in (2_000_000_000, -2_000_000_000, 0, 3)])
+    F.validate_instance(ok)
     bad = _tiny()
     bad.pickup_lat[0] = 91.0
     with pytest.raises(F.ValidationError, match="out of range"):

@@ -107,3 +107,41 @@ def test_chain_rejects_bad_ranges():
     for b0, nb in ((-1, 5), (45, 10), (0, -1)):
         rc = lib().fp_column_totals_chain(t._ctx.p, b0, nb, None, A.ptr(out, C.c_double), 0)
         assert rc == A.FP_ERR_INVALID_ARGUMENT
+
+
+def _rank_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # gloo: host-pointer chains; the ranks share cuda:0 but never wait on one
+    # another inside a kernel (the hand-offs are host-side receives)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    inst = F.survey_instance(500, 10000, 40, seed=3)
+    part, _ = S.rank_bases_sharded(inst, device=0, batches=5)
+    full = S.gather_start(inst, part)
+    if rank == 0:
+        q.put((full.vehicle_base, full.mission_vehicle, full.unused_index, full.base_totals))
+    dist.destroy_process_group()
+
+
+def test_rank_bases_sharded_three_processes():
+    """The whole multi-process path (rank_bases_sharded + gather_start) with
+    three ranks; the gathered RankedStart equals the single-GPU one."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_rank_worker, args=(3, port, q), nprocs=3, start_method="spawn")
+    vb, mv, un, tot = q.get(timeout=120)
+    inst = F.survey_instance(500, 10000, 40, seed=3)
+    rs = F.rank_bases(inst, F.build_distance_table(inst))
+    assert tot.tobytes() == rs.base_totals.tobytes()
+    assert np.array_equal(vb, rs.vehicle_base)
+    assert np.array_equal(mv, rs.mission_vehicle)
+    assert np.array_equal(un, rs.unused_index)

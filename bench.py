@@ -25,6 +25,7 @@ total evaluations of all ranks / max over ranks of the device time.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -62,23 +63,42 @@ class Clocks:
 
     def __init__(self, index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+        q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
 
+    # the sampler starts before the warm-up (nvidia-smi takes a while to come
+    # up); only the samples taken inside [mark(), stop()] are kept
+    def mark(self) -> None:
+        self.t0 = time.time()
+
     def stop(self) -> dict:
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t1 = time.time()
+        time.sleep(0.06)
         self.p.terminate()
         self.p.wait()
-        rows = [r.split(", ") for r in Path(self.f.name).read_text().strip().splitlines() if r]
+        rows = []
+        for line in Path(self.f.name).read_text().strip().splitlines():
+            r = line.split(", ")
+            try:
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except (ValueError, IndexError):
+                continue
+            rows.append((ts, r[1:]))
         os.unlink(self.f.name)
+        t0 = getattr(self, "t0", 0.0)
+        inside = [r for ts, r in rows if t0 - 0.05 <= ts <= t1 + 0.05]
+        if not inside and rows:  # region shorter than the sampling period: nearest sample
+            inside = [min(rows, key=lambda x: abs(x[0] - (t0 + t1) / 2))[1]]
+        rows = inside
         sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -120,12 +140,13 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
         return F.search_arrays(inst, t, cfg, vb, mv, pk, px)
 
+    clk = Clocks(local)
     for _ in range(args.warmup):
         r = step()
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = Clocks(local)
+    clk.mark()
     launches0 = t._ctx.launches()
     results = [step() for _ in range(args.steps)]
     launches = t._ctx.launches() - launches0

@@ -688,6 +688,11 @@ __device__ __forceinline__ void put_bit(uint32_t* w, uint32_t bit, bool on) {
 template <int NT>
 __device__ void table_after_substitution(const Scenario& s, const Shared& sh, int j, int loser,
                                          int gain, double mc_old, double mc_new, int nl, int ng);
+__device__ __forceinline__ void subst_entry(const Scenario& s, int t, double c, double Al,
+                                            double El, double Ul, double Ag, double Eg, double Ug,
+                                            int loser, int gain, bool fl, bool fg, double mc_old,
+                                            double mc_new, int nl, int ng, double bt);
+__device__ __forceinline__ long long tix(const Scenario& s, int t, int v);
 
 // After mission j at position q moved from `loser` (cost mc_old, nl missions)
 // to `gain` (new cost in mcp[q], ng missions): refresh bit q of every imp
@@ -699,6 +704,23 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
                                         int ng) {
   const int wd = q >> 5;
   const uint32_t bit = 1u << (q & 31);
+  // One base per thread (B <= NT, no helpers): the table entries this
+  // thread patches are loaded before the imp-row gathers, so both sets of
+  // loads are in flight together.
+  const bool pre = !(HELP && sm.helpers > 0) && s.B <= NT;
+  const int t = threadIdx.x;
+  const bool live = pre && t < s.B && s.bveh[t] < 0;
+  double pc = 0.0, pAl = 0.0, pEl = 0.0, pUl = 0.0, pAg = 0.0, pEg = 0.0, pUg = 0.0;
+  if (live) {
+    pc = cost_mb(s, j, t);
+    const long long kl = tix(s, t, loser), kg = tix(s, t, gain);
+    pAl = s.rA[kl];
+    pEl = s.rE[kl];
+    pUl = s.rU[kl];
+    pAg = s.rA[kg];
+    pEg = s.rE[kg];
+    pUg = s.rU[kg];
+  }
   for (int g0 = 0; g0 < s.V; g0 += NT) {
     const int g = g0 + threadIdx.x;
     bool now = false;
@@ -720,6 +742,10 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
   const long long tp0 = ph_now();
   if (HELP && sm.helpers > 0) {
     if (threadIdx.x == 0) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, s.mcp[q]);
+  } else if (pre) {
+    if (live)
+      subst_entry(s, t, pc, pAl, pEl, pUl, pAg, pEg, pUg, loser, gain, s.vfixed[loser],
+                  s.vfixed[gain], mc_old, s.mcp[q], nl, ng, single_bound(s, sh));
   } else {
     table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, s.mcp[q], nl, ng);
   }
@@ -1021,6 +1047,34 @@ __device__ __forceinline__ void table_patch(const Scenario& s, int t, int v, dou
 // is loaded once and patched in registers. Rows of empty bases outside the
 // pool are kept current too (harmless; they are rebuilt fresh or patched
 // the same way when they enter it).
+// Entry pair (t, loser), (t, gain) of one empty base, values already loaded.
+__device__ __forceinline__ void subst_entry(const Scenario& s, int t, double c, double Al,
+                                            double El, double Ul, double Ag, double Eg, double Ug,
+                                            int loser, int gain, bool fl, bool fg, double mc_old,
+                                            double mc_new, int nl, int ng, double bt) {
+  const bool heli = s.bheli[t];
+  const long long kl = tix(s, t, loser), kg = tix(s, t, gain);
+  int delta = 0;
+  if (!(fl && heli)) delta -= table_unsettled(Al, El, Ul, nl, bt);
+  if (!(fg && heli)) delta -= table_unsettled(Ag, Eg, Ug, ng, bt);
+  const double dl = c - mc_old, dg = c - mc_new;
+  Al -= dl;
+  El += 2.0 * kTwoPowM52 * (fabs(dl) + fabs(Al));
+  Ul = fmax(0.0, Ul - fabs(dl)) + 2.0 * kTwoPowM52 * Ul;
+  Ag += dg;
+  Eg += 2.0 * kTwoPowM52 * (fabs(dg) + fabs(Ag));
+  Ug = (Ug + fabs(dg)) * (1.0 + 2.0 * kTwoPowM52);
+  if (!(fl && heli)) delta += table_unsettled(Al, El, Ul, nl - 1, bt);
+  if (!(fg && heli)) delta += table_unsettled(Ag, Eg, Ug, ng + 1, bt);
+  s.rA[kl] = Al;
+  s.rE[kl] = El;
+  s.rU[kl] = Ul;
+  s.rA[kg] = Ag;
+  s.rE[kg] = Eg;
+  s.rU[kg] = Ug;
+  if (delta) s.rcnt[t] += delta;
+}
+
 template <int NT>
 __device__ void table_after_substitution(const Scenario& s, const Shared& sh, int j, int loser,
                                          int gain, double mc_old, double mc_new, int nl, int ng) {
@@ -1028,30 +1082,10 @@ __device__ void table_after_substitution(const Scenario& s, const Shared& sh, in
   const bool fl = s.vfixed[loser], fg = s.vfixed[gain];
   for (int t = threadIdx.x; t < s.B; t += NT) {
     if (s.bveh[t] >= 0) continue;
-    const bool heli = s.bheli[t];
     const double c = cost_mb(s, j, t);
     const long long kl = tix(s, t, loser), kg = tix(s, t, gain);
-    double Al = s.rA[kl], El = s.rE[kl], Ul = s.rU[kl];
-    double Ag = s.rA[kg], Eg = s.rE[kg], Ug = s.rU[kg];
-    int delta = 0;
-    if (!(fl && heli)) delta -= table_unsettled(Al, El, Ul, nl, bt);
-    if (!(fg && heli)) delta -= table_unsettled(Ag, Eg, Ug, ng, bt);
-    const double dl = c - mc_old, dg = c - mc_new;
-    Al -= dl;
-    El += 2.0 * kTwoPowM52 * (fabs(dl) + fabs(Al));
-    Ul = fmax(0.0, Ul - fabs(dl)) + 2.0 * kTwoPowM52 * Ul;
-    Ag += dg;
-    Eg += 2.0 * kTwoPowM52 * (fabs(dg) + fabs(Ag));
-    Ug = (Ug + fabs(dg)) * (1.0 + 2.0 * kTwoPowM52);
-    if (!(fl && heli)) delta += table_unsettled(Al, El, Ul, nl - 1, bt);
-    if (!(fg && heli)) delta += table_unsettled(Ag, Eg, Ug, ng + 1, bt);
-    s.rA[kl] = Al;
-    s.rE[kl] = El;
-    s.rU[kl] = Ul;
-    s.rA[kg] = Ag;
-    s.rE[kg] = Eg;
-    s.rU[kg] = Ug;
-    if (delta) s.rcnt[t] += delta;
+    subst_entry(s, t, c, s.rA[kl], s.rE[kl], s.rU[kl], s.rA[kg], s.rE[kg], s.rU[kg], loser, gain,
+                fl, fg, mc_old, mc_new, nl, ng, bt);
   }
 }
 

@@ -20,7 +20,11 @@ sample (first `REF_PASSES` passes of the same search) per step.
 
 Multi-GPU (torchrun): the single-instance search does not shard (SURVEY.md
 §8e: "c1/c2 replicas only"); each rank runs an independent replica, value =
-total evaluations of all ranks / max over ranks of the device time.
+total evaluations of all ranks / max over ranks of the device time. Two more
+workloads run on every rank (unless --no-extras): `c4_sharded_table_rank`
+(c4's table build + ranking with the missions sharded over the ranks, the
+column-total chains handed on over NCCL) and `c5_batch` (512 independent c5
+scenarios per GPU, so N = 8 is the whole 4096-scenario batch).
 """
 from __future__ import annotations
 
@@ -224,9 +228,12 @@ def run_ours(args) -> None:
         "clocks": clocks,
     }
     if not args.no_extras:
-        sh = sharded_rank_workload(ws, rank, local)  # every rank takes part
+        # every rank takes part in these two
+        sh = sharded_rank_workload(ws, rank, local)
+        c5 = c5_batch_workload(ws, rank, local)
         if rank == 0:
             line["c4_sharded_table_rank"] = sh
+            line["c5_batch"] = c5
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(inst, host_cost, start, pk, px)
     if rank == 0 and not args.no_extras:
@@ -348,6 +355,47 @@ def sharded_rank_workload(ws: int, rank: int, local: int, reps: int = 2) -> dict
                       "max over ranks"}
 
 
+def c5_batch_workload(ws: int, rank: int, local: int, per_rank: int = 512) -> dict:
+    """c5: independent 200 x 5k x 20 scenarios (seeds 1 + k), tabu to
+    quiescence, scenario-sharded over the ranks with no collective on the
+    data path (dist.run_sharded): 512 scenarios per GPU, so
+    N = 8 runs the whole 4096-scenario batch. Each rank prepares its own
+    scenarios' tables and starts (untimed), then one fp_search_batch launch
+    on its GPU; time = max over ranks of the library's CUDA-event time."""
+    from paper_2001_05291_b200 import fleetplace as F
+    from paper_2001_05291_b200.dist import run_sharded
+
+    n = per_rank * ws
+
+    def solve(rg):
+        insts, starts, tabs = [], [], []
+        for k in rg:
+            ik = F.survey_instance(200, 5000, 20, seed=1 + k)
+            tk = F.build_distance_table(ik, device=local)
+            sk = F.rank_bases(ik, tk)
+            insts.append(ik)
+            starts.append(F._state_arrays(sk.assignment, F.initial_pool(sk, ik), ik))
+            tabs.append(np.ascontiguousarray(tk.cost.T).reshape(-1))
+            del tk
+        res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu), tabs,
+                             device=local)
+        out = [(x.stats.evaluations, x.stats.passes, x.stats.applied_moves,
+                x.stats.final_objective_km) for x in res]
+        return out, res[0].stats.device_ms / 1e3
+
+    allres, tmax = run_sharded(n, solve)
+    if rank != 0:
+        return {}
+    ev = sum(r[0] for r in allres)
+    return {"workload": f"{n} of the 4096 c5 scenarios (200 x 5k x 20, seeds 1..{n}), tabu to "
+                        f"quiescence, {per_rank} per GPU over {ws} GPU(s)",
+            "search_ms": tmax * 1e3, "scenarios": n, "evaluations": ev,
+            "move_evals_per_s": ev / tmax, "passes_max": max(r[1] for r in allres),
+            "applied_moves": sum(r[2] for r in allres),
+            "objective_sum_km": float(sum(r[3] for r in allres)),
+            "timing": "library CUDA events around the batch launch, max over ranks"}
+
+
 def _c4_sweep_roofline(extra: dict, peak: float) -> dict:
     """SURVEY.md §8(d)'s roofline target: the full neighbourhood sweep at c4
     -- every cost column once (the V occupied-base columns score every
@@ -371,9 +419,8 @@ def _c4_sweep_roofline(extra: dict, peak: float) -> dict:
 def extra_workloads(device: int) -> dict:
     """The other BASELINE.json shapes on this GPU (reported, not the headline):
     c3 (2k x 100k x 100) capped at 10 passes and to quiescence, c4 (5k x 1M x 250, a 40 GB
-    table) capped at 1 pass, and one GPU's share of the c5 batch (512 of the
-    4096 independent 200 x 5k x 20 scenarios) to quiescence. Device times from
-    the library's CUDA events."""
+    table) capped at 1 pass, and c1 to quiescence. (The c5 batch runs on every
+    rank: c5_batch_workload.) Device times from the library's CUDA events."""
     from paper_2001_05291_b200 import fleetplace as F
 
     peak, _ = _peaks()
@@ -423,25 +470,6 @@ def extra_workloads(device: int) -> dict:
         "evaluations": r1.stats.evaluations, "applied_moves": r1.stats.applied_moves,
         "final_objective_km": r1.stats.final_objective_km}
     del t1
-    n = 512
-    insts, starts, tabs = [], [], []
-    for k in range(n):
-        ik = F.survey_instance(200, 5000, 20, seed=1 + k)
-        tk = F.build_distance_table(ik, device=device)
-        sk = F.rank_bases(ik, tk)
-        insts.append(ik)
-        starts.append(F._state_arrays(sk.assignment, F.initial_pool(sk, ik), ik))
-        tabs.append(np.ascontiguousarray(tk.cost.T).reshape(-1))
-        del tk
-    res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu), tabs,
-                         device=device)
-    ev = sum(x.stats.evaluations for x in res)
-    ms = res[0].stats.device_ms
-    out["c5_share_512"] = {
-        "workload": "512 of the 4096 c5 scenarios (200 x 5k x 20, seeds 1..512), tabu to quiescence",
-        "search_ms": ms, "evaluations": ev, "move_evals_per_s": ev / (ms / 1e3),
-        "passes_max": max(x.stats.passes for x in res),
-        "applied_moves": sum(x.stats.applied_moves for x in res)}
     return out
 
 

@@ -42,8 +42,17 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     cmds = [[NVCC, *flags, "-c", str(CSRC / s), "-o", str(LIB_DIR / (s + ".o"))] for s in SOURCES]
     cmds.append([NVCC, *ARCH, "-shared", *[str(LIB_DIR / (s + ".o")) for s in SOURCES],
                  "-o", str(LIB)])
+    headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + [ROOT / "include" / "fleetplace_b200.h"]
+    newest_h = max(h.stat().st_mtime for h in headers)
+
+    def run(c):
+        src, obj = Path(c[-3]), Path(c[-1])
+        if not force and obj.exists() and obj.stat().st_mtime > max(src.stat().st_mtime, newest_h):
+            return subprocess.CompletedProcess(c, 0, "", "(up to date)\n")
+        return subprocess.run(c, capture_output=True, text=True)
+
     with ThreadPoolExecutor(len(SOURCES)) as ex:
-        rs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds[:-1]))
+        rs = list(ex.map(run, cmds[:-1]))
     if all(r.returncode == 0 for r in rs):
         rs.append(subprocess.run(cmds[-1], capture_output=True, text=True))
     log = "".join(" ".join(c) + "\n" + r.stdout + r.stderr for c, r in zip(cmds, rs))

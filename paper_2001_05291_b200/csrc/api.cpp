@@ -509,7 +509,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // while the device runs the previous chunk.
   // (single scenarios: one block rebuilding its bitsets is slower than the
   // grid-wide sweep plus a relaunch once V*M passes 64K)
-  const bool inkernel = n > 1 || (long long)maxV * M <= (64ll << 10);
+  bool inkernel = n > 1 || (long long)maxV * M <= (64ll << 10);
+  if (const char* e = std::getenv("FLEETPLACE_INKERNEL")) inkernel = n > 1 || std::atoi(e) != 0;
   // passes per host round trip: in-kernel mode runs them in one launch; the
   // sweep mode enqueues (sweep, pass) launch pairs that exit at once when the
   // scenario is done, so the host only synchronises once per chunk

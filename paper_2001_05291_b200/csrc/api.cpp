@@ -1018,11 +1018,12 @@ fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* in, double rad
     check(fpk::launch_point_cos(plat, M, cosv + B, st), "cos(pickups)");
     check(fpk::launch_point_cos(dlat, M, cosv + B + M, st), "cos(deliveries)");
     EvTimer tk(st);
-    check(fpk::launch_table(blat, blon, cosv, B, plat, plon, cosv + B, dlat, dlon, cosv + B + M,
-                            M, radius_km, ctx->d_cost, st),
+    int sites = 0;
+    check(fpk::launch_table_auto(blat, blon, cosv, B, plat, plon, cosv + B, dlat, dlon,
+                                 cosv + B + M, M, radius_km, ctx->d_cost, st, &sites),
           "table_kernel");
     ctx->last_kernel_ms = tk.stop_ms();
-    ctx->launches += 4;
+    ctx->launches += sites ? 10 : 4;
     start_costT(ctx);
     if (out_cost) d2h(out_cost, ctx->d_cost, (size_t)M * B, st);
     check(cudaStreamSynchronize(st), "table sync");

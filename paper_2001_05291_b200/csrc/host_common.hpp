@@ -24,6 +24,10 @@ cudaError_t launch_table(const double* blat, const double* blon, const double* b
                          const double* plat, const double* plon, const double* pcos,
                          const double* dlat, const double* dlon, const double* dcos, int M,
                          double radius_km, double* cost, cudaStream_t st);
+cudaError_t launch_table_auto(const double* blat, const double* blon, const double* bcos, int B,
+                              const double* plat, const double* plon, const double* pcos,
+                              const double* dlat, const double* dlon, const double* dcos, int M,
+                              double radius_km, double* cost, cudaStream_t st, int* used_sites);
 cudaError_t launch_haversine_pairs(int n, const double* alat, const double* alon,
                                    const double* blat, const double* blon, const double* clat,
                                    const double* clon, double radius_km, double* out,

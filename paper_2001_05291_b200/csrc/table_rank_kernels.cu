@@ -15,6 +15,10 @@
 
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 
@@ -60,6 +64,143 @@ __global__ void __launch_bounds__(256)
     const double la = blat[b], lo = blon[b], ca = bcos[b];
     const double c = __dadd_rn(hav(la, lo, ca, pl, po, pc, two_r), hav(la, lo, ca, dl, d_o, dc, two_r));
     cost[(long long)b * M + m] = c;
+  }
+}
+
+// ---- kernel (1) over distinct points ---------------------------------------
+// mission_cost_km(b, m) = hav(b, pickup_m) + hav(b, delivery_m) depends on the
+// point coordinates only, and generated missions draw both ends from S health
+// sites (proj/src/data.cpp:140-180: S·(S-1) ordered pairs), so the 2·B·M
+// haversines of the table repeat: c4 has 2M mission ends but <= 20k distinct
+// points. The distinct points (exact bit equality of (lat, lon)) are found
+// on the device with two stable radix sorts; H(b, u) is computed once per
+// (base, distinct point) by the same hav() on the same operand bits, and the
+// table is then a gather + one add per entry: cost(m, b) =
+// H(b, pickup_m) + H(b, delivery_m), bit-identical to table_kernel (same
+// operations in the same order on the same values) and HBM-write-bound.
+
+__global__ void point_keys_kernel(const double* __restrict__ plat, const double* __restrict__ plon,
+                                  const double* __restrict__ dlat, const double* __restrict__ dlon,
+                                  int M, unsigned long long* __restrict__ klat,
+                                  unsigned long long* __restrict__ klon, int32_t* __restrict__ idx) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= 2 * M) return;
+  const double la = k < M ? plat[k] : dlat[k - M];
+  const double lo = k < M ? plon[k] : dlon[k - M];
+  klat[k] = (unsigned long long)__double_as_longlong(la);
+  klon[k] = (unsigned long long)__double_as_longlong(lo);
+  idx[k] = k;
+}
+
+__global__ void gather_keys_kernel(const unsigned long long* __restrict__ src,
+                                   const int32_t* __restrict__ idx, int n,
+                                   unsigned long long* __restrict__ dst) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) dst[k] = src[idx[k]];
+}
+
+// flag[k] = sorted point k starts a new distinct (lat, lon)
+__global__ void distinct_flags_kernel(const unsigned long long* __restrict__ klat,
+                                      const unsigned long long* __restrict__ klon,
+                                      const int32_t* __restrict__ order, int n,
+                                      int32_t* __restrict__ flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int a = order[k];
+  flag[k] = k == 0 || klat[a] != klat[order[k - 1]] || klon[a] != klon[order[k - 1]];
+}
+
+__global__ void distinct_scatter_kernel(const unsigned long long* __restrict__ klat,
+                                        const unsigned long long* __restrict__ klon,
+                                        const int32_t* __restrict__ order,
+                                        const int32_t* __restrict__ flag,
+                                        const int32_t* __restrict__ uid1, int n,
+                                        int32_t* __restrict__ pid, double* __restrict__ ulat,
+                                        double* __restrict__ ulon) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int a = order[k], u = uid1[k] - 1;
+  pid[a < n / 2 ? 2 * a : 2 * (a - n / 2) + 1] = u;  // (pickup, delivery) pairs
+  if (flag[k]) {
+    ulat[u] = __longlong_as_double((long long)klat[a]);
+    ulon[u] = __longlong_as_double((long long)klon[a]);
+  }
+}
+
+// H[b * U + u] = hav(base b, distinct point u)
+__global__ void __launch_bounds__(256)
+    site_hav_kernel(const double* __restrict__ blat, const double* __restrict__ blon,
+                    const double* __restrict__ bcos, int B, const double* __restrict__ ulat,
+                    const double* __restrict__ ulon, const double* __restrict__ ucos, int U,
+                    double two_r, double* __restrict__ H) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (u >= U || b >= B) return;
+  H[(long long)b * U + u] = hav(blat[b], blon[b], bcos[b], ulat[u], ulon[u], ucos[u], two_r);
+}
+
+// cost[b*M + m] = H(b, pickup_m) + H(b, delivery_m) with R bases' H rows in
+// shared memory (R consecutive bases per block, a chunk of missions): each
+// mission's (pickup, delivery) pair is loaded once for R columns, four
+// missions per thread in flight; coalesced column stores.
+template <int R>
+__global__ void __launch_bounds__(1024)
+    table_gather_smem_kernel(const double* __restrict__ H, int U, int B,
+                             const int2* __restrict__ pd, int M, int chunk,
+                             double* __restrict__ cost) {
+  extern __shared__ double hs[];
+  const int b0 = blockIdx.x * R;
+  const int nb = min(R, B - b0);
+  const double* h = H + (long long)b0 * U;  // rows b0 .. b0+nb-1 are contiguous
+  {
+    // the rows: eight independent loads in flight per thread
+    const int n = nb * U, bd = blockDim.x;
+    int k = threadIdx.x;
+    for (; k + 7 * bd < n; k += 8 * bd) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = h[k + u * bd];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) hs[k + u * bd] = v[u];
+    }
+    for (; k < n; k += bd) hs[k] = h[k];
+  }
+  __syncthreads();
+  const int m0 = blockIdx.y * chunk, m1 = min(M, m0 + chunk);
+  constexpr int UN = 8;
+  for (int m = m0 + threadIdx.x; m < m1; m += UN * blockDim.x) {
+    int2 p[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int mm = m + u * blockDim.x;
+      p[u] = mm < m1 ? pd[mm] : make_int2(0, 0);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < nb) {
+        double* col = cost + (long long)(b0 + r) * M;
+        const double* hr = hs + r * U;
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          const int mm = m + u * blockDim.x;
+          if (mm < m1) col[mm] = __dadd_rn(hr[p[u].x], hr[p[u].y]);
+        }
+      }
+    }
+  }
+}
+
+// The same with the H row read through L1 / L2 (rows too long for smem).
+__global__ void __launch_bounds__(1024)
+    table_gather_kernel(const double* __restrict__ H, int U, const int2* __restrict__ pd, int M,
+                        int chunk, double* __restrict__ cost) {
+  const int b = blockIdx.x;
+  const double* h = H + (long long)b * U;
+  const int m0 = blockIdx.y * chunk, m1 = min(M, m0 + chunk);
+  double* col = cost + (long long)b * M;
+  for (int m = m0 + threadIdx.x; m < m1; m += blockDim.x) {
+    const int2 p = pd[m];
+    col[m] = __dadd_rn(h[p.x], h[p.y]);
   }
 }
 
@@ -169,6 +310,125 @@ cudaError_t launch_table(const double* blat, const double* blon, const double* b
   dim3 grid((M + 255) / 256, (B + bpb - 1) / bpb);
   table_kernel<<<grid, 256, 0, st>>>(blat, blon, bcos, B, plat, plon, pcos, dlat, dlon, dcos, M,
                                      2.0 * radius_km, bpb, cost);
+  return cudaGetLastError();
+}
+
+// Kernel (1) through the distinct points when they are few (auto: B*M >= 64M
+// entries, U <= M/2 and H fits in 4 GB; FLEETPLACE_TABLE_SITES=0/1 forces
+// either path). The
+// direct table_kernel otherwise. *used_sites reports the path taken.
+cudaError_t launch_table_auto(const double* blat, const double* blon, const double* bcos, int B,
+                              const double* plat, const double* plon, const double* pcos,
+                              const double* dlat, const double* dlon, const double* dcos, int M,
+                              double radius_km, double* cost, cudaStream_t st, int* used_sites) {
+  *used_sites = 0;
+  if (B <= 0 || M <= 0) return cudaSuccess;
+  int force = -1;
+  if (const char* e = std::getenv("FLEETPLACE_TABLE_SITES")) force = std::atoi(e) != 0;
+  // small tables: the direct kernel takes ~0.1 ms, below the dedupe's cost
+  if (force == 0 || 2ll * M >= INT_MAX / 2 || (force < 0 && (long long)B * M < (64ll << 20)))
+    return launch_table(blat, blon, bcos, B, plat, plon, pcos, dlat, dlon, dcos, M, radius_km, cost, st);
+  const int n = 2 * M;
+  {
+    // keep freed stream-ordered allocations mapped (H is up to 4 GB): repeated
+    // builds must not pay the physical mapping again
+    static bool pool_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !pool_set[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long keep = 6ull << 30;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      pool_set[dev] = true;
+    }
+  }
+  // workspace: keys x4, idx x4, flag, uid, pid, ulat, ulon, ucos, + cub temp
+  size_t t_sort = 0, t_scan = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (unsigned long long*)nullptr,
+                                  (unsigned long long*)nullptr, (int32_t*)nullptr,
+                                  (int32_t*)nullptr, n, 0, 64, st);
+  cub::DeviceScan::InclusiveSum(nullptr, t_scan, (int32_t*)nullptr, (int32_t*)nullptr, n, st);
+  const size_t tmp = std::max(t_sort, t_scan);
+  const size_t bytes = 4ull * n * 8 + 6ull * n * 4 + 3ull * n * 8 + tmp + 14 * 256;
+  char* w = nullptr;
+  cudaError_t err = cudaMallocAsync(&w, bytes, st);
+  if (err != cudaSuccess) return err;
+  auto carve = [&](size_t b) {
+    char* p = w;
+    w += (b + 255) & ~size_t(255);
+    return p;
+  };
+  char* base = w;
+  auto* klat = (unsigned long long*)carve(8ull * n);
+  auto* klon = (unsigned long long*)carve(8ull * n);
+  auto* klon_s = (unsigned long long*)carve(8ull * n);
+  auto* klat2 = (unsigned long long*)carve(8ull * n);
+  auto* idx = (int32_t*)carve(4ull * n);
+  auto* idx1 = (int32_t*)carve(4ull * n);
+  auto* idx2 = (int32_t*)carve(4ull * n);
+  auto* flag = (int32_t*)carve(4ull * n);
+  auto* uid = (int32_t*)carve(4ull * n);
+  auto* pid = (int32_t*)carve(4ull * n);
+  auto* ulat = (double*)carve(8ull * n);
+  auto* ulon = (double*)carve(8ull * n);
+  auto* ucos = (double*)carve(8ull * n);
+  void* ctmp = carve(tmp);
+  (void)base;
+  const int g = (n + 255) / 256;
+  point_keys_kernel<<<g, 256, 0, st>>>(plat, plon, dlat, dlon, M, klat, klon, idx);
+  size_t tb = tmp;
+  cub::DeviceRadixSort::SortPairs(ctmp, tb, klon, klon_s, idx, idx1, n, 0, 64, st);
+  gather_keys_kernel<<<g, 256, 0, st>>>(klat, idx1, n, klat2);
+  tb = tmp;
+  // stable: equal latitudes keep their longitude order -> (lat, lon) order
+  cub::DeviceRadixSort::SortPairs(ctmp, tb, klat2, klon_s /* keys out, reused */, idx1, idx2, n,
+                                  0, 64, st);
+  distinct_flags_kernel<<<g, 256, 0, st>>>(klat, klon, idx2, n, flag);
+  tb = tmp;
+  cub::DeviceScan::InclusiveSum(ctmp, tb, flag, uid, n, st);
+  distinct_scatter_kernel<<<g, 256, 0, st>>>(klat, klon, idx2, flag, uid, n, pid, ulat, ulon);
+  int U = 0;
+  cudaMemcpyAsync(&U, uid + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+  err = cudaStreamSynchronize(st);
+  if (err != cudaSuccess) return err;
+  const size_t hbytes = 8ull * B * (size_t)U;
+  if (force != 1 && (U > M / 2 || hbytes > (4ull << 30))) {
+    cudaFreeAsync(base, st);
+    return launch_table(blat, blon, bcos, B, plat, plon, pcos, dlat, dlon, dcos, M, radius_km, cost, st);
+  }
+  double* H = nullptr;
+  err = cudaMallocAsync(&H, hbytes, st);
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    cudaFreeAsync(base, st);
+    return launch_table(blat, blon, bcos, B, plat, plon, pcos, dlat, dlon, dcos, M, radius_km, cost, st);
+  }
+  point_cos_kernel<<<min(1184, (U + 255) / 256), 256, 0, st>>>(ulat, U, ucos);
+  site_hav_kernel<<<dim3((U + 255) / 256, B), 256, 0, st>>>(blat, blon, bcos, B, ulat, ulon, ucos,
+                                                            U, 2.0 * radius_km, H);
+  const size_t row = 8ull * U, cap = 200u << 10;
+  const int R = row * 8 <= cap ? 8 : row * 4 <= cap ? 4 : row * 2 <= cap ? 2 : row <= cap ? 1 : 0;
+  // about eight blocks per SM in all, each block's rows loaded once
+  const int nbb = (B + std::max(R, 1) - 1) / std::max(R, 1);
+  const int chunks = std::max(1, std::min((M + 8191) / 8192, (8 * 148 + nbb - 1) / nbb));
+  const int chunk = (M + chunks - 1) / chunks;
+  auto go = [&](auto kern, int r) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(row * r));
+    kern<<<dim3((B + r - 1) / r, (M + chunk - 1) / chunk), 1024, row * r, st>>>(
+        H, U, B, (const int2*)pid, M, chunk, cost);
+  };
+  if (R == 8) go(table_gather_smem_kernel<8>, 8);
+  else if (R == 4) go(table_gather_smem_kernel<4>, 4);
+  else if (R == 2) go(table_gather_smem_kernel<2>, 2);
+  else if (R == 1) go(table_gather_smem_kernel<1>, 1);
+  else
+    table_gather_kernel<<<dim3(B, (M + chunk - 1) / chunk), 1024, 0, st>>>(H, U, (const int2*)pid,
+                                                                          M, chunk, cost);
+  cudaFreeAsync(H, st);
+  cudaFreeAsync(base, st);
+  *used_sites = 1;
   return cudaGetLastError();
 }
 

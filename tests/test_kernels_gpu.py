@@ -325,3 +325,48 @@ def test_table_upload_into_a_live_context():
     got = F.search_arrays(b, ta, cfg, vb, mv, pk, px)
     assert _stats_key(got) == _stats_key(want)
     assert np.array_equal(got.mission_vehicle, want.mission_vehicle)
+
+
+def _table_bytes(inst):
+    t = F.build_distance_table(inst)
+    return np.ascontiguousarray(t.cost.T).tobytes()
+
+
+@pytest.mark.parametrize("shape", [(50, 200, 10), (500, 10000, 40), (2000, 40000, 100)])
+def test_table_distinct_point_path_bit_identical(shape, monkeypatch):
+    """Kernel (1) through the distinct mission points (H(b, u) once per base
+    and distinct point, then a gather + add per entry) equals the direct
+    per-entry kernel bit for bit."""
+    inst = F.survey_instance(*shape, seed=2)
+    monkeypatch.setenv("FLEETPLACE_TABLE_SITES", "0")
+    direct = _table_bytes(inst)
+    monkeypatch.setenv("FLEETPLACE_TABLE_SITES", "1")
+    assert _table_bytes(inst) == direct
+    monkeypatch.delenv("FLEETPLACE_TABLE_SITES")
+    assert _table_bytes(inst) == direct  # auto picks the distinct-point path here
+
+
+def test_table_distinct_point_path_edge_points(monkeypatch):
+    """All-distinct random points (auto falls back to the direct kernel),
+    +0.0 / -0.0 and repeated coordinates, one mission, pickup == delivery."""
+    rng = np.random.default_rng(11)
+    M = 3000
+    la = rng.uniform(-89, 89, size=(2, M))
+    lo = rng.uniform(-179, 179, size=(2, M))
+    la[:, :50] = 0.0
+    la[0, 50:100] = -0.0
+    lo[1, 100:200] = lo[0, 100:200]
+    la[1, 100:200] = la[0, 100:200]
+    la[0, 300:900] = la[0, 200]
+    lo[0, 300:900] = lo[0, 200]
+    inst = F.Instance.from_arrays(
+        np.arange(7), np.array([0, 1, 0, 1, 0, 0, 1]), rng.uniform(-60, 60, 7), rng.uniform(-170, 170, 7),
+        np.arange(3), np.array([0, 1, 0]), np.arange(M), la[0], lo[0], la[1], lo[1],
+        np.zeros(M, np.uint8))
+    for sub in (inst, inst.mission_slice(0, 1)):
+        monkeypatch.setenv("FLEETPLACE_TABLE_SITES", "0")
+        direct = _table_bytes(sub)
+        monkeypatch.setenv("FLEETPLACE_TABLE_SITES", "1")
+        assert _table_bytes(sub) == direct
+        monkeypatch.delenv("FLEETPLACE_TABLE_SITES")
+        assert _table_bytes(sub) == direct

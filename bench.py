@@ -236,6 +236,8 @@ def run_ours(args) -> None:
             line["c5_batch"] = c5
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(inst, host_cost, start, pk, px)
+        if not args.no_extras:
+            line["cpu_baseline_c5"] = cpu_baseline_c5()
     if rank == 0 and not args.no_extras:
         line["extra_workloads"] = extra_workloads(local)
         line["roofline_c4_sweep"] = _c4_sweep_roofline(line["extra_workloads"], _peaks()[0])
@@ -514,6 +516,50 @@ def cpu_baseline(inst, host_cost, start, pk, px, passes: int = REF_PASSES) -> di
     return {"value": s.stats[1] / s.seconds, "unit": UNIT, "cores": 1, "kind": "reference",
             "sample": f"first {passes} passes of the same c2 tabu_search (sequential reference, "
                       f"{s.stats[1]} evaluations in {s.seconds:.2f} s)"}
+
+
+def cpu_baseline_c5(passes: int = 3) -> dict:
+    """c5's CPU baseline runs independent scenarios on all
+    host cores, one per core. The unmodified reference (oracle/_ref), one
+    c5 scenario (seed 1 + k) per core concurrently (ctypes releases the GIL),
+    each bounded to its first `passes` passes; aggregate evaluations / wall."""
+    import concurrent.futures as cf
+    import platform
+
+    H = _ref_lib()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+    def prep(k):
+        inst = H.ref_survey_instance(200, 5000, 20, seed=1 + k)
+        cost = H.ref_table(inst)
+        r = H.ref_rank(inst, cost)
+        pk, px = H.initial_pool_idx(inst, r.vehicle_base, r.mission_vehicle, r.unused)
+        return inst, cost, r, pk, px
+
+    with cf.ThreadPoolExecutor(cores) as ex:
+        scn = list(ex.map(prep, range(cores)))
+
+        def run(a):
+            inst, cost, r, pk, px = a
+            return H.ref_search(inst, cost, 1, 7, r.vehicle_base, r.mission_vehicle, pk, px,
+                                max_passes=passes)
+
+        t0 = time.perf_counter()
+        res = list(ex.map(run, scn))
+        wall = time.perf_counter() - t0
+    ev = sum(x.stats[1] for x in res)
+    cpu = platform.processor() or platform.machine()
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"value": ev / wall, "unit": UNIT, "cores": cores, "kind": "reference",
+            "cpu": cpu,
+            "sample": f"{cores} c5 scenarios (200 x 5k x 20, seeds 1..{cores}), one per core "
+                      f"concurrently, first {passes} passes each: {ev} evaluations in {wall:.2f} s"}
 
 
 def run_reference(args) -> None:

@@ -418,9 +418,17 @@ def _c4_sweep_roofline(extra: dict, peak: float) -> dict:
     alg = 8 * B * M + 16 * M
     ach = alg / (ms / 1e3) / 1e9
     return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "traffic": None, "ms": ms, "bytes": alg, "kernels": parts,
+            "traffic": _sweep_traffic(), "ms": ms, "bytes": alg, "kernels": parts,
             "note": "one full neighbourhood sweep per search start; per pass the device "
                     "keeps the sweep's results current incrementally (DESIGN.md §3)"}
+
+
+def _sweep_traffic():
+    """DRAM bytes of one c4 sweep (impt_init + rows_stream) from the committed
+    ncu capture (profiles/r1_c4_sweep_traffic.json): 1.09x the algorithmic
+    bytes (the occupied bases' row-major rows and mc are read too)."""
+    f = ROOT / "profiles" / "r1_c4_sweep_traffic.json"
+    return json.loads(f.read_text())["dram_bytes_per_sweep"] if f.exists() else None
 
 
 def _rebuild(t, inst) -> None:

@@ -384,11 +384,20 @@ def c5_batch_workload(ws: int, rank: int, local: int, per_rank: int = 512) -> di
             starts.append(F._state_arrays(sk.assignment, F.initial_pool(sk, ik), ik))
             tabs.append(np.ascontiguousarray(tk.cost.T).reshape(-1))
             del tk
-        res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu), tabs,
-                             device=local)
-        out = [(x.stats.evaluations, x.stats.passes, x.stats.applied_moves,
-                x.stats.final_objective_km) for x in res]
-        return out, res[0].stats.device_ms / 1e3
+        # three identical launches, median reported: the batch time varies
+        # run to run (which scenarios share an SM and when the long ones
+        # start) while the results do not
+        times, out = [], None
+        for _ in range(3):
+            res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu),
+                                 tabs, device=local)
+            o = [(x.stats.evaluations, x.stats.passes, x.stats.applied_moves,
+                  x.stats.final_objective_km) for x in res]
+            assert out is None or o == out, "c5 batch results changed between launches"
+            out = o
+            times.append(res[0].stats.device_ms / 1e3)
+        solve.spread_ms = (min(times) * 1e3, max(times) * 1e3)
+        return out, sorted(times)[1]
 
     allres, tmax = run_sharded(n, solve)
     if rank != 0:
@@ -400,7 +409,9 @@ def c5_batch_workload(ws: int, rank: int, local: int, per_rank: int = 512) -> di
             "move_evals_per_s": ev / tmax, "passes_max": max(r[1] for r in allres),
             "applied_moves": sum(r[2] for r in allres),
             "objective_sum_km": float(sum(r[3] for r in allres)),
-            "timing": "library CUDA events around the batch launch, max over ranks"}
+            "rank0_min_max_ms": list(getattr(solve, "spread_ms", ())),
+            "timing": "library CUDA events around the batch launch, median of 3 identical "
+                      "launches, max over ranks"}
 
 
 def _c4_sweep_roofline(extra: dict, peak: float) -> dict:

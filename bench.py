@@ -384,18 +384,21 @@ def c5_batch_workload(ws: int, rank: int, local: int, per_rank: int = 512) -> di
             starts.append(F._state_arrays(sk.assignment, F.initial_pool(sk, ik), ik))
             tabs.append(np.ascontiguousarray(tk.cost.T).reshape(-1))
             del tk
-        # three identical launches, median reported: the batch time varies
-        # run to run (which scenarios share an SM and when the long ones
-        # start) while the results do not
+        # one long-lived context (as a serving process keeps one: its
+        # workspace is reused), one warm-up launch, then three identical
+        # launches, median reported (fresh contexts run
+        # 268-316 ms, a warm one 232-235 ms; the results never change)
+        ctx = F._Ctx(local)
         times, out = [], None
-        for _ in range(3):
+        for it in range(4):
             res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu),
-                                 tabs, device=local)
+                                 tabs, device=local, ctx=ctx)
             o = [(x.stats.evaluations, x.stats.passes, x.stats.applied_moves,
                   x.stats.final_objective_km) for x in res]
             assert out is None or o == out, "c5 batch results changed between launches"
             out = o
-            times.append(res[0].stats.device_ms / 1e3)
+            if it > 0:
+                times.append(res[0].stats.device_ms / 1e3)
         solve.spread_ms = (min(times) * 1e3, max(times) * 1e3)
         return out, sorted(times)[1]
 
@@ -410,8 +413,8 @@ def c5_batch_workload(ws: int, rank: int, local: int, per_rank: int = 512) -> di
             "applied_moves": sum(r[2] for r in allres),
             "objective_sum_km": float(sum(r[3] for r in allres)),
             "rank0_min_max_ms": list(getattr(solve, "spread_ms", ())),
-            "timing": "library CUDA events around the batch launch, median of 3 identical "
-                      "launches, max over ranks"}
+            "timing": "library CUDA events around the batch launch on a long-lived context, "
+                      "1 warm-up + median of 3 identical launches, max over ranks"}
 
 
 def _c4_sweep_roofline(extra: dict, peak: float) -> dict:

@@ -801,14 +801,16 @@ def small_generated(seed: int, missions: int = 10, aerodromes: int = 12, helipad
 # ------------------------------------------------------------------ batch ----
 def search_batch(insts: Sequence[Instance], starts: Sequence[tuple], cfg: SearchConfig,
                  tables: Optional[Sequence[Optional[np.ndarray]]] = None,
-                 device: int = 0) -> list:
+                 device: int = 0, ctx: Optional["_Ctx"] = None) -> list:
     """Independent scenarios of one mission count searched concurrently, one
     thread block per scenario (C ABI fp_search_batch). `starts[s]` is the
     index-form start (vehicle_base, mission_vehicle, pool_kind, pool_index);
     `tables[s]` a flat column-major host table or None to build it on the
-    device. Returns one SearchResult per scenario."""
+    device. `ctx`: a long-lived context (`_Ctx(device)`) whose workspace is
+    reused across batches, as a serving process keeps one; default a fresh
+    one per call. Returns one SearchResult per scenario."""
     n = len(insts)
-    ctx = _Ctx(device)
+    ctx = ctx if ctx is not None else _Ctx(device)
     ci = (A.fp_instance * n)(*[x.c() for x in insts])
     keep = []
     tp = (C.POINTER(C.c_double) * n)()

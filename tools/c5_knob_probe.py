@@ -20,6 +20,7 @@ for k in range(n):
     tabs.append(np.ascontiguousarray(tk.cost.T).reshape(-1))
     del tk
 cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu)
+CTX = F._Ctx(0) if os.environ.get("C5_KEEP_CTX") else None
 KNOBS = ("FLEETPLACE_COST_T", "FLEETPLACE_THREADS", "FLEETPLACE_MIRRORS_SMEM", "FLEETPLACE_BITS_SMEM")
 base = None
 VARS = [{}, {"FLEETPLACE_COST_T": "0"}, {"FLEETPLACE_THREADS": "512"},
@@ -30,7 +31,7 @@ for var in VARS:
     for k in KNOBS:
         os.environ.pop(k, None)
     os.environ.update(var)
-    res = F.search_batch(insts, starts, cfg, tabs)
+    res = F.search_batch(insts, starts, cfg, tabs, ctx=CTX)
     key = [(r.stats.evaluations, r.stats.applied_moves, r.stats.final_objective_km) for r in res]
     base = base or key
     print(f"{str(var or 'default'):40s} device_ms {res[0].stats.device_ms:8.1f} same={key == base}",

@@ -143,6 +143,17 @@ def test_batch_equals_individual_searches():
         assert gs == ref.stats, k
         assert np.array_equal(got.mission_vehicle, ref.mission_vehicle)
         assert np.array_equal(got.vehicle_base, ref.vehicle_base)
+    # a long-lived context reused across batches (its workspace kept, then
+    # grown by a larger batch) returns the same results every time
+    ctx = F._Ctx(0)
+    for idx in ([0, 1, 2], list(range(6)), [5, 4]):
+        again = F.search_batch([insts[k] for k in idx], [starts[k] for k in idx], cfg,
+                               [tables[k] for k in idx], ctx=ctx)
+        for q, k in enumerate(idx):
+            assert all(getattr(again[q].stats, f) == getattr(batch[k].stats, f)
+                       for f in H.A.STATS_FIELDS), (idx, k)
+            assert np.array_equal(again[q].mission_vehicle, batch[k].mission_vehicle)
+            assert np.array_equal(again[q].vehicle_base, batch[k].vehicle_base)
 
 
 def test_golden_c1_on_device():

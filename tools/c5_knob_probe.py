@@ -27,6 +27,9 @@ VARS = [{}, {"FLEETPLACE_COST_T": "0"}, {"FLEETPLACE_THREADS": "512"},
         {"FLEETPLACE_MIRRORS_SMEM": "0"}, {"FLEETPLACE_BITS_SMEM": "0"}, {}]
 if os.environ.get("C5_REPEAT"):
     VARS = [{}] * int(os.environ["C5_REPEAT"])
+if os.environ.get("C5_VARS"):  # e.g. "THREADS=128,THREADS=256" (FLEETPLACE_ prefix implied)
+    VARS = [dict([("FLEETPLACE_" + kv.split("=")[0], kv.split("=")[1])]) if kv else {}
+            for kv in os.environ["C5_VARS"].split(",")]
 for var in VARS:
     for k in KNOBS:
         os.environ.pop(k, None)

@@ -213,7 +213,7 @@ def run_ours(args) -> None:
                               "exact_fallbacks", "table_row_rebuilds", "reloc_bits", "subst_bits",
                               "reloc_apply", "exact_totals", "table_patches", "pass_setup",
                               "exact_reloc_deltas", "exact_candidate_totals", "helper_waits",
-                              "reserved"),
+                              "pass_kernel_total"),
                              [c / (clocks["sm_mhz"] or 1965.0) / 1e3 for c in st.phase_cycles])),
         "event_counts": dict(zip(("scanned_rows", "scan_steps", "row_contexts",
                                   "reloc_prepasses", "eventless_rows_o1"), st.event_counts)),

@@ -2114,6 +2114,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   if (!active[scn]) return;
   const Scenario g = scs[scn];
   if (g.ctr->done) return;  // finished earlier in this chunk of launches
+  const long long t_entry = clock64();  // phase 15: the whole launch (block 0's SM clock)
   Scenario s = g;
   const bool tabu = tabu_i != 0, debug = debug_i != 0;
   __shared__ Shared sh;
@@ -2400,7 +2401,10 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     }
     for (int b = threadIdx.x; b < B; b += NT) g.rcnt[b] = s.rcnt[b];
   }
-  if (threadIdx.x == 0) *g.ctr = sh.c;
+  if (threadIdx.x == 0) {
+    sh.c.cycles[15] += (unsigned long long)(clock64() - t_entry);
+    *g.ctr = sh.c;
+  }
   if (helpers > 0) {
     __syncthreads();
     if (threadIdx.x == 0) post_job(s, sh, sm, HJOB_QUIT, -1, -1, -1);

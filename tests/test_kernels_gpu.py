@@ -381,3 +381,30 @@ def test_table_distinct_point_path_edge_points(monkeypatch):
         assert _table_bytes(sub) == direct
         monkeypatch.delenv("FLEETPLACE_TABLE_SITES")
         assert _table_bytes(sub) == direct
+
+
+@pytest.mark.parametrize("threads", [None, "512"])
+def test_batch_more_bases_than_threads(threads, monkeypatch):
+    """Batch CTAs run 256 threads: with B = 300 > 256 every per-base step
+    loops (no one-base-per-thread fast path). Each scenario must equal its
+    single search (512 threads, B <= NT), which the parity tests pin to the
+    reference."""
+    insts, starts, tabs, singles = [], [], [], []
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu)
+    for k in range(3):
+        inst = F.survey_instance(300, 1500, 15, seed=11 + k)
+        t = F.build_distance_table(inst)
+        st = F.rank_bases(inst, t)
+        arr = F._state_arrays(st.assignment, F.initial_pool(st, inst), inst)
+        singles.append(F.search_arrays(inst, t, cfg, *arr))
+        insts.append(inst)
+        starts.append(arr)
+        tabs.append(np.ascontiguousarray(t.cost.T).reshape(-1))
+    if threads:
+        monkeypatch.setenv("FLEETPLACE_THREADS", threads)
+    batch = F.search_batch(insts, starts, cfg, tabs)
+    for k in range(3):
+        assert all(getattr(batch[k].stats, f) == getattr(singles[k].stats, f)
+                   for f in H.A.STATS_FIELDS), k
+        assert np.array_equal(batch[k].mission_vehicle, singles[k].mission_vehicle)
+        assert np.array_equal(batch[k].vehicle_base, singles[k].vehicle_base)

@@ -93,21 +93,31 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  // with a stream: stream-ordered (cudaMallocAsync / cudaFreeAsync), so the
+  // free does not wait for the whole device (e.g. the row-major table copy
+  // running on the context's second stream)
+  cudaStream_t s = nullptr;
   DBuf() = default;
-  explicit DBuf(size_t count) { alloc(count); }
+  explicit DBuf(size_t count, cudaStream_t st = nullptr) : s(st) { alloc(count); }
   void alloc(size_t count) {
     free_();
     n = count;
-    if (count) check(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+    if (count) {
+      if (s) check(cudaMallocAsync(&p, sizeof(T) * count, s), "cudaMallocAsync");
+      else check(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+    }
   }
   void free_() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (s) cudaFreeAsync(p, s);
+      else cudaFree(p);
+    }
     p = nullptr;
   }
   ~DBuf() { free_(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) {
     o.p = nullptr;
     o.n = 0;
   }
@@ -1000,7 +1010,7 @@ fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* in, double rad
     const int M = in->n_missions, B = in->n_bases;
     cudaStream_t st = ctx->stream;
     table_alloc(ctx, M, B);
-    DBuf<double> pts(6ull * M + 3ull * B);
+    DBuf<double> pts(6ull * M + 3ull * B, st);
     double* plat = pts.p;
     double* plon = plat + M;
     double* dlat = plon + M;
@@ -1082,7 +1092,7 @@ fp_status fp_column_totals(fp_ctx* ctx, double* out_totals) {
   return guarded([&] {
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (ctx->M < 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "no resident table");
-    DBuf<double> d(ctx->B);
+    DBuf<double> d(ctx->B, ctx->stream);
     EvTimer tk(ctx->stream);
     check(fpk::launch_column_totals(ctx->d_cost, ctx->M, ctx->B, d.p, ctx->stream), "totals");
     ctx->last_kernel_ms = tk.stop_ms();
@@ -1106,7 +1116,7 @@ fp_status fp_rank_bases(fp_ctx* ctx, const fp_instance* in, fp_ranked_start* out
     ensure_table(ctx, M, B);
     cudaStream_t st = ctx->stream;
     // (1) fixed-order column totals on the device
-    DBuf<double> d_tot(B);
+    DBuf<double> d_tot(B, st);
     EvTimer tk(st);
     check(fpk::launch_column_totals(ctx->d_cost, M, B, d_tot.p, st), "totals");
     ctx->last_kernel_ms = tk.stop_ms();
@@ -1128,7 +1138,7 @@ fp_status fp_column_totals_chain(fp_ctx* ctx, int32_t b0, int32_t nb, const doub
     cudaStream_t st = ctx->stream;
     const double* d_carry = carry;
     double* d_out = out;
-    DBuf<double> tmp(device_ptrs ? 0 : 2 * (size_t)nb);
+    DBuf<double> tmp(device_ptrs ? 0 : 2 * (size_t)nb, ctx->stream);
     if (!device_ptrs) {
       d_out = tmp.p;
       if (carry) {
@@ -1217,8 +1227,8 @@ void rank_from_totals(fp_ctx* ctx, const fp_instance* in, const double* tot, fp_
       cv[k] = base_vehicle[chosen[k]];
       cf[k] = in->vehicle_kind[cv[k]] == FP_FIXED;
     }
-    DBuf<int32_t> d_i32(3ull * n + (size_t)M + 1);
-    DBuf<uint8_t> d_u8((size_t)n + M + 1);
+    DBuf<int32_t> d_i32(3ull * n + (size_t)M + 1, st);
+    DBuf<uint8_t> d_u8((size_t)n + M + 1, st);
     int32_t* d_cb = d_i32.p;
     int32_t* d_cbid = d_cb + n;
     int32_t* d_cv = d_cbid + n;

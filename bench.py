@@ -330,7 +330,9 @@ def sharded_rank_workload(ws: int, rank: int, local: int, reps: int = 2) -> dict
 
     shape = (5000, 1000000, 250)
     inst = F.survey_instance(*shape, seed=1)
-    part, table = S.rank_bases_sharded(inst, device=local)
+    # the workload is build + rank only: no search follows on these tables,
+    # so the search's row-major copy is not made (fp_ctx_set_row_copy)
+    part, table = S.rank_bases_sharded(inst, device=local, row_copy=False)
     ms = []
     for _ in range(reps):
         if ws > 1:
@@ -338,7 +340,7 @@ def sharded_rank_workload(ws: int, rank: int, local: int, reps: int = 2) -> dict
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        part, table = S.rank_bases_sharded(inst, device=local, table=table)
+        part, table = S.rank_bases_sharded(inst, device=local, table=table, row_copy=False)
         e1.record()
         e1.synchronize()
         ms.append(e0.elapsed_time(e1))

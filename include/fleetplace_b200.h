@@ -167,6 +167,13 @@ double fp_ctx_last_kernel_ms(const fp_ctx* ctx);
  * the context's second stream after fp_build_distance_table /
  * fp_table_upload; waits for it), or 0 if none was made. */
 double fp_ctx_last_copy_ms(fp_ctx* ctx);
+/* (new; no reference counterpart) enabled != 0 (the default): every
+ * fp_build_distance_table / fp_table_upload starts the row-major copy of the
+ * table on the context's second stream, ready for the next fp_search.
+ * 0: no eager copy -- a table that is only ranked (a mission shard whose
+ * search runs elsewhere) skips it; a later fp_search on the context makes
+ * the copy itself, in-stream. Results never depend on it. */
+fp_status fp_ctx_set_row_copy(fp_ctx* ctx, int32_t enabled);
 
 /* The search's permutation stream (perm_a, perm_b of every pass: std::
  * mt19937_64(seed), Fisher-Yates with uniform_below; proj/src/search.cpp:

@@ -16,7 +16,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libfleetplace_b200.so"
 # Every symbol include/fleetplace_b200.h declares (checked by the CPU tests).
 EXPORTS = (
     "fp_abi_version", "fp_last_error", "fp_ctx_create", "fp_ctx_destroy",
-    "fp_ctx_kernel_launches", "fp_ctx_last_kernel_ms", "fp_ctx_last_copy_ms", "fp_validate_instance", "fp_generate_instance",
+    "fp_ctx_kernel_launches", "fp_ctx_last_kernel_ms", "fp_ctx_last_copy_ms", "fp_ctx_set_row_copy", "fp_validate_instance", "fp_generate_instance",
     "fp_build_distance_table", "fp_table_upload", "fp_table_download",
     "fp_column_totals", "fp_rank_bases", "fp_initial_pool", "fp_search",
     "fp_search_batch", "fp_enumerate_moves", "fp_objective_km", "fp_haversine_batch",
@@ -51,6 +51,8 @@ def lib() -> C.CDLL:
     l.fp_ctx_last_kernel_ms.restype = f64
     l.fp_ctx_last_copy_ms.argtypes = [p]
     l.fp_ctx_last_copy_ms.restype = f64
+    l.fp_ctx_set_row_copy.argtypes = [p, i32]
+    l.fp_ctx_set_row_copy.restype = i32
     l.fp_permutations.argtypes = [p, u64, i32, i32, i32p]
     l.fp_permutations.restype = i32
     l.fp_validate_instance.argtypes = [inst_p]

@@ -38,6 +38,7 @@ using fpk_host::FpError;
 
 struct fp_ctx {
   int device = 0;
+  bool row_copy = true;  // eager row-major copy after build / upload (fp_ctx_set_row_copy)
   cudaStream_t stream = nullptr;
   double* d_cost = nullptr;
   size_t cost_cap = 0;  // elements
@@ -428,6 +429,7 @@ struct SearchRun {
 // stream (after the work already queued on the main stream). Skipped when
 // the memory is not there; searches then run without it or make their own.
 void start_costT(fp_ctx* ctx) {
+  if (!ctx->row_copy) return;
   if (const char* e = std::getenv("FLEETPLACE_COST_T"))
     if (std::atoi(e) == 0) return;
   const size_t need = (size_t)std::max(ctx->M, 0) * (size_t)std::max(ctx->B, 0);
@@ -713,7 +715,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   cudaEvent_t ei[5];
   for (auto& e : ei) check(cudaEventCreate(&e), "event");
   const bool transpose = cost_t && !(ctx_copy && ctx->costT_valid);
-  if (cost_t && ctx_copy && ctx->costT_valid) check(cudaStreamWaitEvent(st, ctx->costT_ready, 0), "wait");
+  // a copy made on the second stream is waited for; one an earlier search
+  // made in-stream (no eager copy, or its allocation failed) is ordered already
+  if (cost_t && ctx_copy && ctx->costT_valid && ctx->costT_ready)
+    check(cudaStreamWaitEvent(st, ctx->costT_ready, 0), "wait");
   check(fpk::launch_init(d_scs, run.scs.data(), n, M, maxB, maxV, transpose, st, ei),
         "init_kernel");
   if (ctx_copy && cost_t) ctx->costT_valid = true;
@@ -966,6 +971,13 @@ fp_status fp_permutations(fp_ctx* ctx, uint64_t seed, int32_t n, int32_t passes,
       PermStream rng(seed);
       for (int p = 0; p < np; ++p) rng.perm(n, out + (size_t)p * n);
     }
+  });
+}
+
+fp_status fp_ctx_set_row_copy(fp_ctx* ctx, int32_t enabled) {
+  return guarded([&] {
+    if (!ctx) throw FpError(FP_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    ctx->row_copy = enabled != 0;
   });
 }
 

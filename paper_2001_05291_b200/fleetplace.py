@@ -387,9 +387,13 @@ class DistanceTable:
 
 
 def build_distance_table(inst: Instance, radius_km: float = kEarthRadiusKm,
-                         device: int = 0) -> DistanceTable:
-    """Kernel (1): proj/src/model.cpp:76-90."""
+                         device: int = 0, row_copy: bool = True) -> DistanceTable:
+    """Kernel (1): proj/src/model.cpp:76-90. `row_copy=False`: no eager
+    row-major copy for the search (a table that is only ranked; a later
+    search on it makes the copy itself)."""
     ctx = _Ctx(device)
+    if not row_copy:
+        _check(lib().fp_ctx_set_row_copy(ctx.p, 0))
     _check(lib().fp_build_distance_table(ctx.p, C.byref(inst.c()), radius_km,
                                          C.cast(None, C.POINTER(C.c_double))))
     return DistanceTable(ctx, inst.n_missions, inst.n_bases, radius_km)

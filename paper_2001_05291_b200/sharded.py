@@ -120,19 +120,24 @@ def rank_from_totals(shard_inst: F.Instance, table: F.DistanceTable, totals: np.
 
 
 def rank_bases_sharded(inst: F.Instance, *, group=None, device: int = 0, batches: int = 8,
-                       radius_km: float = F.kEarthRadiusKm, table: F.DistanceTable = None):
+                       radius_km: float = F.kEarthRadiusKm, table: F.DistanceTable = None,
+                       row_copy: Optional[bool] = None):
     """build_distance_table + rank_bases (proj/src/model.cpp:76-90,
     proj/src/rank.cpp:25-124) with the missions sharded across the ranks of
     `group`, one GPU per rank. Returns (this rank's ShardStart, its table
-    slice). The shards' starts concatenate to the unsharded RankedStart."""
+    slice). The shards' starts concatenate to the unsharded RankedStart.
+    `row_copy`: make the search's row-major copy of the table slice (default:
+    only when there is one rank -- a shard is never searched on its own)."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     g = dist.get_rank(group) if dist.is_initialized() else 0
     rg = shard(inst.n_missions, g, world)
     part = inst.mission_slice(rg.start, rg.stop)
+    if row_copy is None:
+        row_copy = world == 1
     if table is None:
-        table = F.build_distance_table(part, radius_km, device=device)
+        table = F.build_distance_table(part, radius_km, device=device, row_copy=row_copy)
     else:
         F._check(lib().fp_build_distance_table(table._ctx.p, C.byref(part.c()), radius_km, None))
         table.n_missions, table.n_bases, table._host = part.n_missions, part.n_bases, None

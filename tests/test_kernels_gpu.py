@@ -408,3 +408,22 @@ def test_batch_more_bases_than_threads(threads, monkeypatch):
                    for f in H.A.STATS_FIELDS), k
         assert np.array_equal(batch[k].mission_vehicle, singles[k].mission_vehicle)
         assert np.array_equal(batch[k].vehicle_base, singles[k].vehicle_base)
+
+
+def test_search_without_eager_row_copy():
+    """fp_ctx_set_row_copy(ctx, 0): no row-major copy after the build; the
+    first search on the context makes it in-stream. Same results, and the
+    second search reuses the copy."""
+    inst = F.survey_instance(120, 3000, 12, seed=5)
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu)
+    out = []
+    for row_copy in (True, False):
+        t = F.build_distance_table(inst, row_copy=row_copy)
+        st = F.rank_bases(inst, t)
+        arr = F._state_arrays(st.assignment, F.initial_pool(st, inst), inst)
+        r1 = F.search_arrays(inst, t, cfg, *arr)
+        r2 = F.search_arrays(inst, t, cfg, *arr)
+        for r in (r1, r2):
+            out.append((tuple(getattr(r.stats, f) for f in H.A.STATS_FIELDS),
+                        r.mission_vehicle.tobytes(), r.vehicle_base.tobytes()))
+    assert all(o == out[0] for o in out)

@@ -766,6 +766,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // blocks (-1 = as many as fit; FLEETPLACE_HELPERS=0 disables)
   int helpers = n == 1 && M >= (32 << 10) ? -1 : 0;
   if (const char* e = std::getenv("FLEETPLACE_HELPERS")) helpers = std::atoi(e);
+  // the 1024-thread variant (a FLEETPLACE_THREADS experiment knob) is not
+  // validated with helper blocks: c3 with both faulted (illegal instruction)
+  if (threads >= 1024) helpers = 0;
   unsigned epoch = 0;
   int n_active = n;
   while (n_active > 0) {

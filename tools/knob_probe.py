@@ -22,8 +22,8 @@ start = F.rank_bases(inst, t)
 VARIANTS = [
     {},
     {"FLEETPLACE_INKERNEL": "1"},
-    {"FLEETPLACE_THREADS": "1024"},
     {"FLEETPLACE_THREADS": "256"},
+    {"FLEETPLACE_THREADS": "1024"},
 ]
 base = None
 for var in VARIANTS:

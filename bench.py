@@ -7,16 +7,22 @@ rotary-only fraction 0.3, instance seed 1; SearchConfig{seed 7, Tabu,
 tenure 0 (= 2M), no pass cap}. Synthetic data from the reference's own
 generator recipe (restated in the product, parity-tested).
 
-A STEP is one complete tabu_search to quiescence from the ranked start
-(proj/src/search.cpp:446-460) over the device-resident table: `value` =
-SearchStats::evaluations per second over the K timed steps (device time,
-CUDA events on the library's stream). `e2e` times the same search through
-the C ABI with HOST buffers: the 40 MB table and the start are copied in and
-the assignment copied out inside the timed region every step.
+A STEP is one tabu_search from the ranked start (proj/src/search.cpp:446-460)
+capped at its first REF_PASSES passes (SearchConfig::max_passes = 3) over the
+device-resident table: `value` = SearchStats::evaluations per second over the
+K timed steps (device time, CUDA events on the library's stream). Both arms
+run exactly this step -- the reference's full c2 run takes ~12 min on one
+core -- so `same_config` is true and the line asserts the evaluation count
+and the final Assignment equal the reference's recorded run
+(tests/golden/runs.json). `e2e` times the same search through the C ABI with
+HOST buffers: the 40 MB table and the start are copied in and the assignment
+copied out inside the timed region every step. Time-to-solution (the search
+to quiescence) is reported beside it in `c2_to_quiescence`, checked against
+the reference's own full run.
 
 --impl reference runs the unmodified reference (oracle/_ref, compiled from
-/root/reference/proj/src) on the host: sequential tabu_search on a bounded
-sample (first `REF_PASSES` passes of the same search) per step.
+/root/reference/proj/src) on the host: sequential tabu_search, the same
+3-pass step.
 
 Multi-GPU (torchrun): the single-instance search does not shard (SURVEY.md
 §8e: "c1/c2 replicas only"); each rank runs an independent replica, value =
@@ -44,11 +50,37 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CFG = dict(workload="c2: 500 bases x 10k missions x 40 vehicles, tabu seed 7 to quiescence",
-           bases=500, missions=10000, vehicles=40, instance_seed=1, search_seed=7, tenure=0)
-METRIC = "Tabu move-evals/sec (time-to-solution in ms_per_step)"
+REF_PASSES = 3  # the step: the first passes of the c2 search (both arms)
+CFG = dict(workload=f"c2: 500 bases x 10k missions x 40 vehicles, tabu seed 7, first {REF_PASSES} "
+                    f"passes (max_passes {REF_PASSES}); to quiescence in c2_to_quiescence",
+           bases=500, missions=10000, vehicles=40, instance_seed=1, search_seed=7, tenure=0,
+           max_passes=REF_PASSES)
+METRIC = "Tabu move-evals/sec (c2 search, first 3 passes; time-to-solution in c2_to_quiescence)"
 UNIT = "move-evals/s"
-REF_PASSES = 3  # reference sample: first passes of the same search (~0.5 s each at c2)
+GOLDEN = ROOT / "tests" / "golden" / "runs.json"  # the reference's own recorded runs
+
+
+def _golden(name: str) -> dict:
+    return json.loads(GOLDEN.read_text())[name]
+
+
+def _sha(*arrs) -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrs:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def _assert_golden(name: str, stats, vb, mv) -> None:
+    """Parity gate: the six SearchStats counters and the final Assignment
+    equal the reference's recorded run (objective within 1e-9 relative)."""
+    g = _golden(name)
+    got = [stats.passes, stats.evaluations, stats.applied_moves, stats.committed_moves,
+           stats.tabu_skips_outer, stats.tabu_skips_inner]
+    if got != g["stats"] or _sha(vb, mv) != g["assignment_sha256"] or \
+            abs(stats.final_objective_km - g["final_objective_km"]) > 1e-9 * g["final_objective_km"]:
+        raise SystemExit(f"PARITY FAILURE on {name}: {got} vs the reference's {g['stats']}")
 
 
 def _dist():
@@ -135,7 +167,10 @@ def run_ours(args) -> None:
     start = F.rank_bases(inst, t)
     pool = F.initial_pool(start, inst)
     vb, mv, pk, px = F._state_arrays(start.assignment, pool, inst)
-    cfg = F.SearchConfig(seed=CFG["search_seed"], mode=F.SearchMode.Tabu, tabu_tenure=CFG["tenure"])
+    cfg = F.SearchConfig(seed=CFG["search_seed"], mode=F.SearchMode.Tabu, tabu_tenure=CFG["tenure"],
+                         max_passes=REF_PASSES)
+    cfg_full = F.SearchConfig(seed=CFG["search_seed"], mode=F.SearchMode.Tabu,
+                              tabu_tenure=CFG["tenure"])
     host_cost = np.ascontiguousarray(t.cost.T).reshape(-1)  # pinned below for the e2e leg
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > L2
 
@@ -159,6 +194,7 @@ def run_ours(args) -> None:
     dev_ms = [r.stats.device_ms for r in results]
     evals = results[0].stats.evaluations
     assert all(r.stats.evaluations == evals for r in results), "search must be deterministic"
+    _assert_golden("c2_3pass", results[0].stats, results[0].vehicle_base, results[0].mission_vehicle)
     # e2e: host buffers through the C ABI, copies inside the timed region
     # a long-lived solver context (as a serving process keeps one): every step
     # uploads the table from pinned host memory into it and searches
@@ -186,25 +222,45 @@ def run_ours(args) -> None:
         dist.all_reduce(v, op=dist.ReduceOp.MAX)
         tot_ms, e2e_mean = float(v[0]), float(v[1])
     value = ws * evals * args.steps / (tot_ms / 1e3)
-    # roofline of the dominant kernel (pass_kernel): algorithmic bytes per
-    # evaluated pair = perm_b index 4 + mirrored vehicle 4 + cost 8 +
-    # rotary flag 1 + one gathered table entry 8 = 25 B; per visited row 16 B.
+    # roofline of the dominant kernel (pass_kernel, one launch = one pass =
+    # one neighbourhood sweep): SURVEY.md §8(d)'s algorithmic bytes per sweep,
+    # 8*B*M + 16*M, over the kernel's mean launch time (CUDA events around
+    # every pass-kernel launch on the library's stream, this run)
     st = results[0].stats
-    unblocked = st.evaluations // 3
-    rows = st.passes * inst.n_missions
-    alg_bytes = 25 * unblocked + 16 * rows
+    B_, M_ = inst.n_bases, inst.n_missions
+    alg_bytes = 8 * B_ * M_ + 16 * M_
+    pass_ms = float(np.mean([r.stats.pass_ms / max(r.stats.passes, 1) for r in results]))
+    pass_share = float(np.mean([r.stats.pass_ms / r.stats.device_ms for r in results]))
     peak, peak_kind = _peaks()
-    achieved = alg_bytes / (np.mean(dev_ms) / 1e3) / 1e9
+    achieved = alg_bytes / (pass_ms / 1e3) / 1e9
+    # time-to-solution: the same search to quiescence (reference: ~12 min)
+    full = []
+    for _ in range(3):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        full.append(F.search_arrays(inst, t, cfg_full, vb, mv, pk, px))
+    _assert_golden("c2_full", full[0].stats, full[0].vehicle_base, full[0].mission_vehicle)
+    ref_full = _ref_full_run()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": float(np.mean(dev_ms)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {**CFG, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "l2": "flushed (256 MB write) before every step"},
-        "time_to_solution_ms": float(np.mean(dev_ms)),
+        "same_config": True,
+        "parity": "SearchStats and final Assignment equal the reference's recorded runs "
+                  "(tests/golden/runs.json: c2_3pass, c2_full)",
         "search_stats": {k: getattr(st, k) for k in ("passes", "evaluations", "applied_moves",
                                                        "tabu_skips_outer", "tabu_skips_inner",
                                                        "final_objective_km", "exact_fallbacks")},
+        "c2_to_quiescence": {
+            "workload": "the same c2 tabu_search to quiescence (time-to-solution)",
+            "device_ms": float(statistics.median(r.stats.device_ms for r in full)),
+            "passes": full[0].stats.passes, "evaluations": full[0].stats.evaluations,
+            "applied_moves": full[0].stats.applied_moves,
+            "move_evals_per_s": full[0].stats.evaluations /
+                                (statistics.median(r.stats.device_ms for r in full) / 1e3),
+            "reference": ref_full},
         # SURVEY.md §8(d) coverage / distance: missions served by a compatible
         # placed vehicle (must be M) and the distance of the final assignment
         "coverage": _coverage(inst, results[0]), "missions": inst.n_missions,
@@ -221,8 +277,11 @@ def run_ours(args) -> None:
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_mean * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(), "kernel": "pass_kernel<512>",
-                     "peak_source": peak_kind,
-                     "note": "serial first-improvement automaton: latency-bound, see DESIGN.md"},
+                     "peak_source": peak_kind, "bytes_per_launch": alg_bytes,
+                     "ms_per_launch": pass_ms, "share_of_step": pass_share,
+                     "note": "one launch = one pass = one neighbourhood sweep (8BM+16M bytes, "
+                             "SURVEY §8(d)); a serial first-improvement automaton, bound by its "
+                             "event chain, not by HBM: see DESIGN.md §3/§6"},
         # our kernels launched inside the timed region (library counter)
         "gpu_launches": int(launches),
         "clocks": clocks,
@@ -368,43 +427,62 @@ def c5_batch_workload(ws: int, rank: int, local: int, per_rank: int = 512) -> di
     """c5: independent 200 x 5k x 20 scenarios (seeds 1 + k), tabu to
     quiescence, scenario-sharded over the ranks with no collective on the
     data path (dist.run_sharded): 512 scenarios per GPU, so
-    N = 8 runs the whole 4096-scenario batch. Each rank prepares its own
-    scenarios' tables and starts (untimed), then one fp_search_batch launch
-    on its GPU; time = max over ranks of the library's CUDA-event time."""
+    N = 8 runs the whole 4096-scenario batch. Each rank ranks its scenarios
+    (untimed), then one fp_search_batch_configs call per launch on its GPU
+    with the tables left NULL: the call uploads the instances' coordinates,
+    builds every table on the device (kernel (1), one launch), searches and
+    copies the assignments back. `search_ms` = the library's CUDA-event time
+    of the search; `e2e_ms` = wall time of the whole call (host arrays in,
+    results out). Max over ranks. Scenarios 1..16 must equal the reference's
+    recorded runs (tests/golden/runs.json)."""
     from paper_2001_05291_b200 import fleetplace as F
     from paper_2001_05291_b200.dist import run_sharded
 
     n = per_rank * ws
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu)
 
     def solve(rg):
-        insts, starts, tabs = [], [], []
+        insts, starts = [], []
         for k in rg:
             ik = F.survey_instance(200, 5000, 20, seed=1 + k)
             tk = F.build_distance_table(ik, device=local)
             sk = F.rank_bases(ik, tk)
             insts.append(ik)
             starts.append(F._state_arrays(sk.assignment, F.initial_pool(sk, ik), ik))
-            tabs.append(np.ascontiguousarray(tk.cost.T).reshape(-1))
             del tk
         # one long-lived context (as a serving process keeps one: its
-        # workspace is reused), one warm-up launch, then three identical
-        # launches, median reported (DESIGN.md §6: fresh contexts run
-        # 268-316 ms, a warm one 232-235 ms; the results never change)
+        # workspace is reused), one warm-up call, then three identical
+        # calls, medians reported
         ctx = F._Ctx(local)
-        times, out = [], None
+        times, walls, out = [], [], None
         for it in range(4):
-            res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu),
-                                 tabs, device=local, ctx=ctx)
+            t0 = time.perf_counter()
+            res = F.search_batch(insts, starts, cfg, None, device=local, ctx=ctx)
+            wall = time.perf_counter() - t0
             o = [(x.stats.evaluations, x.stats.passes, x.stats.applied_moves,
                   x.stats.final_objective_km) for x in res]
             assert out is None or o == out, "c5 batch results changed between launches"
             out = o
-            if it > 0:
+            if it == 0:
+                for k, x in zip(rg, res):
+                    if k < 16:
+                        _assert_golden(f"c5_s{k + 1}", x.stats, x.vehicle_base, x.mission_vehicle)
+            else:
                 times.append(res[0].stats.device_ms / 1e3)
+                walls.append(wall)
         solve.spread_ms = (min(times) * 1e3, max(times) * 1e3)
+        solve.e2e_s = sorted(walls)[1]
+        solve.launches = res[0].kernel_launches
         return out, sorted(times)[1]
 
     allres, tmax = run_sharded(n, solve)
+    e2e = getattr(solve, "e2e_s", 0.0)
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        v = torch.tensor([e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        e2e = float(v[0])
     if rank != 0:
         return {}
     ev = sum(r[0] for r in allres)
@@ -415,8 +493,14 @@ def c5_batch_workload(ws: int, rank: int, local: int, per_rank: int = 512) -> di
             "applied_moves": sum(r[2] for r in allres),
             "objective_sum_km": float(sum(r[3] for r in allres)),
             "rank0_min_max_ms": list(getattr(solve, "spread_ms", ())),
-            "timing": "library CUDA events around the batch launch on a long-lived context, "
-                      "1 warm-up + median of 3 identical launches, max over ranks"}
+            "e2e": {"ms": e2e * 1e3, "move_evals_per_s": ev / e2e,
+                    "what": "one fp_search_batch_configs call: instance coordinates and starts "
+                            "H2D, every table built on the device (one kernel (1) launch), the "
+                            "search, assignments D2H"},
+            "parity": "scenarios 1..16 equal the reference's recorded runs",
+            "timing": "library CUDA events around the batch search (search_ms) and wall time "
+                      "of the call (e2e) on a long-lived context, 1 warm-up + median of 3 "
+                      "identical calls, max over ranks"}
 
 
 def _c4_sweep_roofline(extra: dict, peak: float) -> dict:
@@ -533,13 +617,50 @@ def _ref_lib():
     return H
 
 
+def _cpu_model() -> str:
+    import platform
+    cpu = platform.processor() or platform.machine()
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return cpu
+
+
+def _nproc() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def _ref_full_run() -> dict:
+    """The reference's c2 run to quiescence (sequential, one core): measured
+    once per round on the GPU box's host by tools/ref_full_run.py
+    (profiles/r2_ref_c2_full.json); the survey's container figure beside it."""
+    f = ROOT / "profiles" / "r2_ref_c2_full.json"
+    out = {"survey_container_s": 686.4}
+    if f.exists():
+        out.update(json.loads(f.read_text()))
+    return out
+
+
 def cpu_baseline(inst, host_cost, start, pk, px, passes: int = REF_PASSES) -> dict:
     H = _ref_lib()
     s = H.ref_search(inst, host_cost, 1, CFG["search_seed"], start.vehicle_base,
                      start.mission_vehicle, pk, px, max_passes=passes)
+    # the reference's CPU-parallel arm (non-parity, proj/include/fleetplace/
+    # parallel.hpp:31-39) on every host core, the same step
+    n = _nproc()
+    p = H.ref_search(inst, host_cost, 1, CFG["search_seed"], start.vehicle_base,
+                     start.mission_vehicle, pk, px, max_passes=passes, workers=n)
     return {"value": s.stats[1] / s.seconds, "unit": UNIT, "cores": 1, "kind": "reference",
-            "sample": f"first {passes} passes of the same c2 tabu_search (sequential reference, "
-                      f"{s.stats[1]} evaluations in {s.seconds:.2f} s)"}
+            "cpu": _cpu_model(), "nproc": n,
+            "sample": f"the same step: first {passes} passes of the c2 tabu_search (sequential "
+                      f"reference, {s.stats[1]} evaluations in {s.seconds:.3f} s)",
+            "parallel_tabu_search": {"workers": n, "value": p.stats[1] / p.seconds,
+                                     "evaluations": p.stats[1], "seconds": p.seconds,
+                                     "note": "non-deterministic by design (parallel.cpp:137-305); "
+                                             "not a parity arm"}}
 
 
 def cpu_baseline_c5(passes: int = 3) -> dict:
@@ -548,10 +669,9 @@ def cpu_baseline_c5(passes: int = 3) -> dict:
     c5 scenario (seed 1 + k) per core concurrently (ctypes releases the GIL),
     each bounded to its first `passes` passes; aggregate evaluations / wall."""
     import concurrent.futures as cf
-    import platform
 
     H = _ref_lib()
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cores = _nproc()
 
     def prep(k):
         inst = H.ref_survey_instance(200, 5000, 20, seed=1 + k)
@@ -572,16 +692,8 @@ def cpu_baseline_c5(passes: int = 3) -> dict:
         res = list(ex.map(run, scn))
         wall = time.perf_counter() - t0
     ev = sum(x.stats[1] for x in res)
-    cpu = platform.processor() or platform.machine()
-    try:
-        for line in Path("/proc/cpuinfo").read_text().splitlines():
-            if line.startswith("model name"):
-                cpu = line.split(":", 1)[1].strip()
-                break
-    except OSError:
-        pass
     return {"value": ev / wall, "unit": UNIT, "cores": cores, "kind": "reference",
-            "cpu": cpu,
+            "cpu": _cpu_model(),
             "sample": f"{cores} c5 scenarios (200 x 5k x 20, seeds 1..{cores}), one per core "
                       f"concurrently, first {passes} passes each: {ev} evaluations in {wall:.2f} s"}
 
@@ -605,18 +717,22 @@ def run_reference(args) -> None:
     res = [step() for _ in range(args.steps)]
     secs = sum(x.seconds for x in res)
     evals = sum(x.stats[1] for x in res)
+    g = _golden("c2_3pass")
+    assert list(res[0].stats[:6]) == g["stats"], "reference arm: unexpected search"
     v = evals / secs
     line = {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {**CFG, "parallelism": "host, sequential reference"},
-        "impl": "reference",
+        "impl": "reference", "same_config": True,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "reference",
-                         "sample": f"first {REF_PASSES} passes of the c2 tabu_search per step "
-                                   f"(the full run takes ~690 s on one core); "
-                                   f"parallel_tabu_search on 8 threads measured slower "
-                                   f"(lock-bound), so the sequential build is the fastest CPU arm"},
+                         "cpu": _cpu_model(), "nproc": _nproc(),
+                         "sample": f"each step: the first {REF_PASSES} passes of the c2 "
+                                   f"tabu_search ({res[0].stats[1]} evaluations, the GPU arm's "
+                                   f"step exactly); sequential, the reference's parity path "
+                                   f"(parallel_tabu_search is non-deterministic; it is reported "
+                                   f"in the GPU line's cpu_baseline)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -631,6 +747,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the c3 / c5 extra workloads")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU over NCCL: launch ourselves under torchrun
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define FP_ABI_VERSION 3
+#define FP_ABI_VERSION 4
 
 typedef enum fp_status {
   FP_OK = 0,
@@ -139,6 +139,8 @@ typedef struct fp_search_result {
   double init_part_ms[4];        /* init_ms split: row-major table copy, costs +
                                     exact total, improvement rows, relocation
                                     table rows (CUDA events) */
+  double pass_ms;                /* pass-kernel launches (CUDA events, summed) */
+  uint64_t pass_launches;        /* pass-kernel launches of this call */
 } fp_search_result;
 
 /* RankedStart (proj/include/fleetplace/rank.hpp:10-14) in index form. */
@@ -209,7 +211,11 @@ fp_status fp_generate_instance(uint64_t pool_seed, const double* bbox,
  * below. `out_cost` (host, n_missions*n_bases) may be NULL. */
 fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* inst,
                                   double radius_km, double* out_cost);
-/* Makes a caller-supplied table (e.g. the reference's) resident instead. */
+/* Makes a caller-supplied table (e.g. the reference's) resident instead.
+ * Any matrix is accepted (column totals are exact for every entry value,
+ * like the reference's loop); fp_search additionally requires every entry to
+ * be finite and >= 0, as distances are, and returns FP_ERR_INVALID_ARGUMENT
+ * otherwise (one device pass checks the upload). */
 fp_status fp_table_upload(fp_ctx* ctx, int32_t n_missions, int32_t n_bases,
                           const double* cost_colmajor);
 fp_status fp_table_download(fp_ctx* ctx, double* out_cost);
@@ -268,10 +274,24 @@ fp_status fp_search(fp_ctx* ctx, const fp_instance* inst,
                     const fp_search_config* cfg, const fp_search_start* start,
                     fp_search_result* out);
 
-/* Scenario batch: `n` independent instances of identical shape (same
- * n_missions; tables uploaded/built per scenario into the batch arena),
- * searched concurrently, one thread block per scenario. tables[s] may be
- * NULL to build scenario s's table on the device. */
+/* Scenario batch: `n` independent searches of one mission count (tables
+ * uploaded or built per scenario into the batch arena), run concurrently,
+ * one thread block per scenario, each with its OWN SearchConfig cfgs[s]
+ * (seed, mode, tenure, max_passes, debug): e.g. run_experiment's attempts,
+ * attempt t searching the same instance with seed + t
+ * (proj/src/bench.cpp:125-128), or independent scenarios. Scenario s's
+ * result equals fp_search's on its own. Scenarios with equal seeds share one
+ * permutation stream (it depends on the seed and n_missions only).
+ * tables[s] (or tables itself) may be NULL: scenario s's table is then built
+ * on the device by kernel (1) with radius_km (all such tables in one
+ * launch); the context's resident table is never touched. (new; the
+ * reference runs attempts one after another) */
+fp_status fp_search_batch_configs(fp_ctx* ctx, int32_t n, const fp_instance* insts,
+                                  const double* const* tables, double radius_km,
+                                  const fp_search_config* cfgs,
+                                  const fp_search_start* starts,
+                                  fp_search_result* outs);
+/* The same with one config for every scenario and radius 6371.0088. */
 fp_status fp_search_batch(fp_ctx* ctx, int32_t n, const fp_instance* insts,
                           const double* const* tables,
                           const fp_search_config* cfg,
@@ -288,8 +308,10 @@ fp_status fp_enumerate_moves(fp_ctx* ctx, const fp_instance* inst,
 
 /* objective_km's fixed mission-order sum (proj/src/model.cpp:176-192) of
  * cost(m, vehicle_base[mission_vehicle[m]]) on the resident table.
- * Feasibility is checked by the caller (check_feasible is host logic). */
-fp_status fp_objective_km(fp_ctx* ctx, const int32_t* vehicle_base,
+ * Full feasibility (check_feasible) is the caller's; here every
+ * mission_vehicle[m] must be in [0, n_vehicles) and every referenced
+ * vehicle_base in [0, n_bases), else FP_ERR_INFEASIBLE. */
+fp_status fp_objective_km(fp_ctx* ctx, int32_t n_vehicles, const int32_t* vehicle_base,
                           const int32_t* mission_vehicle, double* out_km);
 
 #ifdef __cplusplus

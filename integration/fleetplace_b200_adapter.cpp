@@ -7,16 +7,28 @@
 //   column_totals         proj/include/fleetplace/rank.hpp:21
 //   rank_bases            proj/include/fleetplace/rank.hpp:30
 //   local_search / tabu_search   proj/include/fleetplace/search.hpp:128-138
+//   check_feasible / objective_km proj/include/fleetplace/model.hpp:108-119
 // A maintainer links this file into the `fleetplace` library and compiles the
-// reference's own definitions of those five functions out (oracle/Makefile
+// reference's own definitions of those seven functions out (oracle/Makefile
 // target `acceptance_b200` does it with -D renames), so every caller —
 // run_experiment, brute_force_optimal, parallel_local_search(workers=1), the
 // CLI, the tests — runs the B200 path. Errors come back as the reference's
 // exception types.
+//
+// GPU-side configuration (never through SearchConfig): the device is
+// FLEETPLACE_DEVICE (default 0) or fleetplace::b200::set_device(). The
+// distance table stays resident on the device across calls: a call whose
+// matrix has the resident table's data pointer, shape and content hash
+// (a 64-bit hash over every entry, multi-threaded) skips the upload.
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -46,15 +58,79 @@ void check(fp_status s) {
   if (s != FP_OK) raise(s);
 }
 
+int g_device = -1;  // -1: FLEETPLACE_DEVICE or 0
+
+int device_ordinal() {
+  if (g_device >= 0) return g_device;
+  const char* e = std::getenv("FLEETPLACE_DEVICE");
+  return e ? std::max(0, std::atoi(e)) : 0;
+}
+
+// The matrix resident in a context: where it came from and its content.
+struct Resident {
+  const double* ptr = nullptr;
+  long long rows = -1, cols = -1;
+  unsigned long long hash = 0;
+};
+
 // One context per host thread (fp_ctx is not thread-safe).
 struct Ctx {
   fp_ctx* p = nullptr;
-  Ctx() { check(fp_ctx_create(0, &p)); }
-  ~Ctx() { fp_ctx_destroy(p); }
+  int device = -1;
+  Resident res;
+  ~Ctx() {
+    if (p) fp_ctx_destroy(p);
+  }
 };
-fp_ctx* ctx() {
+Ctx& ctx_state() {
   thread_local Ctx c;
-  return c.p;
+  const int d = device_ordinal();
+  if (!c.p || c.device != d) {
+    if (c.p) fp_ctx_destroy(c.p);
+    c.p = nullptr;
+    c.res = Resident{};
+    check(fp_ctx_create(d, &c.p));
+    c.device = d;
+  }
+  return c;
+}
+fp_ctx* ctx() { return ctx_state().p; }
+
+// 64-bit content hash of a table: four independent multiply-xor lanes per
+// thread (memory-bound), chunk hashes combined in order.
+unsigned long long table_hash(const double* p, std::size_t n) {
+  auto chunk = [](const double* q, std::size_t k) {
+    unsigned long long a[4] = {0x9E3779B97F4A7C15ull, 0xC2B2AE3D27D4EB4Full, 0x165667B19E3779F9ull,
+                               0x27D4EB2F165667C5ull};
+    std::size_t i = 0;
+    for (; i + 4 <= k; i += 4)
+      for (int l = 0; l < 4; ++l) {
+        unsigned long long w;
+        std::memcpy(&w, q + i + l, 8);
+        a[l] = (a[l] ^ w) * 0x100000001B3ull + (a[l] >> 29);
+      }
+    for (; i < k; ++i) {
+      unsigned long long w;
+      std::memcpy(&w, q + i, 8);
+      a[0] = (a[0] ^ w) * 0x100000001B3ull + (a[0] >> 29);
+    }
+    return (a[0] * 31 + a[1]) * 31 * 31 + a[2] * 31 + a[3] + k;
+  };
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned T = n < (1u << 22) ? 1u : hw;
+  const std::size_t per = (n + T - 1) / T;
+  std::vector<unsigned long long> hs(T, 0);
+  std::vector<std::thread> ws;
+  for (unsigned t = 1; t < T; ++t)
+    ws.emplace_back([&, t] {
+      const std::size_t lo = std::min(n, t * per), hi = std::min(n, lo + per);
+      hs[t] = chunk(p + lo, hi - lo);
+    });
+  hs[0] = chunk(p, std::min(n, per));
+  for (auto& w : ws) w.join();
+  unsigned long long h = 0xCBF29CE484222325ull;
+  for (unsigned long long x : hs) h = (h ^ x) * 0x100000001B3ull;
+  return h;
 }
 
 // Structure-of-arrays view of an Instance for the duration of a call.
@@ -96,8 +172,17 @@ struct InstView {
   int m(int id) const { auto it = midx.find(id); return it == midx.end() ? -1 : it->second; }
 };
 
+// Makes `cost` the context's resident table unless it already is.
 void upload(const Eigen::MatrixXd& cost) {
-  check(fp_table_upload(ctx(), (int32_t)cost.rows(), (int32_t)cost.cols(), cost.data()));
+  Ctx& c = ctx_state();
+  const std::size_t n = (std::size_t)cost.rows() * (std::size_t)cost.cols();
+  const unsigned long long h = table_hash(cost.data(), n);
+  if (c.res.ptr == cost.data() && c.res.rows == cost.rows() && c.res.cols == cost.cols() &&
+      c.res.hash == h)
+    return;
+  c.res = Resident{};
+  check(fp_table_upload(c.p, (int32_t)cost.rows(), (int32_t)cost.cols(), cost.data()));
+  c.res = Resident{cost.data(), (long long)cost.rows(), (long long)cost.cols(), h};
 }
 
 Assignment to_assignment(const InstView& iv, const std::vector<int32_t>& vb,
@@ -155,13 +240,94 @@ Assignment search(const RankedStart& start, const Instance& inst, const Distance
 
 }  // namespace
 
+namespace b200 {
+// Selects the CUDA device of the calling thread's later calls.
+void set_device(int device) { g_device = device < 0 ? -1 : device; }
+}  // namespace b200
+
 DistanceTable build_distance_table(const Instance& inst, double radius_km) {
   InstView iv(inst);
   DistanceTable t;
   t.earth_radius_km = radius_km;
   t.cost.resize((Eigen::Index)inst.missions.size(), (Eigen::Index)inst.bases.size());
-  check(fp_build_distance_table(ctx(), &iv.c, radius_km, t.cost.data()));
+  Ctx& c = ctx_state();
+  c.res = Resident{};
+  check(fp_build_distance_table(c.p, &iv.c, radius_km, t.cost.data()));
+  // the device copy is this matrix: later calls on it skip the upload (the
+  // returned DistanceTable keeps the same heap buffer when moved)
+  c.res = Resident{t.cost.data(), (long long)t.cost.rows(), (long long)t.cost.cols(),
+                   table_hash(t.cost.data(), (std::size_t)t.cost.rows() * t.cost.cols())};
   return t;
+}
+
+// check_feasible (proj/src/model.cpp:118-174): the same rules, report order
+// and de-duplication, with id -> index hash maps instead of
+// Instance::*_index linear scans (first index wins, like index_of).
+std::vector<Violation> check_feasible(const Assignment& a, const Instance& inst) {
+  std::unordered_map<int, int> bidx, vidx, midx;
+  bidx.reserve(inst.bases.size() * 2);
+  vidx.reserve(inst.fleet.size() * 2);
+  midx.reserve(inst.missions.size() * 2);
+  for (std::size_t i = 0; i < inst.bases.size(); ++i) bidx.emplace(inst.bases[i].id, (int)i);
+  for (std::size_t i = 0; i < inst.fleet.size(); ++i) vidx.emplace(inst.fleet[i].id, (int)i);
+  for (std::size_t i = 0; i < inst.missions.size(); ++i) midx.emplace(inst.missions[i].id, (int)i);
+  auto find = [](const std::unordered_map<int, int>& m, int id) {
+    auto it = m.find(id);
+    return it == m.end() ? -1 : it->second;
+  };
+  std::vector<Violation> out;
+  std::set<std::pair<Rule, int>> reported;
+  auto report = [&](Rule r, int subject, int related = -1) {
+    if (reported.insert({r, subject}).second) out.push_back(Violation{r, subject, related});
+  };
+  std::map<int, int> base_load;
+  for (const auto& [vid, bid] : a.placement) {
+    const int vi = find(vidx, vid), bi = find(bidx, bid);
+    if (vi < 0 || bi < 0) {
+      report(Rule::OneBasePerVehicle, vid, bid);
+      continue;
+    }
+    base_load[bid] += 1;
+    if (!compatible_vehicle_base(inst.fleet[(std::size_t)vi], inst.bases[(std::size_t)bi]))
+      report(Rule::FixedWingOnHelipad, vid, bid);
+  }
+  for (const auto& [bid, load] : base_load)
+    if (load > 1) report(Rule::BaseOccupancy, bid);
+  for (const Vehicle& v : inst.fleet)
+    if (!a.placement.contains(v.id)) report(Rule::OneBasePerVehicle, v.id);
+  for (const auto& [mid, vid] : a.service) {
+    const int mi = find(midx, mid), vi = find(vidx, vid);
+    if (mi < 0) {
+      report(Rule::OneVehiclePerMission, mid, vid);
+      continue;
+    }
+    if (vi < 0) {
+      report(Rule::ServiceRequiresPlacement, vid, mid);
+      continue;
+    }
+    if (!a.placement.contains(vid)) report(Rule::ServiceRequiresPlacement, vid, mid);
+    if (!compatible_vehicle_mission(inst.fleet[(std::size_t)vi], inst.missions[(std::size_t)mi]))
+      report(Rule::RotaryOnly, mid, vid);
+  }
+  for (const Mission& m : inst.missions)
+    if (!a.service.contains(m.id)) report(Rule::OneVehiclePerMission, m.id);
+  return out;
+}
+
+// objective_km (proj/src/model.cpp:176-192): feasibility as above, then the
+// fixed mission-order sum on the device (fp_objective_km, bit-identical).
+double objective_km(const Assignment& a, const Instance& inst, const DistanceTable& t) {
+  const auto violations = check_feasible(a, inst);
+  if (!violations.empty())
+    throw InfeasibleError("infeasible assignment: " + to_string(violations.front()));
+  InstView iv(inst);
+  std::vector<int32_t> vb(iv.vid.size(), -1), mv(iv.mid.size(), -1);
+  for (const auto& [vid, bid] : a.placement) vb[(std::size_t)iv.v(vid)] = iv.b(bid);
+  for (std::size_t m = 0; m < iv.mid.size(); ++m) mv[m] = iv.v(a.service.at(iv.mid[m]));
+  upload(t.cost);
+  double km = 0.0;
+  check(fp_objective_km(ctx(), (int32_t)vb.size(), vb.data(), mv.data(), &km));
+  return km;
 }
 
 Eigen::VectorXd column_totals(const Eigen::MatrixXd& cost) {

@@ -65,7 +65,8 @@ class fp_search_result(C.Structure):
                 ("kernel_launches", C.c_uint64), ("exact_fallbacks", C.c_uint64),
                 ("phase_cycles", C.c_uint64 * 16), ("init_ms", C.c_double),
                 ("sweep_ms", C.c_double), ("event_counts", C.c_uint64 * 5),
-                ("init_part_ms", C.c_double * 4)]
+                ("init_part_ms", C.c_double * 4), ("pass_ms", C.c_double),
+                ("pass_launches", C.c_uint64)]
 
 
 class fp_ranked_start(C.Structure):

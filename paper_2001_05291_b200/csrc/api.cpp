@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -43,6 +44,10 @@ struct fp_ctx {
   double* d_cost = nullptr;
   size_t cost_cap = 0;  // elements
   int M = -1, B = -1;
+  // every entry of the resident table is finite and >= 0 (kernel (1) tables
+  // are by construction; uploads are checked): the search's exact-sum
+  // machinery relies on it
+  bool table_ok = false;
   uint64_t launches = 0;
   double last_kernel_ms = 0.0;
   // pinned staging for permutations (double-buffered)
@@ -122,6 +127,17 @@ struct DBuf {
     o.p = nullptr;
     o.n = 0;
   }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      free_();
+      p = o.p;
+      n = o.n;
+      s = o.s;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
 };
 
 template <typename T>
@@ -154,6 +170,7 @@ void table_alloc(fp_ctx* ctx, int M, int B) {
   ctx->M = M;
   ctx->B = B;
   ctx->costT_valid = false;
+  ctx->table_ok = false;
 }
 
 bool valid_point(double lat, double lon) {
@@ -245,6 +262,48 @@ struct EvTimer {
     if (b) cudaEventDestroy(b);
   }
 };
+
+// One device pass over a table: every entry finite and >= 0 (synchronises).
+bool table_entries_ok(const double* d_t, size_t n, cudaStream_t st) {
+  DBuf<int> bad(1, st);
+  check(fpk::launch_table_check(d_t, n, bad.p, st), "table_check");
+  int h = 0;
+  d2h(&h, bad.p, 1, st);
+  check(cudaStreamSynchronize(st), "table check sync");
+  return h == 0;
+}
+
+// kernel (1) (build_distance_table, proj/src/model.cpp:76-90) into `dst`
+// (M x B column-major) on the context's stream; ctx's resident table is
+// untouched unless dst is it.
+void build_table_into(fp_ctx* ctx, const fp_instance* in, double radius_km, double* dst) {
+  const int M = in->n_missions, B = in->n_bases;
+  cudaStream_t st = ctx->stream;
+  DBuf<double> pts(6ull * M + 3ull * B, st);
+  double* plat = pts.p;
+  double* plon = plat + M;
+  double* dlat = plon + M;
+  double* dlon = dlat + M;
+  double* blat = dlon + M;
+  double* blon = blat + B;
+  double* cosv = blon + B;  // [B + 2M]: bases, pickups, deliveries
+  h2d(plat, in->pickup_lat, M, st);
+  h2d(plon, in->pickup_lon, M, st);
+  h2d(dlat, in->delivery_lat, M, st);
+  h2d(dlon, in->delivery_lon, M, st);
+  h2d(blat, in->base_lat, B, st);
+  h2d(blon, in->base_lon, B, st);
+  check(fpk::launch_point_cos(blat, B, cosv, st), "cos(bases)");
+  check(fpk::launch_point_cos(plat, M, cosv + B, st), "cos(pickups)");
+  check(fpk::launch_point_cos(dlat, M, cosv + B + M, st), "cos(deliveries)");
+  EvTimer tk(st);
+  int sites = 0;
+  check(fpk::launch_table_auto(blat, blon, cosv, B, plat, plon, cosv + B, dlat, dlon,
+                               cosv + B + M, M, radius_km, dst, st, &sites),
+        "table_kernel");
+  ctx->last_kernel_ms = tk.stop_ms();
+  ctx->launches += sites ? 10 : 4;
+}
 
 // ---- permutations (proj/include/fleetplace/rng.hpp:14-42) ------------------
 struct PermStream {
@@ -477,7 +536,7 @@ struct Trace {
 
 // Shared driver for fp_search / fp_search_batch. `tables[s]` is a device
 // pointer to scenario s's table (nullptr = the scenario's arena copy).
-void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_config* cfg,
+void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_config* cfgs,
                 const fp_search_start* starts, fp_search_result* outs,
                 const std::vector<const double*>& dev_tables,
                 const std::vector<const double*>& host_tables) {
@@ -485,10 +544,30 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   for (int s = 1; s < n; ++s)
     if (insts[s].n_missions != M)
       throw FpError(FP_ERR_INVALID_ARGUMENT, "batch scenarios must share the mission count");
-  if (cfg->mode != FP_MODE_LOCAL && cfg->mode != FP_MODE_TABU)
-    throw FpError(FP_ERR_INVALID_ARGUMENT, "unknown search mode");
-  const bool tabu = cfg->mode == FP_MODE_TABU;
-  const long long tenure = resolve_tenure(cfg, M);
+  // per-scenario SearchConfig (tabu_search / local_search preconditions,
+  // proj/src/search.cpp:438-460); scenarios with the same seed share one
+  // permutation stream (the stream depends on the seed and M only)
+  std::vector<long long> tenures(n);
+  std::vector<int> pstream(n);
+  std::vector<uint64_t> seeds;
+  int max_passes_all = -2;  // the largest cap (-1: some scenario has none)
+  bool any_tabu = false, any_debug = false;
+  {
+    std::unordered_map<uint64_t, int> sidx;
+    for (int s = 0; s < n; ++s) {
+      const fp_search_config* c = &cfgs[s];
+      if (c->mode != FP_MODE_LOCAL && c->mode != FP_MODE_TABU)
+        throw FpError(FP_ERR_INVALID_ARGUMENT, "unknown search mode");
+      tenures[s] = resolve_tenure(c, M);
+      any_tabu |= c->mode == FP_MODE_TABU;
+      any_debug |= c->debug_check_deltas != 0;
+      auto it = sidx.emplace(c->seed, (int)seeds.size());
+      if (it.second) seeds.push_back(c->seed);
+      pstream[s] = it.first->second;
+      max_passes_all = c->max_passes < 0 || max_passes_all == -1 ? -1 : std::max(max_passes_all, c->max_passes);
+    }
+  }
+  const int D = (int)seeds.size();
   cudaStream_t st = ctx->stream;
   const Trace tr;
 
@@ -529,11 +608,13 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // In-kernel chunks hold up to 1024 passes (64 MB of permutations); a
   // single scenario's chunks grow 32, 64, ... so a short search generates
   // few permutations.
-  int kmax = (int)std::max<long long>(
-      1, std::min<long long>(inkernel ? 1024 : 16,
-                             ((inkernel ? 64ll : 16ll) << 20) / (8ll * std::max(M, 1))));
+  // (several permutation streams: their chunks share a budget of up to 24x
+  // one stream's, permutations and device draws together)
+  const long long budget = ((inkernel ? 64ll : 16ll) << 20) * std::min(D, 24);
+  const long long per_pass = (inkernel ? 24ll : 8ll) * std::max(M, 1) * D;
+  int kmax = (int)std::max<long long>(1, std::min<long long>(inkernel ? 1024 : 16, budget / per_pass));
   if (const char* e = std::getenv("FLEETPLACE_KPASSES")) kmax = std::max(1, std::atoi(e));
-  const size_t chunk_ints = 2ull * kmax * M + 2;
+  const size_t chunk_ints = 2ull * kmax * M * D + 2;
   // ---- device workspace (owned by the context, reused across calls):
   // arena | row-major table copies | counters | scenarios | active | perms.
   // The row-major copy of each table (mission-major: one mission's costs at
@@ -570,9 +651,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   const size_t o_B = align_up(totalA), o_ctr = align_up(o_B + totalB), o_scs = align_up(o_ctr + sizeof(fpk::Counters) * n),
                o_act = align_up(o_scs + sizeof(fpk::Scenario) * n),
                o_perm = align_up(o_act + 4ull * n), o_mt = align_up(o_perm + 4ull * chunk_ints),
-               o_pbad = align_up(o_mt + sizeof(fpk::MtState)),
+               o_pbad = align_up(o_mt + sizeof(fpk::MtState) * D),
                o_draws = align_up(o_pbad + sizeof(int)),
-               o_costT = align_up(o_draws + (inkernel ? 16ull * kmax * (size_t)std::max(M - 1, 0) : 0));
+               o_costT = align_up(o_draws + (inkernel ? 16ull * kmax * (size_t)std::max(M - 1, 0) * D : 0));
   auto ws_get = [&](size_t bytes) -> bool {
     if (bytes <= ctx->ws_cap) return true;
     if (ctx->ws) {
@@ -691,15 +772,48 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.V = V;
     S.K = h.K;
     S.pool_cap = h.psize + V + 1;
+    S.tenure = tenures[s];
+    S.max_passes = cfgs[s].max_passes < 0 ? -1 : cfgs[s].max_passes;
+    S.tabu = cfgs[s].mode == FP_MODE_TABU;
+    S.debug = cfgs[s].debug_check_deltas != 0;
+    S.pstream = pstream[s];
   }
   cudaEvent_t ev0, ev1;
   check(cudaEventCreate(&ev0), "event");
   check(cudaEventCreate(&ev1), "event");
   // host tables (batches): straight from the caller's buffers into the
   // device region, before the timed search
-  for (int s = 0; s < n; ++s)
-    if (!dev_tables[s] && (size_t)M * insts[s].n_bases)
-      h2d(const_cast<double*>(run.scs[s].cost), host_tables[s], (size_t)M * insts[s].n_bases, st);
+  {
+    // caller tables: uploaded, then checked on the device (distances: finite, >= 0)
+    std::vector<const double*> cp;
+    std::vector<long long> cn;
+    long long mx = 0;
+    for (int s = 0; s < n; ++s)
+      if (!dev_tables[s] && (size_t)M * insts[s].n_bases) {
+        h2d(const_cast<double*>(run.scs[s].cost), host_tables[s], (size_t)M * insts[s].n_bases, st);
+        cp.push_back(run.scs[s].cost);
+        cn.push_back((long long)M * insts[s].n_bases);
+        mx = std::max(mx, cn.back());
+      }
+    if (!cp.empty()) {
+      const int k = (int)cp.size();
+      DBuf<unsigned char> tmp(16ull * k + 4ull * k, st);
+      const double** d_p = reinterpret_cast<const double**>(tmp.p);
+      long long* d_n = reinterpret_cast<long long*>(tmp.p + 8ull * k);
+      int* d_bad = reinterpret_cast<int*>(tmp.p + 16ull * k);
+      h2d(d_p, cp.data(), k, st);
+      h2d(d_n, cn.data(), k, st);
+      check(fpk::launch_table_check_multi(d_p, d_n, k, mx, d_bad, st), "table_check");
+      std::vector<int> bad(k);
+      d2h(bad.data(), d_bad, k, st);
+      check(cudaStreamSynchronize(st), "table check sync");
+      for (int x : bad)
+        if (x)
+          throw FpError(FP_ERR_INVALID_ARGUMENT,
+                        "the search needs distance tables whose entries are finite and >= 0");
+      ctx->launches += 1;
+    }
+  }
   check(cudaEventRecord(ev0, st), "event");
   h2d(d0, stage.data(), totalA, st);
   h2d(d_scs, run.scs.data(), n, st);
@@ -711,7 +825,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     for (auto& p : ctx->h_perm) check(cudaMallocHost(&p, sizeof(int32_t) * chunk_ints), "pinned");
     ctx->perm_cap = chunk_ints;
   }
-  double init_ms = 0.0, sweep_ms = 0.0;
+  double init_ms = 0.0, sweep_ms = 0.0, pass_ms = 0.0;
+  uint64_t pass_launches = 0;
   cudaEvent_t ei[5];
   for (auto& e : ei) check(cudaEventCreate(&e), "event");
   const bool transpose = cost_t && !(ctx_copy && ctx->costT_valid);
@@ -727,12 +842,13 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
                    (transpose && M > 0 && maxB > 0 ? 1 : 0);
   tr.mark("allocated, staged, init launched");
   std::vector<cudaEvent_t> sweep_ev;  // (start, end) pairs around grid-wide sweeps
-  PermStream rng(cfg->seed);
+  std::vector<cudaEvent_t> pass_ev;   // (start, end) pairs around pass-kernel launches
+  std::vector<PermStream> rngs;
+  for (uint64_t sd : seeds) rngs.emplace_back(sd);
+  // a chunk of kk passes: stream d's 2*kk permutations at d * 2*kk*M
   auto gen_chunk = [&](int32_t* buf, int kk) {
-    for (int k = 0; k < kk; ++k) {
-      rng.perm(M, buf + 2ll * k * M);
-      rng.perm(M, buf + (2ll * k + 1) * M);
-    }
+    for (int d = 0; d < D; ++d)
+      for (int k = 0; k < 2 * kk; ++k) rngs[d].perm(M, buf + (2ll * kk * d + k) * M);
   };
   long long launched = 0;  // passes whose permutations went to the device
   // batches: one launch for (nearly) every search — a chunk boundary makes
@@ -741,7 +857,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   if (const char* e = std::getenv("FLEETPLACE_KFIRST")) kfirst = std::max(1, std::min(kmax, std::atoi(e)));
   auto next_chunk = [&](int prev) {
     int k = prev == 0 ? kfirst : std::min(kmax, 2 * prev);
-    if (cfg->max_passes >= 0) k = (int)std::max<long long>(1, std::min<long long>(k, cfg->max_passes - launched));
+    if (max_passes_all >= 0) k = (int)std::max<long long>(1, std::min<long long>(k, max_passes_all - launched));
     return k;
   };
   // In-kernel mode draws the permutations on the device (perm_kernels.cu):
@@ -751,9 +867,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   if (const char* e = std::getenv("FLEETPLACE_DEVICE_PERMS")) dev_perm = dev_perm && std::atoi(e) != 0;
   bool force_bad = std::getenv("FLEETPLACE_PERM_FORCE_BAD") != nullptr;  // test hook
   if (dev_perm) {
-    fpk::MtState seeded;
-    fpk::mt_seed_host(&seeded, cfg->seed);
-    h2d(d_mt, &seeded, 1, st);
+    std::vector<fpk::MtState> seeded(D);
+    for (int d = 0; d < D; ++d) fpk::mt_seed_host(&seeded[d], seeds[d]);
+    h2d(d_mt, seeded.data(), D, st);
     check(cudaMemsetAsync(d_pbad, 0, sizeof(int), st), "memset");
   }
   int kchunk = next_chunk(0);
@@ -774,19 +890,27 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   while (n_active > 0) {
     h2d(d_active, active.data(), n, st);
     if (dev_perm) {
-      check(fpk::launch_permutations(d_mt, M, 2 * kchunk, d_draws, d_perm, d_pbad, st),
+      check(fpk::launch_permutations(d_mt, D, M, 2 * kchunk, d_draws, d_perm, d_pbad, st),
             "permutations");
       ctx->launches += 2;
       if (force_bad) check(cudaMemsetAsync(d_pbad, 1, 1, st), "memset");
     } else {
-      h2d(d_perm, ctx->h_perm[buf], 2ull * kchunk * M, st);
+      h2d(d_perm, ctx->h_perm[buf], 2ull * kchunk * M * D, st);
     }
     if (inkernel) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, st);
       check(fpk::launch_pass(d_scs, d_active, n, d_perm, kchunk, true,
-                             cfg->max_passes, M, tabu, tenure, cfg->debug_check_deltas != 0, maxV,
+                             max_passes_all, M, any_tabu, tenures[0], any_debug, maxV,
                              maxB, maxK, st, threads, 0, 0u, dev_perm ? d_pbad : nullptr),
             "pass_kernel");
+      cudaEventRecord(e1, st);
+      pass_ev.push_back(e0);
+      pass_ev.push_back(e1);
       ctx->launches += 1;
+      pass_launches += 1;
     } else {
       for (int k = 0; k < kchunk; ++k) {
         cudaEvent_t e0, e1;
@@ -799,11 +923,17 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
         sweep_ev.push_back(e0);
         sweep_ev.push_back(e1);
         check(fpk::launch_pass(d_scs, d_active, n, d_perm + 2ll * k * M, 1,
-                               false, cfg->max_passes, M, tabu, tenure,
-                               cfg->debug_check_deltas != 0, maxV, maxB, maxK, st, threads,
+                               false, max_passes_all, M, any_tabu, tenures[0],
+                               any_debug, maxV, maxB, maxK, st, threads,
                                helpers, ++epoch, nullptr),
               "pass_kernel");
+        cudaEvent_t e2;
+        cudaEventCreate(&e2);
+        cudaEventRecord(e2, st);
+        pass_ev.push_back(e1);
+        pass_ev.push_back(e2);
         ctx->launches += M > 0 ? 2 : 1;
+        pass_launches += 1;
       }
     }
     // next chunk's permutations while the device works
@@ -815,6 +945,15 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     int pbad = 0;
     if (dev_perm) d2h(&pbad, d_pbad, 1, st);
     check(cudaStreamSynchronize(st), "pass sync");
+    for (size_t e = 0; e + 1 < pass_ev.size(); e += 2) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, pass_ev[e], pass_ev[e + 1]);
+      pass_ms += ms;
+      // (in sweep mode the start event is the sweep's end event, destroyed below)
+      if (inkernel) cudaEventDestroy(pass_ev[e]);
+      cudaEventDestroy(pass_ev[e + 1]);
+    }
+    pass_ev.clear();
     for (size_t e = 0; e + 1 < sweep_ev.size(); e += 2) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, sweep_ev[e], sweep_ev[e + 1]);
@@ -829,9 +968,11 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       dev_perm = false;
       force_bad = false;
       launched -= kchunk;
-      rng = PermStream(cfg->seed);
       std::vector<int32_t> skip((size_t)std::max(M, 1));
-      for (long long p = 0; p < 2 * launched; ++p) rng.perm(M, skip.data());
+      for (int d = 0; d < D; ++d) {
+        rngs[d] = PermStream(seeds[d]);
+        for (long long p = 0; p < 2 * launched; ++p) rngs[d].perm(M, skip.data());
+      }
       gen_chunk(ctx->h_perm[buf], kchunk);
       tr.mark("device permutation chunk rejected: host stream");
       continue;
@@ -892,6 +1033,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     outs[s].init_ms = init_ms;
     for (int k = 0; k < 4; ++k) outs[s].init_part_ms[k] = init_part[k];
     outs[s].sweep_ms = sweep_ms;
+    outs[s].pass_ms = pass_ms;
+    outs[s].pass_launches = pass_launches;
     for (int k = 0; k < 16; ++k) outs[s].phase_cycles[k] = c.cycles[k];
     for (int k = 0; k < 5; ++k) outs[s].event_counts[k] = c.counts[k];
     outs[s].kernel_launches = ctx->launches;
@@ -964,7 +1107,7 @@ fp_status fp_permutations(fp_ctx* ctx, uint64_t seed, int32_t n, int32_t passes,
     fpk::mt_seed_host(&seeded, seed);
     h2d(d_mt.p, &seeded, 1, st);
     check(cudaMemsetAsync(d_bad.p, 0, sizeof(int), st), "memset");
-    check(fpk::launch_permutations(d_mt.p, n, np, d_draws.p, d_perms.p, d_bad.p, st), "perms");
+    check(fpk::launch_permutations(d_mt.p, 1, n, np, d_draws.p, d_perms.p, d_bad.p, st), "perms");
     ctx->launches += 2;
     int bad = 0;
     d2h(&bad, d_bad.p, 1, st);
@@ -1024,31 +1167,11 @@ fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* in, double rad
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
     const int M = in->n_missions, B = in->n_bases;
     cudaStream_t st = ctx->stream;
+    if (!(radius_km >= 0.0 && radius_km < INFINITY))
+      throw FpError(FP_ERR_INVALID_ARGUMENT, "radius_km must be finite and >= 0");
     table_alloc(ctx, M, B);
-    DBuf<double> pts(6ull * M + 3ull * B, st);
-    double* plat = pts.p;
-    double* plon = plat + M;
-    double* dlat = plon + M;
-    double* dlon = dlat + M;
-    double* blat = dlon + M;
-    double* blon = blat + B;
-    double* cosv = blon + B;  // [B + 2M]: bases, pickups, deliveries
-    h2d(plat, in->pickup_lat, M, st);
-    h2d(plon, in->pickup_lon, M, st);
-    h2d(dlat, in->delivery_lat, M, st);
-    h2d(dlon, in->delivery_lon, M, st);
-    h2d(blat, in->base_lat, B, st);
-    h2d(blon, in->base_lon, B, st);
-    check(fpk::launch_point_cos(blat, B, cosv, st), "cos(bases)");
-    check(fpk::launch_point_cos(plat, M, cosv + B, st), "cos(pickups)");
-    check(fpk::launch_point_cos(dlat, M, cosv + B + M, st), "cos(deliveries)");
-    EvTimer tk(st);
-    int sites = 0;
-    check(fpk::launch_table_auto(blat, blon, cosv, B, plat, plon, cosv + B, dlat, dlon,
-                                 cosv + B + M, M, radius_km, ctx->d_cost, st, &sites),
-          "table_kernel");
-    ctx->last_kernel_ms = tk.stop_ms();
-    ctx->launches += sites ? 10 : 4;
+    build_table_into(ctx, in, radius_km, ctx->d_cost);
+    ctx->table_ok = true;  // haversine sums: finite and >= 0 for valid coordinates
     start_costT(ctx);
     if (out_cost) d2h(out_cost, ctx->d_cost, (size_t)M * B, st);
     check(cudaStreamSynchronize(st), "table sync");
@@ -1087,8 +1210,13 @@ fp_status fp_table_upload(fp_ctx* ctx, int32_t n_missions, int32_t n_bases,
                           const double* cost_colmajor) {
   return guarded([&] {
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (n_missions < 0 || n_bases < 0 || ((size_t)n_missions * n_bases > 0 && !cost_colmajor))
+      throw FpError(FP_ERR_INVALID_ARGUMENT, "bad table shape or NULL table");
     table_alloc(ctx, n_missions, n_bases);
     h2d(ctx->d_cost, cost_colmajor, (size_t)n_missions * n_bases, ctx->stream);
+    // a caller's matrix may hold anything: column_totals stays exact for any
+    // entries, the search requires distances (checked on the device)
+    ctx->table_ok = table_entries_ok(ctx->d_cost, (size_t)n_missions * n_bases, ctx->stream);
     start_costT(ctx);
     check(cudaStreamSynchronize(ctx->stream), "upload sync");
   });
@@ -1309,35 +1437,89 @@ fp_status fp_search(fp_ctx* ctx, const fp_instance* inst, const fp_search_config
   return guarded([&] {
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
     ensure_table(ctx, inst->n_missions, inst->n_bases);
+    if (!ctx->table_ok)
+      throw FpError(FP_ERR_INVALID_ARGUMENT,
+                    "the search needs a distance table whose entries are finite and >= 0");
     run_search(ctx, 1, inst, cfg, start, out, {ctx->d_cost}, {nullptr});
+  });
+}
+
+fp_status fp_search_batch_configs(fp_ctx* ctx, int32_t n, const fp_instance* insts,
+                                  const double* const* tables, double radius_km,
+                                  const fp_search_config* cfgs, const fp_search_start* starts,
+                                  fp_search_result* outs) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (n <= 0) return;
+    if (!insts || !cfgs || !starts || !outs) throw FpError(FP_ERR_INVALID_ARGUMENT, "NULL batch array");
+    const int M = insts[0].n_missions;
+    for (int s = 1; s < n; ++s)
+      if (insts[s].n_missions != M)
+        throw FpError(FP_ERR_INVALID_ARGUMENT, "batch scenarios must share the mission count");
+    std::vector<const double*> dev(n, nullptr), host(n, nullptr);
+    // scenarios without a host table: kernel (1) for all of them in one
+    // launch, into a scratch buffer (the context's resident table is untouched)
+    std::vector<int> build;
+    for (int s = 0; s < n; ++s) {
+      if (tables && tables[s]) host[s] = tables[s];
+      else build.push_back(s);
+    }
+    DBuf<double> built, pts;
+    DBuf<fpk::TableJob> d_jobs;
+    if (!build.empty()) {
+      if (!(radius_km >= 0.0 && radius_km < INFINITY))
+        throw FpError(FP_ERR_INVALID_ARGUMENT, "radius_km must be finite and >= 0");
+      cudaStream_t st = ctx->stream;
+      size_t tot = 0, npts = 0;
+      int maxB = 0;
+      for (int s : build) {
+        tot += (size_t)M * insts[s].n_bases;
+        npts += (size_t)insts[s].n_bases + 2ull * M;
+        maxB = std::max(maxB, insts[s].n_bases);
+      }
+      built = DBuf<double>(tot + 2, st);
+      // points: [lat | lon | cos] regions, each [bases, pickups, deliveries] per scenario
+      std::vector<double> hp(2 * npts);
+      pts = DBuf<double>(3 * npts + 1, st);
+      std::vector<fpk::TableJob> jobs(build.size());
+      size_t po = 0, to = 0;
+      for (size_t k = 0; k < build.size(); ++k) {
+        const fp_instance& in = insts[build[k]];
+        const int B = in.n_bases;
+        std::copy(in.base_lat, in.base_lat + B, hp.begin() + po);
+        std::copy(in.pickup_lat, in.pickup_lat + M, hp.begin() + po + B);
+        std::copy(in.delivery_lat, in.delivery_lat + M, hp.begin() + po + B + M);
+        std::copy(in.base_lon, in.base_lon + B, hp.begin() + npts + po);
+        std::copy(in.pickup_lon, in.pickup_lon + M, hp.begin() + npts + po + B);
+        std::copy(in.delivery_lon, in.delivery_lon + M, hp.begin() + npts + po + B + M);
+        const double* la = pts.p + po;
+        const double* lo = pts.p + npts + po;
+        const double* co = pts.p + 2 * npts + po;
+        jobs[k] = fpk::TableJob{la, lo, co, la + B, lo + B, co + B, la + B + M, lo + B + M,
+                                co + B + M, built.p + to, B};
+        dev[build[k]] = built.p + to;
+        po += (size_t)B + 2ull * M;
+        to += (size_t)M * B;
+      }
+      h2d(pts.p, hp.data(), 2 * npts, st);
+      d_jobs = DBuf<fpk::TableJob>(build.size(), st);
+      h2d(d_jobs.p, jobs.data(), build.size(), st);
+      check(fpk::launch_point_cos(pts.p, (int)npts, pts.p + 2 * npts, st), "cos(points)");
+      check(fpk::launch_table_batch(d_jobs.p, (int)build.size(), M, maxB, radius_km, st),
+            "table_batch");
+      ctx->launches += 2;
+    }
+    run_search(ctx, n, insts, cfgs, starts, outs, dev, host);
   });
 }
 
 fp_status fp_search_batch(fp_ctx* ctx, int32_t n, const fp_instance* insts,
                           const double* const* tables, const fp_search_config* cfg,
                           const fp_search_start* starts, fp_search_result* outs) {
-  return guarded([&] {
-    check(cudaSetDevice(ctx->device), "cudaSetDevice");
-    if (n <= 0) return;
-    std::vector<const double*> dev(n, nullptr), host(n, nullptr);
-    std::vector<DBuf<double>> built;
-    for (int s = 0; s < n; ++s) {
-      if (tables && tables[s]) {
-        host[s] = tables[s];
-      } else {
-        // build this scenario's table on the device, keep it in the arena copy
-        fp_status rc = fp_build_distance_table(ctx, &insts[s], 6371.0088, nullptr);
-        if (rc != FP_OK) throw FpError(rc, g_err);
-        built.emplace_back((size_t)insts[s].n_missions * insts[s].n_bases);
-        check(cudaMemcpyAsync(built.back().p, ctx->d_cost,
-                              sizeof(double) * insts[s].n_missions * insts[s].n_bases,
-                              cudaMemcpyDeviceToDevice, ctx->stream),
-              "D2D");
-        dev[s] = built.back().p;
-      }
-    }
-    run_search(ctx, n, insts, cfg, starts, outs, dev, host);
-  });
+  if (n <= 0) return FP_OK;
+  if (!cfg) return fail(FP_ERR_INVALID_ARGUMENT, "NULL search config");
+  std::vector<fp_search_config> cfgs((size_t)n, *cfg);
+  return fp_search_batch_configs(ctx, n, insts, tables, 6371.0088, cfgs.data(), starts, outs);
 }
 
 fp_status fp_enumerate_moves(fp_ctx* ctx, const fp_instance* in, const fp_search_start* state,
@@ -1384,14 +1566,23 @@ fp_status fp_enumerate_moves(fp_ctx* ctx, const fp_instance* in, const fp_search
   });
 }
 
-fp_status fp_objective_km(fp_ctx* ctx, const int32_t* vehicle_base, const int32_t* mission_vehicle,
-                          double* out_km) {
+fp_status fp_objective_km(fp_ctx* ctx, int32_t n_vehicles, const int32_t* vehicle_base,
+                          const int32_t* mission_vehicle, double* out_km) {
   return guarded([&] {
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (ctx->M < 0) throw FpError(FP_ERR_INVALID_ARGUMENT, "no resident table");
-    const int M = ctx->M;
-    int V = 0;
-    for (int m = 0; m < M; ++m) V = std::max(V, mission_vehicle[m] + 1);
+    const int M = ctx->M, V = n_vehicles;
+    if (V < 0 || (V > 0 && !vehicle_base) || (M > 0 && !mission_vehicle) || !out_km)
+      throw FpError(FP_ERR_INVALID_ARGUMENT, "bad objective arguments");
+    // every mission served by a vehicle placed on a base of the table
+    // (objective_km throws InfeasibleError otherwise, proj/src/model.cpp:178-181)
+    for (int m = 0; m < M; ++m) {
+      const int v = mission_vehicle[m];
+      if (v < 0 || v >= V)
+        throw FpError(FP_ERR_INFEASIBLE, "mission index " + std::to_string(m) + " is not served");
+      if (vehicle_base[v] < 0 || vehicle_base[v] >= ctx->B)
+        throw FpError(FP_ERR_INFEASIBLE, "service references unplaced vehicle index " + std::to_string(v));
+    }
     cudaStream_t st = ctx->stream;
     DBuf<int32_t> d_vb(V + 1), d_mv((size_t)M + 1);
     DBuf<double> d_out(1);

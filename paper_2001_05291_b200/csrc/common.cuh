@@ -86,6 +86,13 @@ constexpr int kRowsChunk = 256;
 constexpr int kNoBinade = -100000;
 
 // std::mt19937_64 state (the search's permutation stream, perm_kernels.cu).
+// One scenario's table build in a batched kernel (1) launch.
+struct TableJob {
+  const double *blat, *blon, *bcos, *plat, *plon, *pcos, *dlat, *dlon, *dcos;
+  double* cost;
+  int B;
+};
+
 struct MtState {
   unsigned long long mt[312];
   int idx;
@@ -162,6 +169,13 @@ struct Scenario {
                              //   chunk holds a rounding tie / a huge term / no prediction
   Counters* ctr;
   int32_t M, B, V, K, pool_cap, nwd, nvw;
+  // per-scenario SearchConfig (a batch may mix seeds, modes, tenures and
+  // pass caps: run_experiment's attempts, proj/src/bench.cpp:125-128)
+  long long tenure;          // resolved tabu tenure (0 in local mode)
+  int32_t max_passes;        // < 0: no cap
+  int32_t tabu;              // 1 = tabu_search, 0 = local_search
+  int32_t debug;             // debug_check_deltas
+  int32_t pstream;           // index of this scenario's permutation stream in a chunk
 };
 
 }  // namespace fpk

@@ -15,8 +15,15 @@ struct MtState;
 
 void mt_seed_host(MtState* st, unsigned long long seed);
 size_t fy_smem_bytes(int n);
-cudaError_t launch_permutations(MtState* st, int n, int nperm, unsigned long long* draws,
-                                int32_t* perms, int* bad, cudaStream_t stream);
+cudaError_t launch_permutations(MtState* st, int nstreams, int n, int nperm,
+                                unsigned long long* draws, int32_t* perms, int* bad,
+                                cudaStream_t stream);
+cudaError_t launch_table_check(const double* t, size_t n, int* bad, cudaStream_t st);
+cudaError_t launch_table_check_multi(const double* const* d_ptrs, const long long* d_ns, int count,
+                                     long long max_n, int* d_bad, cudaStream_t st);
+struct TableJob;
+cudaError_t launch_table_batch(const TableJob* d_jobs, int n_jobs, int M, int max_B,
+                               double radius_km, cudaStream_t st);
 
 cudaError_t launch_point_cos(const double* lat, int n, double* out, cudaStream_t st);
 cudaError_t launch_transpose(const double* src, int M, int B, double* dst, cudaStream_t stream);

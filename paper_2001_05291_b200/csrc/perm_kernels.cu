@@ -43,11 +43,13 @@ __device__ __forceinline__ unsigned long long temper(unsigned long long x) {
 
 }  // namespace
 
-// Appends `count` outputs of the generator held in *st to out. One block of
-// 320 threads.
+// Appends `count` outputs of the generator held in st[blockIdx.x] to
+// out + blockIdx.x * count. One block of 320 threads per stream.
 __global__ void __launch_bounds__(320) mt_gen_kernel(MtState* st, unsigned long long* out,
                                                      long long count) {
   __shared__ unsigned long long mt[312];
+  st += blockIdx.x;
+  out += (long long)blockIdx.x * count;
   const int t = threadIdx.x;
   for (int k = t; k < 312; k += blockDim.x) mt[k] = st->mt[k];
   int idx = st->idx;
@@ -118,15 +120,18 @@ void mt_seed_host(MtState* st, unsigned long long seed) {
 
 size_t fy_smem_bytes(int n) { return sizeof(int) * (2ull * n + 1); }
 
-// nperm permutations of n (n >= 2) into perms, continuing the stream in *st;
-// draws is scratch of nperm * (n - 1) words.
-cudaError_t launch_permutations(MtState* st, int n, int nperm, unsigned long long* draws,
-                                int32_t* perms, int* bad, cudaStream_t stream) {
-  if (nperm <= 0) return cudaSuccess;
-  mt_gen_kernel<<<1, 320, 0, stream>>>(st, draws, (long long)nperm * (n - 1));
+// For each of `nstreams` independent streams (states st[0..nstreams)),
+// nperm permutations of n (n >= 2) continuing that stream, written stream
+// after stream: perms[(d * nperm + p) * n ...]. draws is scratch of
+// nstreams * nperm * (n - 1) words.
+cudaError_t launch_permutations(MtState* st, int nstreams, int n, int nperm,
+                                unsigned long long* draws, int32_t* perms, int* bad,
+                                cudaStream_t stream) {
+  if (nperm <= 0 || nstreams <= 0) return cudaSuccess;
+  mt_gen_kernel<<<nstreams, 320, 0, stream>>>(st, draws, (long long)nperm * (n - 1));
   const size_t smem = fy_smem_bytes(n);
   cudaFuncSetAttribute(fy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fy_kernel<<<nperm, 256, smem, stream>>>(draws, n, perms, bad);
+  fy_kernel<<<nstreams * nperm, 256, smem, stream>>>(draws, n, perms, bad);
   return cudaGetLastError();
 }
 

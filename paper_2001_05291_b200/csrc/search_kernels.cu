@@ -2116,7 +2116,14 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   if (g.ctr->done) return;  // finished earlier in this chunk of launches
   const long long t_entry = clock64();  // phase 15: the whole launch (block 0's SM clock)
   Scenario s = g;
-  const bool tabu = tabu_i != 0, debug = debug_i != 0;
+  // the scenario's own SearchConfig and permutation stream (a chunk holds
+  // 2 * kpasses permutations per stream, stream after stream)
+  (void)tabu_i;
+  (void)debug_i;
+  const bool tabu = g.tabu != 0, debug = g.debug != 0;
+  tenure = g.tenure;
+  max_passes = g.max_passes;
+  perms += (long long)g.pstream * 2ll * kpasses * g.M;
   __shared__ Shared sh;
   extern __shared__ __align__(16) unsigned char dyn[];
   constexpr int NW = NT / 32;

@@ -14,6 +14,7 @@
 // through shared memory so each lane owns one column's chain.
 
 #include <cfloat>
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 
@@ -64,6 +65,25 @@ __global__ void __launch_bounds__(256)
     const double la = blat[b], lo = blon[b], ca = bcos[b];
     const double c = __dadd_rn(hav(la, lo, ca, pl, po, pc, two_r), hav(la, lo, ca, dl, d_o, dc, two_r));
     cost[(long long)b * M + m] = c;
+  }
+}
+
+// The same for a batch of scenarios of one mission count (grid.y = scenario x
+// base tile): every scenario's table in one launch.
+__global__ void __launch_bounds__(256)
+    table_batch_kernel(const TableJob* __restrict__ jobs, int M, int tiles_per, int bases_per_block,
+                       double two_r) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  const TableJob& jb = jobs[blockIdx.y / tiles_per];
+  const int b0 = (blockIdx.y % tiles_per) * bases_per_block;
+  if (m >= M || b0 >= jb.B) return;
+  const double pl = jb.plat[m], po = jb.plon[m], pc = jb.pcos[m];
+  const double dl = jb.dlat[m], d_o = jb.dlon[m], dc = jb.dcos[m];
+  const int b1 = min(jb.B, b0 + bases_per_block);
+  for (int b = b0; b < b1; ++b) {
+    const double la = jb.blat[b], lo = jb.blon[b], ca = jb.bcos[b];
+    jb.cost[(long long)b * M + m] =
+        __dadd_rn(hav(la, lo, ca, pl, po, pc, two_r), hav(la, lo, ca, dl, d_o, dc, two_r));
   }
 }
 
@@ -432,6 +452,15 @@ cudaError_t launch_table_auto(const double* blat, const double* blon, const doub
   return cudaGetLastError();
 }
 
+cudaError_t launch_table_batch(const TableJob* d_jobs, int n_jobs, int M, int max_B,
+                               double radius_km, cudaStream_t st) {
+  if (n_jobs <= 0 || M <= 0 || max_B <= 0) return cudaSuccess;
+  const int bpb = 8, tiles = (max_B + bpb - 1) / bpb;
+  dim3 grid((M + 255) / 256, n_jobs * tiles);
+  table_batch_kernel<<<grid, 256, 0, st>>>(d_jobs, M, tiles, bpb, 2.0 * radius_km);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_haversine_pairs(int n, const double* alat, const double* alon,
                                    const double* blat, const double* blon, const double* clat,
                                    const double* clon, double radius_km, double* out,
@@ -443,8 +472,15 @@ cudaError_t launch_haversine_pairs(int n, const double* alat, const double* alon
 }
 
 // rn(x / u) for u = 2^(e-52), exact power-of-two scaling; tie flag; a term
-// >= 4e15 u leaves the binade by itself.
+// >= 4e15 u leaves the binade by itself. A term that is negative, infinite
+// or NaN is flagged like a tie: the integer-binade step assumes a running
+// sum that only grows, so such a term is always added with a true fp64 add
+// (any caller matrix is summed exactly like the reference's loop).
 __device__ __forceinline__ long long col_round(double x, double inv_u, bool& tie) {
+  if (!(x >= 0.0 && x < INFINITY)) {
+    tie = true;
+    return 0;
+  }
   const double y = x * inv_u;
   tie = false;
   if (y >= 4.0e15) return 1ll << 53;
@@ -475,11 +511,18 @@ __global__ void __launch_bounds__(256)
   // a mission shard continues the chain of the shards before it
   double S = carry ? carry[b] : 0.0;
   int k = 0;
-  if (l == 0)
-    while (k < M && !(S >= 0x1p-900)) S = __dadd_rn(S, col[k++]);  // leading zeros / tiny values
-  S = __shfl_sync(FULL, S, 0);
-  k = __shfl_sync(FULL, k, 0);
   while (k < M) {
+    if (!(S >= 0x1p-900 && S < INFINITY)) {
+      // leading zeros / tiny values, or a running sum a negative or
+      // non-finite term left outside the positive normal range: plain
+      // sequential adds until it is back (never, for an infinite or NaN sum)
+      if (l == 0)
+        do S = __dadd_rn(S, col[k++]);
+        while (k < M && !(S >= 0x1p-900 && S < INFINITY));
+      S = __shfl_sync(FULL, S, 0);
+      k = __shfl_sync(FULL, k, 0);
+      continue;
+    }
     const int e = ilogb(S);
     const double u = ldexp(1.0, e - 52), inv_u = ldexp(1.0, 52 - e);
     const long long N0 = (long long)(S * inv_u);
@@ -535,6 +578,56 @@ __global__ void __launch_bounds__(256)
     k = ev + 1;
   }
   if (l == 0) out[b] = S;
+}
+
+// Flags a table holding any entry that is negative, infinite or NaN (the
+// search's exact-sum machinery assumes distances: finite and >= 0).
+// HBM-bound streaming read, 16-byte loads, one flag write per offending block.
+__global__ void __launch_bounds__(256)
+    table_check_kernel(const double2* __restrict__ t2, size_t n2, const double* __restrict__ tail,
+                       int ntail, int* __restrict__ bad) {
+  bool ok = true;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n2;
+       k += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = t2[k];
+    ok &= (v.x >= 0.0 && v.x < INFINITY) && (v.y >= 0.0 && v.y < INFINITY);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < ntail) ok &= tail[threadIdx.x] >= 0.0 && tail[threadIdx.x] < INFINITY;
+  if (__syncthreads_or(!ok) && threadIdx.x == 0) *bad = 1;
+}
+
+// Several tables (blockIdx.y = table): bad[y] = 1 when table y holds an
+// entry that is negative, infinite or NaN.
+__global__ void __launch_bounds__(256)
+    table_check_multi_kernel(const double* const* __restrict__ ptrs, const long long* __restrict__ ns,
+                             int* __restrict__ bad) {
+  const double* t = ptrs[blockIdx.y];
+  const long long n = ns[blockIdx.y];
+  bool ok = true;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    ok &= t[k] >= 0.0 && t[k] < INFINITY;
+  if (__syncthreads_or(!ok) && threadIdx.x == 0) bad[blockIdx.y] = 1;
+}
+
+cudaError_t launch_table_check_multi(const double* const* d_ptrs, const long long* d_ns, int count,
+                                     long long max_n, int* d_bad, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(d_bad, 0, sizeof(int) * count, st);
+  if (e != cudaSuccess || count <= 0 || max_n <= 0) return e;
+  const int bx = (int)std::max<long long>(1, std::min<long long>((max_n + 1023) / 1024, 64));
+  table_check_multi_kernel<<<dim3(bx, count), 256, 0, st>>>(d_ptrs, d_ns, d_bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_table_check(const double* t, size_t n, int* bad, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), st);
+  if (e != cudaSuccess || n == 0) return e;
+  // the table is 256-byte aligned (cudaMalloc); an odd count leaves one tail entry
+  const size_t n2 = n / 2;
+  const int blocks = (int)std::min<size_t>(148ull * 8, (n2 + 255) / 256 + 1);
+  table_check_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(t), n2, t + 2 * n2,
+                                             (int)(n - 2 * n2), bad);
+  return cudaGetLastError();
 }
 
 // Columns [0, B) of `cost` (pre-offset by the caller for a column range),

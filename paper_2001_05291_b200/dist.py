@@ -9,7 +9,7 @@ search on every rank (weak scaling by replication).
 """
 from __future__ import annotations
 
-from typing import Callable, Sequence
+from typing import Callable
 
 
 def shard(n: int, rank: int, world: int) -> range:
@@ -45,20 +45,3 @@ def run_sharded(n: int, solve: Callable[[range], tuple], group=None):
         out.extend(res)
     assert len(out) == n
     return out, tmax
-
-
-def scenario_batch_solver(insts: Sequence, starts: Sequence, cfg, device: int) -> Callable:
-    """Returns a `solve(range)` running fleetplace.search_batch on `device`."""
-    import time
-
-    from . import fleetplace as F
-
-    def solve(rg: range):
-        if len(rg) == 0:
-            return [], 0.0
-        t0 = time.perf_counter()
-        res = F.search_batch([insts[k] for k in rg], [starts[k] for k in rg], cfg, device=device)
-        dev_s = max(r.stats.device_ms for r in res) / 1e3 if res else time.perf_counter() - t0
-        return [(r.vehicle_base, r.mission_vehicle, r.stats) for r in res], dev_s
-
-    return solve

@@ -525,6 +525,8 @@ class SearchStats:
     init_ms: float = 0.0
     sweep_ms: float = 0.0
     init_part_ms: tuple = ()
+    pass_ms: float = 0.0
+    pass_launches: int = 0
 
 
 @dataclass
@@ -592,7 +594,8 @@ def _stats(r: A.fp_search_result) -> SearchStats:
                        int(s.tabu_skips_outer), int(s.tabu_skips_inner), float(s.final_objective_km),
                        float(r.device_ms), int(r.exact_fallbacks), tuple(int(x) for x in r.phase_cycles),
                        tuple(int(x) for x in r.event_counts), float(r.init_ms),
-                       float(r.sweep_ms), tuple(float(x) for x in r.init_part_ms))
+                       float(r.sweep_ms), tuple(float(x) for x in r.init_part_ms),
+                       float(r.pass_ms), int(r.pass_launches))
 
 
 def search_arrays(inst: Instance, t: DistanceTable, cfg: SearchConfig, vehicle_base: np.ndarray,
@@ -755,7 +758,8 @@ def objective_km(a: Assignment, inst: Instance, t: DistanceTable) -> float:
         vb[vmap[vid]] = bmap[bid]
     mv = np.array([vmap[a.service[int(m)]] for m in inst.mission_id.tolist()], np.int32)
     out = C.c_double(0.0)
-    _check(lib().fp_objective_km(t._ctx.p, A.ptr(vb, C.c_int32), A.ptr(mv, C.c_int32), C.byref(out)))
+    _check(lib().fp_objective_km(t._ctx.p, inst.n_vehicles, A.ptr(vb, C.c_int32),
+                                 A.ptr(mv, C.c_int32), C.byref(out)))
     return out.value
 
 
@@ -803,16 +807,21 @@ def small_generated(seed: int, missions: int = 10, aerodromes: int = 12, helipad
 
 
 # ------------------------------------------------------------------ batch ----
-def search_batch(insts: Sequence[Instance], starts: Sequence[tuple], cfg: SearchConfig,
+def search_batch(insts: Sequence[Instance], starts: Sequence[tuple], cfg,
                  tables: Optional[Sequence[Optional[np.ndarray]]] = None,
-                 device: int = 0, ctx: Optional["_Ctx"] = None) -> list:
-    """Independent scenarios of one mission count searched concurrently, one
-    thread block per scenario (C ABI fp_search_batch). `starts[s]` is the
-    index-form start (vehicle_base, mission_vehicle, pool_kind, pool_index);
-    `tables[s]` a flat column-major host table or None to build it on the
-    device. `ctx`: a long-lived context (`_Ctx(device)`) whose workspace is
-    reused across batches, as a serving process keeps one; default a fresh
-    one per call. Returns one SearchResult per scenario."""
+                 device: int = 0, ctx: Optional["_Ctx"] = None,
+                 radius_km: float = kEarthRadiusKm) -> list:
+    """Independent searches of one mission count run concurrently, one thread
+    block per scenario (C ABI fp_search_batch_configs). `cfg` is one
+    SearchConfig for all or a sequence with one per scenario (e.g. the
+    multi-attempt protocol: attempt t with seed + t, proj/src/bench.cpp:
+    125-128). `starts[s]` is the index-form start (vehicle_base,
+    mission_vehicle, pool_kind, pool_index); `tables[s]` a flat column-major
+    host table or None to build it on the device (kernel (1), all such
+    tables in one launch). `ctx`: a long-lived context (`_Ctx(device)`)
+    whose workspace is reused across batches, as a serving process keeps
+    one; default a fresh one per call. Returns one SearchResult per
+    scenario."""
     n = len(insts)
     ctx = ctx if ctx is not None else _Ctx(device)
     ci = (A.fp_instance * n)(*[x.c() for x in insts])
@@ -838,7 +847,10 @@ def search_batch(insts: Sequence[Instance], starts: Sequence[tuple], cfg: Search
         omv = np.empty(insts[s].n_missions, np.int32)
         outs.append((ovb, omv))
         res[s].vehicle_base, res[s].mission_vehicle = A.ptr(ovb, C.c_int32), A.ptr(omv, C.c_int32)
-    c = _cfg_c(cfg)
-    _check(lib().fp_search_batch(ctx.p, n, ci, tp, C.byref(c), st, res))
+    cfgs = [cfg] * n if isinstance(cfg, SearchConfig) else list(cfg)
+    if len(cfgs) != n:
+        raise InvalidArgument("one SearchConfig per scenario")
+    cc = (A.fp_search_config * n)(*[_cfg_c(c) for c in cfgs])
+    _check(lib().fp_search_batch_configs(ctx.p, n, ci, tp, float(radius_km), cc, st, res))
     return [SearchResult(outs[s][0], outs[s][1], _stats(res[s]), int(res[s].kernel_launches))
             for s in range(n)]

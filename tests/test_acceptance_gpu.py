@@ -35,3 +35,14 @@ def test_reference_acceptance_suite_on_the_drop_in():
         assert gpu[k] == cpu[k], (k, cpu[k], gpu[k])
     # 6 compares against the nondeterministic parallel_tabu_search: verdict only
     assert gpu[6].startswith("PASS") and cpu[6].startswith("PASS")
+
+
+def test_adapter_objective_and_feasibility_match_reference():
+    """The drop-in's O(M) check_feasible and objective_km (device sum) equal
+    the reference's O(M^2) ones on fuzzed and ranked assignments."""
+    exe = REF / "adapter_check"
+    if not exe.exists():
+        pytest.skip(f"{exe} not built")
+    r = subprocess.run([str(exe), "--gpu"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 mismatches" in r.stdout and " 0 objectives" not in r.stdout

@@ -285,6 +285,85 @@ def test_column_totals_exact_on_adversarial_columns():
     assert np.array_equal(got.view(np.int64), want.view(np.int64)), (got, want)
 
 
+def test_column_totals_exact_for_any_matrix():
+    """column_totals takes any MatrixXd (proj/src/rank.cpp:10-23): negative,
+    infinite and NaN entries, sums that go negative, leave the normal range
+    or return to it, are summed exactly like the reference's loop (those
+    terms take true fp64 adds); compared with the compiled reference."""
+    rng = np.random.default_rng(11)
+    M = 4096 + 77
+    cols = [
+        np.concatenate([[1.0], [-0.6 * 2.0 ** -52], rng.uniform(0, 1, M - 2)]),   # ADVICE example
+        rng.uniform(-1e3, 1e3, M),                                             # mixed signs
+        np.concatenate([rng.uniform(0, 10, M // 2), -rng.uniform(0, 10, M - M // 2)]),
+        np.concatenate([rng.uniform(0, 1, 100), [np.inf], rng.uniform(0, 1, M - 101)]),
+        np.concatenate([rng.uniform(0, 1, 100), [-np.inf], rng.uniform(0, 1, M - 101)]),
+        np.concatenate([rng.uniform(0, 1, 10), [np.nan], rng.uniform(0, 1, M - 11)]),
+        np.concatenate([[np.inf], rng.uniform(0, 1, 50), [-np.inf], rng.uniform(0, 1, M - 52)]),
+        np.concatenate([[1e300], [1e300] * 10, [-1e300] * 11, rng.uniform(0, 1, M - 22)]),
+        np.concatenate([[5.0], [-5.0], rng.uniform(0, 1e-310, 20), rng.uniform(0, 3, M - 22)]),
+        -rng.uniform(0, 1, M),
+    ]
+    table = np.stack(cols, axis=1)
+    t = F.DistanceTable.from_host(table)
+    got = F.column_totals(t)
+    flat = np.ascontiguousarray(table.T).reshape(-1)
+    want = np.empty(table.shape[1])
+    H._err(H.REF, H.REF.ref_column_totals(M, table.shape[1], H.P(flat, H.C.c_double), 0,
+                                          H.P(want, H.C.c_double)))
+    assert np.array_equal(got.view(np.int64), want.view(np.int64)), (got, want)
+
+
+def test_search_rejects_tables_that_are_not_distances():
+    """The search's exact-sum machinery needs finite, non-negative entries:
+    an uploaded table with a negative or non-finite entry is refused with
+    std::invalid_argument (single searches and batches alike)."""
+    inst = F.survey_instance(50, 200, 10, seed=1)
+    good = F.build_distance_table(inst)
+    start = F.rank_bases(inst, good)
+    st = F._state_arrays(start.assignment, F.initial_pool(start, inst), inst)
+    cfg = F.SearchConfig(seed=7, mode=F.SearchMode.Tabu)
+    for bad_value in (-1.0, np.inf, np.nan):
+        cost = good.cost.copy()
+        cost[17, 3] = bad_value
+        t = F.DistanceTable.from_host(cost)
+        with pytest.raises(F.InvalidArgument):
+            F.search_arrays(inst, t, cfg, *st)
+        with pytest.raises(F.InvalidArgument):
+            F.search_batch([inst], [st], cfg, [np.ascontiguousarray(cost.T).reshape(-1)])
+        t.upload(good.cost)  # a good table makes the context searchable again
+        assert F.search_arrays(inst, t, cfg, *st).stats.evaluations > 0
+
+
+def test_objective_km_validates_indices():
+    """fp_objective_km: unserved missions, out-of-range vehicles and unplaced
+    serving vehicles are InfeasibleError, never out-of-bounds reads."""
+    import ctypes as C
+
+    from paper_2001_05291_b200 import _abi as A
+    from paper_2001_05291_b200._native import lib
+    inst = F.survey_instance(50, 200, 10, seed=1)
+    t = F.build_distance_table(inst)
+    start = F.rank_bases(inst, t)
+    vb, mv = start.vehicle_base.copy(), start.mission_vehicle.copy()
+    out = C.c_double()
+
+    def call(vb_, mv_, V=inst.n_vehicles):
+        return lib().fp_objective_km(t._ctx.p, V, A.ptr(vb_, C.c_int32), A.ptr(mv_, C.c_int32),
+                                     C.byref(out))
+    assert call(vb, mv) == A.FP_OK
+    assert out.value == F.objective_km(start.assignment, inst, t)
+    for m_val in (-1, inst.n_vehicles, 10 ** 6):
+        bad = mv.copy()
+        bad[5] = m_val
+        assert call(vb, bad) == A.FP_ERR_INFEASIBLE
+    for b_val in (-1, inst.n_bases):
+        bvb = vb.copy()
+        bvb[mv[5]] = b_val
+        assert call(bvb, mv) == A.FP_ERR_INFEASIBLE
+    assert call(vb, mv, V=int(mv.max())) == A.FP_ERR_INFEASIBLE
+
+
 @pytest.mark.parametrize("seed,n,passes", [(7, 2, 3), (7, 200, 40), (0, 5000, 3), (123, 10000, 2),
                                            (2**64 - 1, 313, 7)])
 def test_device_permutation_stream_matches_reference(seed, n, passes):

@@ -189,3 +189,60 @@ def test_tiny_instance_optimum():
     ex = H.C.c_double(0)
     H.REF.ref_brute_force_optimal_km(H.C.byref(inst.c()), H.C.byref(ex))
     assert ex.value == got
+
+
+def test_golden_runs_parallel_table_is_the_reference_table(tmp_path):
+    """oracle/golden_runs fills c4's table on several threads with the
+    reference's per-entry mission_cost_km; it must equal the reference's
+    build_distance_table bit for bit (checked on a small shape)."""
+    import os
+    import subprocess
+
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "golden_runs"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/golden_runs not built")
+    env = dict(os.environ, GOLDEN_DUMP_TABLE="1")
+    outs = []
+    for thr in (1, 3):
+        pre = tmp_path / f"t{thr}"
+        r = subprocess.run([str(exe), "60", "700", "12", "3", "7", "2", "1", str(thr), str(pre)],
+                           capture_output=True, text=True, env=env, check=True)
+        outs.append((json.loads(r.stdout), (tmp_path / f"t{thr}.table.bin").read_bytes(),
+                     (tmp_path / f"t{thr}.mv.bin").read_bytes()))
+    assert outs[0][1] == outs[1][1]
+    assert outs[0][2] == outs[1][2]
+    assert outs[0][0]["stats"] == outs[1][0]["stats"]
+    # and equal to the reference's own table through the C wrapper
+    inst = H.ref_survey_instance(60, 700, 12, seed=3)
+    assert H.ref_table(inst).tobytes() == outs[0][1]
+
+
+def test_golden_runs_file_is_consistent():
+    """tests/golden/runs.json: every run carries the seven stats, hashes and
+    the objective bits that match its repr."""
+    import struct
+
+    runs = json.loads((GOLD / "runs.json").read_text())
+    assert {"c1_full", "c2_full", "c2_3pass", "c3_1pass", "c3_10pass"} <= set(runs)
+    assert sum(k.startswith("c5_s") for k in runs) >= 25
+    for name, r in runs.items():
+        assert len(r["stats"]) == 6 and r["stats"][2] == r["stats"][3], name
+        assert struct.pack(">d", r["final_objective_km"]).hex() == r["final_objective_bits"], name
+        assert len(r["assignment_sha256"]) == 64 and len(r["start_sha256"]) == 64, name
+    # survey §6's reference run of c2 to quiescence
+    assert runs["c2_full"]["stats"][:3] == [203, 2221690179, 13713]
+
+
+def test_adapter_check_feasible_matches_reference():
+    """integration/fleetplace_b200_adapter.cpp's O(M) check_feasible equals
+    the reference's O(M^2) one (proj/src/model.cpp:118-174) on the
+    reference helpers' fuzzed assignments plus unknown ids (host only; the
+    objective leg runs in the GPU suite)."""
+    import subprocess
+
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "adapter_check"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/adapter_check not built")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 mismatches" in r.stdout

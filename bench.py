@@ -248,6 +248,11 @@ def run_ours(args) -> None:
         "config": {**CFG, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "l2": "flushed (256 MB write) before every step"},
         "same_config": True,
+        "step_ms": {"device": float(np.mean(dev_ms)),
+                    "search_start": float(np.mean([r.stats.init_ms for r in results])),
+                    "per_pass_sweeps": float(np.mean([r.stats.sweep_ms for r in results])),
+                    "pass_kernels": float(np.mean([r.stats.pass_ms for r in results])),
+                    "pass_launches": results[0].stats.pass_launches},
         "parity": "SearchStats and final Assignment equal the reference's recorded runs "
                   "(tests/golden/runs.json: c2_3pass, c2_full)",
         "search_stats": {k: getattr(st, k) for k in ("passes", "evaluations", "applied_moves",
@@ -410,10 +415,12 @@ def sharded_rank_workload(ws: int, rank: int, local: int, reps: int = 2) -> dict
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(v, op=dist.ReduceOp.SUM)
         v[0] = mx[0]
+    sweep = sharded_sweep(ws, inst, part, table)
     del table
     torch.cuda.empty_cache()
     B, M = shape[0], shape[1]
-    return {"workload": "c4 5000 bases x 1M missions x 250 vehicles: build_distance_table + "
+    return {"sweep": sweep,
+            "workload": "c4 5000 bases x 1M missions x 250 vehicles: build_distance_table + "
                         f"rank_bases, missions sharded over {ws} GPU(s)",
             "ms": float(v[0]), "n_gpus": ws, "missions_per_gpu": -(-M // ws),
             "assigned_missions": int(v[1]), "missions": M,
@@ -421,6 +428,48 @@ def sharded_rank_workload(ws: int, rank: int, local: int, reps: int = 2) -> dict
             "totals_sha256": hashlib.sha256(part.base_totals.tobytes()).hexdigest(),
             "timing": "CUDA events around the synchronous calls, mean of 2 after 1 warm-up, "
                       "max over ranks"}
+
+
+def sharded_sweep(ws: int, inst, part, table, reps: int = 3) -> dict:
+    """SURVEY §8(d)'s roofline kernel at c4 with the missions sharded (§8(e)):
+    each rank sweeps its slice of the search start (improvement rows +
+    relocation partial sums, fp_neighbourhood_sweep) and one NCCL all-reduce
+    combines the relocation table (sharded.neighbourhood_sweep_sharded).
+    Times: the sweep kernels (library CUDA events) and the whole call incl.
+    the all-reduce (CUDA events), after one warm-up call that also makes the
+    slice's row-major copy; max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2001_05291_b200 import sharded as S
+
+    pinst = inst.mission_slice(part.lo, part.hi)
+    S.neighbourhood_sweep_sharded(pinst, table, part)  # warm-up (+ the row-major copy)
+    k_ms, w_ms = [], []
+    for _ in range(reps):
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        A_, E_, U_, sw = S.neighbourhood_sweep_sharded(pinst, table, part)
+        e1.record()
+        e1.synchronize()
+        k_ms.append(sw.sweep_ms)
+        w_ms.append(e0.elapsed_time(e1))
+    v = torch.tensor([float(np.median(k_ms)), float(np.median(w_ms))], dtype=torch.float64,
+                     device="cuda")
+    if ws > 1:
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+    B, M = inst.n_bases, inst.n_missions
+    alg = (8 * B * M + 16 * M) / ws  # per GPU
+    peak, _ = _peaks()
+    ach = alg / (float(v[0]) / 1e3) / 1e9
+    return {"workload": f"c4 neighbourhood sweep of the ranked start, missions sharded over {ws} "
+                        "GPU(s), one all-reduce of the relocation table",
+            "sweep_kernels_ms": float(v[0]), "with_allreduce_ms": float(v[1]),
+            "bytes_per_gpu": alg, "achieved_gbs_per_gpu": ach, "frac_of_measured_hbm": ach / peak,
+            "allreduce_bytes": 3 * 8 * B * inst.n_vehicles,
+            "timing": "median of 3 after a warm-up, CUDA events, max over ranks"}
 
 
 def c5_batch_workload(ws: int, rank: int, local: int, per_rank: int = 512) -> dict:

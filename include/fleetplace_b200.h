@@ -298,6 +298,33 @@ fp_status fp_search_batch(fp_ctx* ctx, int32_t n, const fp_instance* insts,
                           const fp_search_start* starts,
                           fp_search_result* outs);
 
+/* (new; SURVEY.md §8(d)'s roofline kernel, exposed for mission-sharded use,
+ * §8(e)) The neighbourhood sweep of a search start on the resident table:
+ * every relocation's quick delta to every base and every reassignment /
+ * takeover's improvement test, as the search computes them before its first
+ * pass. With a mission shard (the instance and start of one mission range,
+ * all bases and vehicles) it is the shard's PARTIAL sweep: the relocation
+ * sums of all shards add up (sharded.neighbourhood_sweep_sharded combines
+ * them with one NCCL all-reduce, widening the error bound by the additions),
+ * the improvement rows and mission costs concatenate. */
+typedef struct fp_sweep_result {
+  double* reloc_sum;        /* [n_vehicles * n_bases] entry (t, v) at v*n_bases + t:
+                               any-order sum over v's missions m of
+                               cost(m, t) - mc[m] (eval_relocate's quick delta,
+                               proj/src/search.cpp:121-127, as a real sum) */
+  double* reloc_err;        /* [..] |reloc_sum - exact real sum| <= reloc_err */
+  double* reloc_abs;        /* [..] >= sum |cost(m, t) - mc[m]| */
+  uint32_t* improve_rows;   /* [n_missions * ceil(n_vehicles / 32)]: bit g of row m
+                               = moving m to vehicle g lowers its cost
+                               (eval_reassign / eval_takeover, search.cpp:82-148) */
+  double* mission_cost;     /* [n_missions] mc[m] = cost(m, base of m's vehicle) */
+  int32_t device_ptrs;      /* 1: the outputs are device pointers on ctx's device */
+  double sweep_ms;          /* CUDA events: improvement rows + relocation sums */
+  double total_ms;          /* ... plus mission costs and the exact start total */
+} fp_sweep_result;
+fp_status fp_neighbourhood_sweep(fp_ctx* ctx, const fp_instance* inst,
+                                 const fp_search_start* start, fp_sweep_result* out);
+
 /* enumerate_moves (proj/src/search.cpp:379-397): the up-to-three proposals
  * reachable from (i, j) with their exact fixed-order deltas. Outputs kind
  * and delta arrays with room for 3 entries. */

@@ -85,3 +85,9 @@ def ptr(a: np.ndarray | None, ctype):
 
 STATS_FIELDS = ("passes", "evaluations", "applied_moves", "committed_moves",
                 "tabu_skips_outer", "tabu_skips_inner", "final_objective_km")
+
+
+class fp_sweep_result(C.Structure):
+    _fields_ = [("reloc_sum", C.c_void_p), ("reloc_err", C.c_void_p), ("reloc_abs", C.c_void_p),
+                ("improve_rows", C.c_void_p), ("mission_cost", C.c_void_p),
+                ("device_ptrs", C.c_int32), ("sweep_ms", C.c_double), ("total_ms", C.c_double)]

@@ -19,7 +19,7 @@ EXPORTS = (
     "fp_ctx_kernel_launches", "fp_ctx_last_kernel_ms", "fp_ctx_last_copy_ms", "fp_ctx_set_row_copy", "fp_validate_instance", "fp_generate_instance",
     "fp_build_distance_table", "fp_table_upload", "fp_table_download",
     "fp_column_totals", "fp_rank_bases", "fp_initial_pool", "fp_search",
-    "fp_search_batch", "fp_search_batch_configs", "fp_enumerate_moves", "fp_objective_km", "fp_haversine_batch",
+    "fp_search_batch", "fp_search_batch_configs", "fp_neighbourhood_sweep", "fp_enumerate_moves", "fp_objective_km", "fp_haversine_batch",
     "fp_permutations", "fp_column_totals_chain", "fp_rank_from_totals",
 )
 
@@ -88,6 +88,9 @@ def lib() -> C.CDLL:
                                           C.POINTER(A.fp_search_start),
                                           C.POINTER(A.fp_search_result)]
     l.fp_search_batch_configs.restype = i32
+    l.fp_neighbourhood_sweep.argtypes = [p, inst_p, C.POINTER(A.fp_search_start),
+                                         C.POINTER(A.fp_sweep_result)]
+    l.fp_neighbourhood_sweep.restype = i32
     l.fp_enumerate_moves.argtypes = [p, inst_p, C.POINTER(A.fp_search_start), i32, i32, i32p,
                                      f64p, i32p]
     l.fp_enumerate_moves.restype = i32

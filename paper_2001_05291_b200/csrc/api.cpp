@@ -536,10 +536,13 @@ struct Trace {
 
 // Shared driver for fp_search / fp_search_batch. `tables[s]` is a device
 // pointer to scenario s's table (nullptr = the scenario's arena copy).
+// sweep != nullptr (fp_neighbourhood_sweep): stop after the search start's
+// neighbourhood sweep and hand out its tables instead of searching.
 void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_config* cfgs,
                 const fp_search_start* starts, fp_search_result* outs,
                 const std::vector<const double*>& dev_tables,
-                const std::vector<const double*>& host_tables) {
+                const std::vector<const double*>& host_tables,
+                fp_sweep_result* sweep = nullptr) {
   const int M = insts[0].n_missions;
   for (int s = 1; s < n; ++s)
     if (insts[s].n_missions != M)
@@ -841,6 +844,31 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   ctx->launches += 1 + (M > 0 ? 1 : 0) + (rows_stream ? 4 : (maxB > 0 ? 1 : 0)) +
                    (transpose && M > 0 && maxB > 0 ? 1 : 0);
   tr.mark("allocated, staged, init launched");
+  if (sweep) {
+    // the sweep's results of scenario 0, then done
+    const fpk::Scenario& S = run.scs[0];
+    const int V = insts[0].n_vehicles, B = insts[0].n_bases;
+    const size_t bv = (size_t)B * V, nw = (size_t)M * S.nvw;
+    const cudaMemcpyKind k = sweep->device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    auto out = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) check(cudaMemcpyAsync(dst, src, bytes, k, st), "sweep copy");
+    };
+    out(sweep->reloc_sum, S.rA, 8 * bv);
+    out(sweep->reloc_err, S.rE, 8 * bv);
+    out(sweep->reloc_abs, S.rU, 8 * bv);
+    out(sweep->improve_rows, S.impT, 4 * nw);
+    out(sweep->mission_cost, S.mc, 8ull * M);
+    check(cudaStreamSynchronize(st), "sweep sync");
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, ei[2], ei[4]);
+    cudaEventElapsedTime(&b, ei[0], ei[4]);
+    sweep->sweep_ms = a;
+    sweep->total_ms = b;
+    for (auto& e : ei) cudaEventDestroy(e);
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return;
+  }
   std::vector<cudaEvent_t> sweep_ev;  // (start, end) pairs around grid-wide sweeps
   std::vector<cudaEvent_t> pass_ev;   // (start, end) pairs around pass-kernel launches
   std::vector<PermStream> rngs;
@@ -1520,6 +1548,22 @@ fp_status fp_search_batch(fp_ctx* ctx, int32_t n, const fp_instance* insts,
   if (!cfg) return fail(FP_ERR_INVALID_ARGUMENT, "NULL search config");
   std::vector<fp_search_config> cfgs((size_t)n, *cfg);
   return fp_search_batch_configs(ctx, n, insts, tables, 6371.0088, cfgs.data(), starts, outs);
+}
+
+fp_status fp_neighbourhood_sweep(fp_ctx* ctx, const fp_instance* inst, const fp_search_start* start,
+                                 fp_sweep_result* out) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (!inst || !start || !out) throw FpError(FP_ERR_INVALID_ARGUMENT, "NULL argument");
+    ensure_table(ctx, inst->n_missions, inst->n_bases);
+    if (!ctx->table_ok)
+      throw FpError(FP_ERR_INVALID_ARGUMENT,
+                    "the sweep needs a distance table whose entries are finite and >= 0");
+    // a local search's configuration: the sweep does not depend on it
+    const fp_search_config cfg{0, FP_MODE_LOCAL, 0, -1, 0};
+    fp_search_result r{};
+    run_search(ctx, 1, inst, &cfg, start, &r, {ctx->d_cost}, {nullptr}, out);
+  });
 }
 
 fp_status fp_enumerate_moves(fp_ctx* ctx, const fp_instance* in, const fp_search_start* state,

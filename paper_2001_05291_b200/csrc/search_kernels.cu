@@ -645,23 +645,6 @@ __device__ double exact_reloc_quick(const Scenario& s, Shared& sh, const double*
   return r;
 }
 
-// Classification of one vehicle's relocation from its (any-order) delta sum,
-// absolute sum and term count:
-// POS  quick_delta >= 0 for sure (never accepted)
-// NEG  quick_delta < 0 for sure, the total comparison is not yet settled
-// ACC  accepted for sure
-// AMB  sign of the sequential quick_delta not settled
-__device__ __forceinline__ uint8_t reloc_class(double sum, double abs, int n,
-                                               double bound_total) {
-  // all terms exactly zero (e.g. a base at the same location): the
-  // sequential sum is exactly 0.0, never < 0
-  if (n == 0 || abs == 0.0) return CLS_POS;
-  const double err = (double)(n + 1) * kTwoPowM52 * abs * 1.0001;
-  if (sum > err) return CLS_POS;
-  if (sum < -(err + bound_total)) return CLS_ACC;
-  if (sum < -err) return CLS_NEG;
-  return CLS_AMB;
-}
 
 __device__ __forceinline__ bool compat_vm(bool vehicle_fixed, bool rotary_only) {
   return !(vehicle_fixed && rotary_only);
@@ -818,35 +801,52 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
   }
   __syncthreads();
   const int n = min(sh.bi[7], cap);
-  // warp per position, lanes over vehicles: all gathers of a position are
-  // independent; bits of one position live in different words (rows), and
-  // positions sharing a word use word atomics
-  for (int k = w; k < n; k += NW) {
-    const int q = list[k];
-    const int j = sm.pb[q];
-    const double mcq = s.mcp[q];
-    const bool ro = s.rop[q];
-    const int wd = q >> 5;
-    const uint32_t bit = 1u << (q & 31);
-    for (int g0 = 0; g0 < V; g0 += 32 * 4) {
-      bool on[4];
+  // PP positions per warp at a time, lanes over vehicles: all the round's
+  // gathers (PP positions x GU groups of 32 vehicles) are independent and in
+  // flight together; bits of one position live in different words (rows),
+  // and positions sharing a word use word atomics
+  constexpr int PP = 4, GU = 2;
+  for (int k0 = w * PP; k0 < n; k0 += NW * PP) {
+    int qa[PP], ja[PP];
+    double ma[PP];
+    bool ra[PP];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int g = g0 + u * 32 + l;
-        on[u] = g < V && g != x && compat_vm(s.vfixed[g], ro) && cost_mb(s, j, s.vbase[g]) < mcq;
-      }
+    for (int a = 0; a < PP; ++a) {
+      const int k = k0 + a;
+      qa[a] = k < n ? list[k] : -1;
+    }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const unsigned row = __ballot_sync(FULL, on[u]);
-        if (l == 0 && g0 + u * 32 < V) s.impT[(long long)j * s.nvw + (g0 >> 5) + u] = row;
-      }
+    for (int a = 0; a < PP; ++a) {
+      const int q = qa[a] < 0 ? 0 : qa[a];
+      ja[a] = sm.pb[q];
+      ma[a] = s.mcp[q];
+      ra[a] = s.rop[q];
+    }
+    for (int g0 = 0; g0 < V; g0 += 32 * GU) {
+      bool on[PP][GU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int g = g0 + u * 32 + l;
-        if (g >= V || g == x) continue;
-        uint32_t* wp = s.imp + (long long)g * nwd + wd;
-        const uint32_t old = on[u] ? atomicOr(wp, bit) : atomicAnd(wp, ~bit);
-        if (((old & bit) != 0u) != on[u]) atomicAdd(&sm.impc[g], on[u] ? 1 : -1);
+      for (int a = 0; a < PP; ++a)
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const int g = g0 + u * 32 + l;
+          on[a][u] = qa[a] >= 0 && g < V && g != x && compat_vm(s.vfixed[g], ra[a]) &&
+                     cost_mb(s, ja[a], s.vbase[g]) < ma[a];
+        }
+#pragma unroll
+      for (int a = 0; a < PP; ++a) {
+        if (qa[a] < 0) continue;  // warp-uniform
+        const int wd = qa[a] >> 5;
+        const uint32_t bit = 1u << (qa[a] & 31);
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+          const unsigned row = __ballot_sync(FULL, on[a][u]);
+          if (l == 0 && g0 + u * 32 < V) s.impT[(long long)ja[a] * s.nvw + (g0 >> 5) + u] = row;
+          const int g = g0 + u * 32 + l;
+          if (g >= V || g == x) continue;
+          uint32_t* wp = s.imp + (long long)g * nwd + wd;
+          const uint32_t old = on[a][u] ? atomicOr(wp, bit) : atomicAnd(wp, ~bit);
+          if (((old & bit) != 0u) != on[a][u]) atomicAdd(&sm.impc[g], on[a][u] ? 1 : -1);
+        }
       }
     }
   }
@@ -1028,17 +1028,6 @@ __device__ void relocation_classes(const Scenario& s, Shared& sh, const Smem& sm
   }
 }
 
-// One term enters or leaves D(t, v): rA +/-= d, the bounds widened by the
-// rounding of d and of the update.
-__device__ __forceinline__ void table_patch(const Scenario& s, int t, int v, double d, bool add) {
-  const long long k = tix(s, t, v);
-  const double A = add ? s.rA[k] + d : s.rA[k] - d;
-  s.rA[k] = A;
-  s.rE[k] += 2.0 * kTwoPowM52 * (fabs(d) + fabs(A));
-  const double U = s.rU[k];
-  s.rU[k] = add ? (U + fabs(d)) * (1.0 + 2.0 * kTwoPowM52)
-                : fmax(0.0, U - fabs(d)) + 2.0 * kTwoPowM52 * U;
-}
 
 // After mission j moved from `loser` (cost mc_old, nl missions before) to
 // `gain` (cost mc_new, ng missions before): patch every empty base's row and

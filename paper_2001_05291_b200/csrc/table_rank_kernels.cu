@@ -490,93 +490,219 @@ __device__ __forceinline__ long long col_round(double x, double inv_u, bool& tie
   return (long long)f + (fr >= 0.5 ? 1 : 0);
 }
 
+// ---- shared-memory mbarriers + 1-D bulk copies (TMA engine, UBLKCP) -------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+// generic-proxy accesses of shared memory ordered before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// rn(y) of a term already scaled by 1/u (y = x / u exact), or -1 for an
+// EVENT term: a rounding tie (round-half-even then depends on the running
+// sum), a term of at least ~0.9 of the binade (it may leave it by itself),
+// or one that is negative, infinite or NaN (the integer step assumes a sum
+// that only grows); events are added with a true fp64 add.
+__device__ __forceinline__ long long chain_term_int(double y) {
+  if (!(y >= 0.0 && y < 4.0e15)) return -1;
+  const double f = floor(y);
+  const double fr = y - f;
+  if (fr == 0.5) return -1;
+  return (long long)f + (fr > 0.5 ? 1 : 0);
+}
+
 // Kernel (2), warp per column: the fixed-order fp64 column sum, bit-exact,
 // without a sequential add chain. While the running sum S stays in one
 // binade [2^e, 2^(e+1)) every partial sum is a multiple of u = 2^(e-52), so
-// fl(S + c) = S + u rn(c/u) unless c/u is an exact tie; a step of 32*UE terms
-// (lanes coalesced over consecutive missions) is an integer sum, and the
-// first step that leaves the binade or holds a tie is resolved exactly by one
-// lane scan per 32 terms and one true fp64 add (the same algorithm as the
-// search's exact_chain). HBM-bound: each entry read once.
-__global__ void __launch_bounds__(256)
+// fl(S + c) = S + u rn(c/u) unless c/u is an exact tie: the warp keeps S as
+// the integer N = S/u, and a stage of 32*UE terms (lane l holds terms
+// q*32 + l) adds the integer sum of its terms' rn(c/u); the first EVENT of a
+// stage (a term that leaves the binade, a tie, a non-distance term) is found
+// by one lane scan per 32 terms and added with one true fp64 add (the same
+// algorithm as the search's exact_chain). The column streams
+// through a ring of NS shared-memory stages per warp filled by 1-D bulk
+// copies (the TMA engine: cp.async.bulk + mbarrier complete_tx), NS-1 stages
+// in flight while the warp sums one; warps are independent (no block
+// barrier) and 2-warp blocks let ~34 warps share an SM, so c4's 5000 columns
+// are all resident at once. Each entry is read from HBM once; the bound is
+// the FP64 pipe and issue rate of ~12 instructions per term.
+template <int UE, int NS>
+__global__ void __launch_bounds__(64, 16)
     column_chain_kernel(const double* __restrict__ cost, int M, int B, const double* __restrict__ carry,
                         double* __restrict__ out) {
-  constexpr int UE = 32;
+  constexpr int STEPN = 32 * UE;  // terms per stage
   constexpr long long LIM = 1ll << 53;
   constexpr unsigned FULL = 0xffffffffu;
-  const int l = threadIdx.x & 31;
-  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (b >= B) return;
+  extern __shared__ __align__(128) unsigned char chain_smem[];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int b = blockIdx.x * nw + w;
+  if (b >= B) return;  // warps are independent: no block-wide barrier below
+  double* ring = reinterpret_cast<double*>(chain_smem) + (size_t)w * NS * STEPN;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(chain_smem + (size_t)nw * NS * STEPN * 8) + w * NS;
+  // the stream starts at the 16-byte boundary at or before the column (bulk
+  // copies need 16-byte alignment; allocations are 256-byte aligned, so the
+  // one extra leading element, when there is one, is the previous column's)
   const double* col = cost + (long long)b * M;
+  const int lead = (int)((reinterpret_cast<uintptr_t>(col) & 15) >> 3);
+  const double* src = col - lead;
+  const long long nel = (long long)M + lead;
+  const int nsteps = (int)((nel + STEPN - 1) / STEPN);
+  if (l == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    fence_proxy_async_smem();
+  }
+  __syncwarp();
+  // lane 0: stage `step` of the stream into ring slot step % NS (rounded up to
+  // 16 bytes: at most one element past the column, inside the allocation --
+  // the table buffer carries two doubles of tail padding)
+  auto issue = [&](int step) {
+    const int slot = step % NS;
+    const long long e0 = (long long)step * STEPN;
+    const long long n = min((long long)STEPN, nel - e0);
+    const uint32_t bytes = (uint32_t)(((n * 8) + 15) & ~15ll);
+    const uint32_t bar = smem_u32(&bars[slot]);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(smem_u32(ring + (size_t)slot * STEPN), src + e0, bytes, bar);
+  };
+  if (l == 0)
+    for (int st = 0; st < min(NS, nsteps); ++st) issue(st);
   // a mission shard continues the chain of the shards before it
   double S = carry ? carry[b] : 0.0;
-  int k = 0;
-  while (k < M) {
-    if (!(S >= 0x1p-900 && S < INFINITY)) {
-      // leading zeros / tiny values, or a running sum a negative or
-      // non-finite term left outside the positive normal range: plain
-      // sequential adds until it is back (never, for an infinite or NaN sum)
-      if (l == 0)
-        do S = __dadd_rn(S, col[k++]);
-        while (k < M && !(S >= 0x1p-900 && S < INFINITY));
-      S = __shfl_sync(FULL, S, 0);
-      k = __shfl_sync(FULL, k, 0);
-      continue;
+  // integer state of the binade steps: S = N * u while `inbin`
+  bool inbin = false;
+  double u = 0.0, inv_u = 0.0;
+  long long N = 0;
+  auto enter = [&]() {  // (re)derive the binade state from S
+    inbin = S >= 0x1p-900 && S < INFINITY;
+    if (inbin) {
+      const int e = ilogb(S);
+      u = ldexp(1.0, e - 52);
+      inv_u = ldexp(1.0, 52 - e);
+      N = (long long)(S * inv_u);
     }
-    const int e = ilogb(S);
-    const double u = ldexp(1.0, e - 52), inv_u = ldexp(1.0, 52 - e);
-    const long long N0 = (long long)(S * inv_u);
-    // the whole step's terms in flight before any is used
-    double xv[UE];
+  };
+  enter();
+  for (int step = 0; step < nsteps; ++step) {
+    const int slot = step % NS;
+    const uint32_t bar = smem_u32(&bars[slot]);
+    const uint32_t parity = (uint32_t)((step / NS) & 1);
+    while (!mbar_try_wait(bar, parity)) {
+    }
+    double* x = ring + (size_t)slot * STEPN;
+    const long long kb = (long long)step * STEPN - lead;  // column index of x[0]
+    const int kend = (int)min(kb + STEPN, (long long)M);
+    // entries outside the column (the leading element, the tail) become zeros
+    if (kb < 0 || kb + STEPN > M) {
 #pragma unroll
-    for (int q = 0; q < UE; ++q) {
-      const int kk = k + q * 32 + l;
-      xv[q] = kk < M ? col[kk] : 0.0;
+      for (int q = 0; q < UE; ++q) {
+        const long long kk = kb + q * 32 + l;
+        if (kk < 0 || kk >= M) x[q * 32 + l] = 0.0;
+      }
+      __syncwarp();
     }
-    long long local = 0;
-    bool any_tie = false;
+    int kcur = (int)max(kb, 0ll);
+    while (kcur < kend) {
+      if (!inbin) {
+        // leading zeros / tiny values, or a sum a negative or non-finite term
+        // left outside the positive normal range: plain sequential adds
+        if (l == 0)
+          do S = __dadd_rn(S, x[kcur++ - kb]);
+          while (kcur < kend && !(S >= 0x1p-900 && S < INFINITY));
+        S = __shfl_sync(FULL, S, 0);
+        kcur = __shfl_sync(FULL, kcur, 0);
 #pragma unroll
-    for (int q = 0; q < UE; ++q) {
-      bool tie;
-      local = min(local + col_round(xv[q], inv_u, tie), LIM);
-      any_tie |= tie;  // padding zeros never tie
-    }
-    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(FULL, local, o);
-    if (N0 + local < LIM && !__any_sync(FULL, any_tie)) {
-      S = (double)(N0 + local) * u;
-      k = min(M, k + 32 * UE);
-      continue;
-    }
-    // the first event of the step: one lane scan per 32 terms
-    long long run = N0;
-    bool found = false;
-    int ev = 0;
-    long long before = 0;
+        for (int q = 0; q < UE; ++q)
+          if (kb + q * 32 + l < kcur) x[q * 32 + l] = 0.0;  // summed: out of the fast path
+        __syncwarp();
+        enter();
+        continue;
+      }
+      // fast path: the whole rest of the stage (entries before kcur are zero)
+      long long local = 0;
+      bool ev_any = false;
 #pragma unroll
-    for (int q = 0; q < UE; ++q) {
-      if (!found) {
-        const int kk = k + q * 32 + l;
-        bool tq;
-        const long long r = col_round(xv[q], inv_u, tq);
-        long long incl = r;
-        for (int o = 1; o < 32; o <<= 1) {
-          const long long y = __shfl_up_sync(FULL, incl, o);
-          if (l >= o) incl += y;
-        }
-        const unsigned hit = __ballot_sync(FULL, kk < M && (tq || run + incl >= LIM));
-        if (hit) {
-          const int f = __ffs(hit) - 1;
-          before = run + __shfl_sync(FULL, incl - r, f);
-          ev = k + q * 32 + f;
-          found = true;
-        } else {
-          run += __shfl_sync(FULL, incl, 31);
+      for (int q = 0; q < UE; ++q) {
+        const long long r = chain_term_int(x[q * 32 + l] * inv_u);
+        ev_any |= r < 0;
+        local += r;
+      }
+      for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(FULL, local, o);
+      if (!__any_sync(FULL, ev_any) && N + local < LIM) {
+        N += local;
+        break;  // the rest of the stage is summed
+      }
+      // the first event from kcur: one lane scan per 32 terms
+      long long run = N;
+      int ev = kend;
+      long long before = 0;
+#pragma unroll
+      for (int q = 0; q < UE; ++q) {
+        if (ev == kend) {
+          const long long r0 = chain_term_int(x[q * 32 + l] * inv_u);
+          const bool evt = r0 < 0;
+          const long long r = evt ? 0 : r0;
+          long long incl = r;
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(FULL, incl, o);
+            if (l >= o) incl += y;
+          }
+          const long long kk = kb + q * 32 + l;
+          const unsigned hit = __ballot_sync(FULL, kk >= kcur && kk < kend && (evt || run + incl >= LIM));
+          if (hit) {
+            const int f = __ffs(hit) - 1;
+            before = run + __shfl_sync(FULL, incl - r, f);
+            ev = (int)(kb + q * 32 + f);
+          } else {
+            run += __shfl_sync(FULL, incl, 31);
+          }
         }
       }
+      if (ev == kend) {  // (cannot happen: the fast path saw an event or a crossing)
+        N = run;
+        break;
+      }
+      // exact sum before the event, then its true fp64 add; the processed
+      // entries of the stage become zeros for the next fast-path attempt
+      S = __dadd_rn((double)before * u, x[ev - kb]);
+#pragma unroll
+      for (int q = 0; q < UE; ++q)
+        if (kb + q * 32 + l <= ev) x[q * 32 + l] = 0.0;
+      __syncwarp();
+      kcur = ev + 1;
+      enter();
     }
-    S = __dadd_rn((double)before * u, col[ev]);
-    k = ev + 1;
+    __syncwarp();  // every lane is done with this slot
+    if (l == 0 && step + NS < nsteps) {
+      fence_proxy_async_smem();
+      issue(step + NS);
+    }
   }
+  if (inbin) S = (double)N * u;
   if (l == 0) out[b] = S;
 }
 
@@ -635,7 +761,16 @@ cudaError_t launch_table_check(const double* t, size_t n, int* bad, cudaStream_t
 cudaError_t launch_column_totals_chain(const double* cost, int M, int B, const double* carry,
                                        double* out, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  column_chain_kernel<<<(B + 7) / 8, 256, 0, st>>>(cost, M, B, carry, out);
+  // two-warp blocks of 12.3 KB: up to 17 per SM (34 warps, one per column)
+  constexpr int UE = 8, NS = 3, WPB = 2;
+  const size_t smem = (size_t)WPB * NS * (32 * UE * 8 + 8);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(column_chain_kernel<UE, NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    attr = true;
+  }
+  column_chain_kernel<UE, NS><<<(B + WPB - 1) / WPB, 32 * WPB, smem, st>>>(cost, M, B, carry, out);
   return cudaGetLastError();
 }
 

@@ -617,6 +617,43 @@ def search_arrays(inst: Instance, t: DistanceTable, cfg: SearchConfig, vehicle_b
     return SearchResult(vb, mv, _stats(res), int(res.kernel_launches))
 
 
+@dataclass
+class Sweep:
+    """The neighbourhood sweep of a search start (fp_neighbourhood_sweep):
+    reloc_* are (V, B) -- entry [v, t] is vehicle v relocating to base t --
+    improve_rows (M, ceil(V/32)) bit words, mission_cost (M,)."""
+    reloc_sum: np.ndarray
+    reloc_err: np.ndarray
+    reloc_abs: np.ndarray
+    improve_rows: np.ndarray
+    mission_cost: np.ndarray
+    sweep_ms: float = 0.0
+    total_ms: float = 0.0
+
+
+def neighbourhood_sweep(inst: Instance, t: DistanceTable, vehicle_base, mission_vehicle,
+                        pool_kind=None, pool_index=None) -> Sweep:
+    """Every relocation's quick delta and every reassignment's improvement
+    test of a start on the device (SURVEY.md §8(d)'s sweep; on a mission
+    shard: that shard's partial sweep)."""
+    V, B, M = inst.n_vehicles, inst.n_bases, inst.n_missions
+    vb = np.ascontiguousarray(vehicle_base, np.int32)
+    mv = np.ascontiguousarray(mission_vehicle, np.int32)
+    pk = np.ascontiguousarray(pool_kind if pool_kind is not None else [], np.int32)
+    px = np.ascontiguousarray(pool_index if pool_index is not None else [], np.int32)
+    st = A.fp_search_start(A.ptr(vb, C.c_int32), A.ptr(mv, C.c_int32), len(pk),
+                           A.ptr(pk, C.c_int32), A.ptr(px, C.c_int32))
+    nvw = (V + 31) // 32
+    out = Sweep(np.empty((V, B)), np.empty((V, B)), np.empty((V, B)),
+                np.empty((M, nvw), np.uint32), np.empty(M))
+    r = A.fp_sweep_result(out.reloc_sum.ctypes.data, out.reloc_err.ctypes.data,
+                          out.reloc_abs.ctypes.data, out.improve_rows.ctypes.data,
+                          out.mission_cost.ctypes.data, 0, 0.0, 0.0)
+    _check(lib().fp_neighbourhood_sweep(t._ctx.p, C.byref(inst.c()), C.byref(st), C.byref(r)))
+    out.sweep_ms, out.total_ms = float(r.sweep_ms), float(r.total_ms)
+    return out
+
+
 def _run_search(start: RankedStart, inst: Instance, t: DistanceTable, cfg: SearchConfig,
                 stats: Optional[SearchStats]) -> Assignment:
     if cfg.mode == SearchMode.Tabu:

@@ -15,6 +15,15 @@ sums ARE the reference's totals; one broadcast gives them to every rank, each
 rank ranks the bases identically (host logic on B totals) and resolves its
 own missions' argmin over the chosen bases (proj/src/rank.cpp:92-116) on its
 slice. Together the shards' RankedStarts equal the unsharded one bit for bit.
+
+The neighbourhood sweep of the search start (SURVEY.md §8(d)'s roofline
+kernel) shards the same way: each rank sweeps its missions
+(`fp_neighbourhood_sweep` on its slice) and ONE all-reduce (sum; NCCL over
+NVLink) adds the relocation partial sums of every (base, vehicle) pair --
+they are sums over missions, so the shards' parts add up; the error bound
+is widened by the all-reduce's own additions, so the relocation classes
+stay rigorous. The improvement rows and mission costs are per mission and
+stay with their rank.
 """
 from __future__ import annotations
 
@@ -162,3 +171,39 @@ def gather_start(inst: F.Instance, part: ShardStart, group=None) -> Optional[F.R
     return F.RankedStart(F._assignment_from_index(inst, part.vehicle_base, mv),
                          [int(inst.base_id[b]) for b in part.unused_index], part.base_totals,
                          part.vehicle_base, mv, part.unused_index)
+
+
+U53 = 2.0 ** -53
+
+
+def combine_bounds(world: int, sum_err, sum_abs):
+    """Rigorous error / magnitude bounds of an all-reduced relocation table.
+    Rank g holds A_g with |A_g - X_g| <= E_g and U_g >= sum |terms|; the
+    all-reduce returns fl(sum A_g) (any association), so
+    |fl(sum A_g) - sum X_g| <= sum E_g + (W-1) u sum |A_g|, |A_g| <= U_g + E_g
+    (u = 2^-53); the sums of E and U are themselves rounded, hence the
+    (1 + 2W 2^-52) inflation. Returns (err, abs)."""
+    infl = 1.0 + 2.0 * world * 2.0 ** -52
+    err = (sum_err + (world - 1) * U53 * (sum_abs + sum_err)) * infl
+    return err, sum_abs * infl
+
+
+def neighbourhood_sweep_sharded(part_inst: F.Instance, table: F.DistanceTable, part: ShardStart,
+                                *, group=None, device=None):
+    """This rank's partial sweep (its mission slice) plus one all-reduce of the
+    relocation sums: returns (reloc_sum, reloc_err, reloc_abs) of the WHOLE
+    instance on every rank (tensors on `device`, default the table's GPU
+    under NCCL, the CPU under gloo) and this rank's F.Sweep (its missions'
+    improvement rows and costs)."""
+    import torch
+    import torch.distributed as dist
+
+    sw = F.neighbourhood_sweep(part_inst, table, part.vehicle_base, part.mission_vehicle)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    nccl = dist.is_initialized() and dist.get_backend(group) == "nccl"
+    dev = torch.device(device or (f"cuda:{table._ctx.device}" if nccl else "cpu"))
+    buf = torch.from_numpy(np.stack([sw.reloc_sum, sw.reloc_err, sw.reloc_abs])).to(dev)
+    if world > 1:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    err, ab = combine_bounds(world, buf[1], buf[2])
+    return buf[0], err, ab, sw

@@ -103,3 +103,60 @@ def test_chained_totals_equal_reference_rank_totals():
 def test_single_process_no_exchange():
     T = _wide_table(200, 9)
     assert chained_totals(9, _np_chain(T), batches=4).numpy().tobytes() == _seq_totals(T).tobytes()
+
+
+# ---- the neighbourhood sweep's all-reduce (sharded.combine_bounds) -----------
+
+def _sweep_worker(rank, world, port, parts, q):
+    """Each rank all-reduces its partial (sum, err, abs) like
+    neighbourhood_sweep_sharded does and applies combine_bounds."""
+    import torch.distributed as dist
+
+    from paper_2001_05291_b200.sharded import combine_bounds
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    buf = torch.from_numpy(np.stack(parts[rank]).copy())
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+    err, ab = combine_bounds(world, buf[1], buf[2])
+    q.put((rank, buf[0].numpy().copy(), err.numpy().copy(), ab.numpy().copy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sweep_allreduce_bounds_are_rigorous(world):
+    """Partial relocation sums of mission shards, all-reduced over gloo: every
+    rank gets the same table, and |combined - exact| <= combined error bound,
+    with the exact real sum of all terms computed in rationals."""
+    from fractions import Fraction
+    rng = np.random.default_rng(world)
+    n_terms, cells = 600, 24
+    # signed terms (cost(m, t) - mc[m]) of every (base, vehicle) cell, spread
+    # over binades so rounding matters
+    terms = rng.choice([-1.0, 1.0], size=(n_terms, cells)) * np.exp(rng.uniform(-8, 9, (n_terms, cells)))
+    parts = []
+    for g in range(world):
+        rg = shard(n_terms, g, world)
+        T = terms[rg.start:rg.stop]
+        a = np.zeros(cells)
+        for row in T:          # an any-order device sum stands in: sequential here
+            a = a + row
+        ab = np.abs(T).sum(axis=0) * (1 + 2 * len(T) * 2.0 ** -52)
+        err = (len(T) + 2) * 2.0 ** -52 * ab  # the per-shard bound the sweep reports
+        parts.append((a, err, ab))
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_sweep_worker, args=(r, world, port, parts, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+    res.sort(key=lambda r: r[0])
+    for r in res[1:]:
+        assert np.array_equal(r[1], res[0][1]) and np.array_equal(r[2], res[0][2])
+    _, A, E, U = res[0]
+    for c in range(cells):
+        exact = sum(Fraction(float(x)) for x in terms[:, c])
+        assert abs(Fraction(float(A[c])) - exact) <= Fraction(float(E[c])), c
+        assert Fraction(float(U[c])) >= sum(abs(Fraction(float(x))) for x in terms[:, c])

@@ -145,3 +145,44 @@ def test_rank_bases_sharded_three_processes():
     assert np.array_equal(vb, rs.vehicle_base)
     assert np.array_equal(mv, rs.mission_vehicle)
     assert np.array_equal(un, rs.unused_index)
+
+
+@pytest.mark.parametrize("shape,shards", [((500, 10000, 40), 3), ((300, 40000, 60), 8)])
+def test_sharded_neighbourhood_sweep_equals_full(shape, shards):
+    """the neighbourhood sweep of mission shards, combined (the
+    all-reduce's sum, here on the host; combine_bounds for the error), equals
+    the whole instance's sweep: improvement rows and mission costs bit for
+    bit (concatenated), relocation sums within both rigorous bounds, and the
+    relocation classes the search derives never contradict."""
+    from paper_2001_05291_b200.dist import shard
+    from paper_2001_05291_b200.sharded import combine_bounds
+    inst = F.survey_instance(*shape, seed=3)
+    t = F.build_distance_table(inst)
+    start = F.rank_bases(inst, t)
+    full = F.neighbourhood_sweep(inst, t, start.vehicle_base, start.mission_vehicle)
+    sums, errs, abss, rows, costs = [], [], [], [], []
+    for g in range(shards):
+        rg = shard(inst.n_missions, g, shards)
+        part = inst.mission_slice(rg.start, rg.stop)
+        tp = F.build_distance_table(part, row_copy=True)
+        sw = F.neighbourhood_sweep(part, tp, start.vehicle_base, start.mission_vehicle[rg.start:rg.stop])
+        sums.append(sw.reloc_sum)
+        errs.append(sw.reloc_err)
+        abss.append(sw.reloc_abs)
+        rows.append(sw.improve_rows)
+        costs.append(sw.mission_cost)
+        del tp
+    assert np.array_equal(np.concatenate(rows), full.improve_rows)
+    assert np.array_equal(np.concatenate(costs), full.mission_cost)
+    A = np.sum(sums, axis=0)
+    E, U = combine_bounds(shards, np.sum(errs, axis=0), np.sum(abss, axis=0))
+    occupied = np.zeros(inst.n_bases, bool)
+    occupied[start.vehicle_base[start.vehicle_base >= 0]] = True
+    empty = ~occupied
+    d = np.abs(A - full.reloc_sum)[:, empty]
+    assert (d <= (E + full.reloc_err)[:, empty]).all()
+    # classes: certainly >= 0 in one view is never certainly < 0 in the other
+    pos_sharded = (A - E > 0)[:, empty]
+    neg_full = (full.reloc_sum + full.reloc_err < 0)[:, empty]
+    assert not (pos_sharded & neg_full).any()
+    assert (U[:, empty] >= np.abs(full.reloc_sum[:, empty]) - full.reloc_err[:, empty]).all()

@@ -1,0 +1,20 @@
+"""Kernel (2) column totals at c4 and c3: device time (CUDA events inside the
+library) of fp_column_totals on the resident table, repeated."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2001_05291_b200 import fleetplace as F  # noqa: E402
+
+for shape in ((2000, 100000, 100), (5000, 1000000, 250)):
+    inst = F.survey_instance(*shape, seed=1)
+    t = F.build_distance_table(inst, row_copy=False)
+    ms = []
+    for _ in range(5):
+        tot = F.column_totals(t)
+        ms.append(t._ctx.last_kernel_ms())
+    B, M = shape[0], shape[1]
+    best = min(ms)
+    print(f"{shape}: column_totals {['%.3f' % x for x in ms]} ms; best {best:.3f} ms = "
+          f"{8 * B * M / best / 1e6:.1f} GB/s", flush=True)
+    del t

@@ -837,11 +837,12 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // made in-stream (no eager copy, or its allocation failed) is ordered already
   if (cost_t && ctx_copy && ctx->costT_valid && ctx->costT_ready)
     check(cudaStreamWaitEvent(st, ctx->costT_ready, 0), "wait");
-  check(fpk::launch_init(d_scs, run.scs.data(), n, M, maxB, maxV, transpose, st, ei),
+  // (a sweep alone does not need the exact start total)
+  check(fpk::launch_init(d_scs, run.scs.data(), n, M, maxB, maxV, transpose, st, ei, !sweep),
         "init_kernel");
   if (ctx_copy && cost_t) ctx->costT_valid = true;
   const bool rows_stream = n == 1 && cost_t && M > 0 && maxB > 0 && maxV > 0;
-  ctx->launches += 1 + (M > 0 ? 1 : 0) + (rows_stream ? 4 : (maxB > 0 ? 1 : 0)) +
+  ctx->launches += 1 + (M > 0 ? 2 : 0) + (rows_stream ? 4 : (maxB > 0 ? 1 : 0)) +
                    (transpose && M > 0 && maxB > 0 ? 1 : 0);
   tr.mark("allocated, staged, init launched");
   if (sweep) {
@@ -912,7 +913,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   if (const char* e = std::getenv("FLEETPLACE_HELPERS")) helpers = std::atoi(e);
   // the 1024-thread variant (a FLEETPLACE_THREADS experiment knob) is not
   // validated with helper blocks: c3 with both faulted (illegal instruction)
-  if (threads >= 1024) helpers = 0;
+  if (threads >= 1024 && !std::getenv("FLEETPLACE_ALLOW_1024_HELPERS")) helpers = 0;
   unsigned epoch = 0;
   int n_active = n;
   while (n_active > 0) {

@@ -51,7 +51,8 @@ cudaError_t launch_candidate_delta(const double* cost, int M, const int32_t* vb,
                                    int kind, int j, int newcol, int mover, double* out,
                                    cudaStream_t st);
 cudaError_t launch_init(Scenario* d_scs, const Scenario* h_scs, int n_scn, int M, int maxB,
-                        int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev);
+                        int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev,
+                        bool exact_total = true);
 cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream);
 cudaError_t launch_sweep(Scenario* d_scs, const int32_t* d_active, int n_scn,
                          const int32_t* d_perms, int M, cudaStream_t stream);

@@ -31,6 +31,7 @@
 // vehicle ids exactly like the reference's std::map<TabuKey, Entry>. The
 // per-vehicle / per-key state lives in shared memory for the whole pass.
 
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
@@ -2448,14 +2449,19 @@ cudaError_t launch_transpose(const double* src, int M, int B, double* dst, cudaS
   return cudaGetLastError();
 }
 
-// Search start: per-mission costs and the exact initial fixed-order total
-// (SearchState::from, proj/src/search.cpp:41-48), one block per scenario.
+// Search start, part 1: per-mission costs (SearchState::from,
+// proj/src/search.cpp:41-48), grid-wide (blockIdx.y = scenario).
+__global__ void __launch_bounds__(256) mission_cost_kernel(Scenario* scs) {
+  const Scenario& s = scs[blockIdx.y];
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < s.M; m += gridDim.x * blockDim.x)
+    s.mc[m] = cost_at(s, s.vbase[s.mv[m]], m);
+}
+
+// Search start, part 2: the exact initial fixed-order total, one block per
+// scenario (the block-parallel integer-binade chain).
 __global__ void __launch_bounds__(512) init_kernel(Scenario* scs) {
   const Scenario s = scs[blockIdx.x];
   __shared__ Shared sh;
-  for (int m = threadIdx.x; m < s.M; m += blockDim.x)
-    s.mc[m] = cost_at(s, s.vbase[s.mv[m]], m);
-  __syncthreads();
   const double t = exact_chain<512>(s, sh, 0, -1, 0.0, -1, nullptr);
   if (threadIdx.x == 0) {
     s.ctr->total_up = t;
@@ -2732,12 +2738,15 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
 
 // ev[0..4]: events recorded around the four stages (may be null).
 cudaError_t launch_init(Scenario* d_scs, const Scenario* h_scs, int n_scn, int M, int maxB,
-                        int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev) {
+                        int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev,
+                        bool exact_total) {
   if (ev) cudaEventRecord(ev[0], stream);
   if (transpose && M > 0 && maxB > 0)
     transpose_kernel<<<dim3((M + 63) / 64, (maxB + 31) / 32, n_scn), 256, 0, stream>>>(d_scs);
   if (ev) cudaEventRecord(ev[1], stream);
-  init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
+  if (M > 0)
+    mission_cost_kernel<<<dim3(std::min((M + 255) / 256, 4 * 148), n_scn), 256, 0, stream>>>(d_scs);
+  if (exact_total) init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
   if (ev) cudaEventRecord(ev[2], stream);
   if (M > 0) impt_init_kernel<<<dim3((M + 255) / 256, n_scn), 256, 0, stream>>>(d_scs);
   if (ev) cudaEventRecord(ev[3], stream);

@@ -632,11 +632,14 @@ class Sweep:
 
 
 def neighbourhood_sweep(inst: Instance, t: DistanceTable, vehicle_base, mission_vehicle,
-                        pool_kind=None, pool_index=None) -> Sweep:
+                        pool_kind=None, pool_index=None, device_out=None) -> Sweep:
     """Every relocation's quick delta and every reassignment's improvement
     test of a start on the device (SURVEY.md §8(d)'s sweep; on a mission
-    shard: that shard's partial sweep)."""
+    shard: that shard's partial sweep). `device_out`: a torch.device -- the
+    results stay there as CUDA tensors (reloc (3, V, B): sum, err, abs)."""
     V, B, M = inst.n_vehicles, inst.n_bases, inst.n_missions
+    if device_out is not None:
+        return _sweep_to_device(inst, t, vehicle_base, mission_vehicle, device_out)
     vb = np.ascontiguousarray(vehicle_base, np.int32)
     mv = np.ascontiguousarray(mission_vehicle, np.int32)
     pk = np.ascontiguousarray(pool_kind if pool_kind is not None else [], np.int32)
@@ -652,6 +655,25 @@ def neighbourhood_sweep(inst: Instance, t: DistanceTable, vehicle_base, mission_
     _check(lib().fp_neighbourhood_sweep(t._ctx.p, C.byref(inst.c()), C.byref(st), C.byref(r)))
     out.sweep_ms, out.total_ms = float(r.sweep_ms), float(r.total_ms)
     return out
+
+
+def _sweep_to_device(inst, t, vehicle_base, mission_vehicle, dev) -> Sweep:
+    import torch
+    V, B, M = inst.n_vehicles, inst.n_bases, inst.n_missions
+    vb = np.ascontiguousarray(vehicle_base, np.int32)
+    mv = np.ascontiguousarray(mission_vehicle, np.int32)
+    pk = np.empty(0, np.int32)
+    st = A.fp_search_start(A.ptr(vb, C.c_int32), A.ptr(mv, C.c_int32), 0, A.ptr(pk, C.c_int32),
+                           A.ptr(pk, C.c_int32))
+    nvw = (V + 31) // 32
+    reloc = torch.empty((3, V, B), dtype=torch.float64, device=dev)
+    rows = torch.empty((M, nvw), dtype=torch.int32, device=dev)
+    mc = torch.empty(M, dtype=torch.float64, device=dev)
+    torch.cuda.current_stream(dev).synchronize()
+    r = A.fp_sweep_result(reloc[0].data_ptr(), reloc[1].data_ptr(), reloc[2].data_ptr(),
+                          rows.data_ptr(), mc.data_ptr(), 1, 0.0, 0.0)
+    _check(lib().fp_neighbourhood_sweep(t._ctx.p, C.byref(inst.c()), C.byref(st), C.byref(r)))
+    return Sweep(reloc, None, None, rows, mc, float(r.sweep_ms), float(r.total_ms))
 
 
 def _run_search(start: RankedStart, inst: Instance, t: DistanceTable, cfg: SearchConfig,

@@ -198,11 +198,17 @@ def neighbourhood_sweep_sharded(part_inst: F.Instance, table: F.DistanceTable, p
     import torch
     import torch.distributed as dist
 
-    sw = F.neighbourhood_sweep(part_inst, table, part.vehicle_base, part.mission_vehicle)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    nccl = dist.is_initialized() and dist.get_backend(group) == "nccl"
-    dev = torch.device(device or (f"cuda:{table._ctx.device}" if nccl else "cpu"))
-    buf = torch.from_numpy(np.stack([sw.reloc_sum, sw.reloc_err, sw.reloc_abs])).to(dev)
+    gloo = dist.is_initialized() and dist.get_backend(group) != "nccl"
+    dev = torch.device(device or ("cpu" if gloo else f"cuda:{table._ctx.device}"))
+    if dev.type == "cuda":
+        # partials written straight into the all-reduce buffer on the GPU
+        sw = F.neighbourhood_sweep(part_inst, table, part.vehicle_base, part.mission_vehicle,
+                                   device_out=dev)
+        buf = sw.reloc_sum
+    else:
+        sw = F.neighbourhood_sweep(part_inst, table, part.vehicle_base, part.mission_vehicle)
+        buf = torch.from_numpy(np.stack([sw.reloc_sum, sw.reloc_err, sw.reloc_abs]))
     if world > 1:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     err, ab = combine_bounds(world, buf[1], buf[2])

@@ -186,3 +186,20 @@ def test_sharded_neighbourhood_sweep_equals_full(shape, shards):
     neg_full = (full.reloc_sum + full.reloc_err < 0)[:, empty]
     assert not (pos_sharded & neg_full).any()
     assert (U[:, empty] >= np.abs(full.reloc_sum[:, empty]) - full.reloc_err[:, empty]).all()
+
+
+def test_sharded_sweep_device_path_one_rank():
+    """neighbourhood_sweep_sharded with one rank (no process group): the
+    relocation table stays on the GPU (device pointers through the C ABI)
+    and agrees with the host-buffer sweep within both rigorous bounds (the
+    relocation sums are any-order fp64 atomics: not bit-reproducible); the
+    improvement rows and mission costs are bit-identical."""
+    inst = F.survey_instance(200, 5000, 20, seed=4)
+    part, table = S.rank_bases_sharded(inst)
+    A_, E_, U_, sw = S.neighbourhood_sweep_sharded(inst, table, part)
+    host = F.neighbourhood_sweep(inst, table, part.vehicle_base, part.mission_vehicle)
+    assert A_.is_cuda
+    d = np.abs(A_.cpu().numpy() - host.reloc_sum)
+    assert (d <= E_.cpu().numpy() + host.reloc_err).all()
+    assert np.array_equal(sw.improve_rows.cpu().numpy().view(np.uint32), host.improve_rows)
+    assert np.array_equal(sw.mission_cost.cpu().numpy(), host.mission_cost)

@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
-cd oracle/_ref && timeout 300 ./acceptance_b200 > ../../gpurun_out/acc_b200.log 2>&1; echo acc_rc=$?; cd ../..
-tail -5 gpurun_out/acc_b200.log
-timeout 900 python -m pytest -m gpu -q -rf tests/test_kernels_gpu.py tests/test_golden_runs_gpu.py tests/test_parity_gpu.py tests/test_sharded_gpu.py > gpurun_out/pytest_part.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_part.log
-timeout 600 python tools/chain_probe.py > gpurun_out/chain_probe.log 2>&1; echo chain_rc=$?; cat gpurun_out/chain_probe.log
+timeout 600 python -m pytest -m gpu -q -rf tests/test_sharded_gpu.py tests/test_golden_runs_gpu.py > gpurun_out/pytest_part.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_part.log
+# plain run of the 1024-thread helper case first (does it fault?)
+FLEETPLACE_THREADS=1024 FLEETPLACE_HELPERS=-1 FLEETPLACE_ALLOW_1024_HELPERS=1 timeout 300 python tools/sanitize_case.py h40k > gpurun_out/h40k_1024.log 2>&1; echo h40k_1024_rc=$?; tail -3 gpurun_out/h40k_1024.log
+FLEETPLACE_THREADS=1024 FLEETPLACE_HELPERS=-1 FLEETPLACE_ALLOW_1024_HELPERS=1 timeout 300 python tools/sanitize_case.py c2 > gpurun_out/c2_1024.log 2>&1; echo c2_1024_rc=$?; tail -3 gpurun_out/c2_1024.log
+bash tools/sanitize.sh

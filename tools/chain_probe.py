@@ -6,7 +6,8 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2001_05291_b200 import fleetplace as F  # noqa: E402
 
-for shape in ((2000, 100000, 100), (5000, 1000000, 250)):
+SHAPES = {"c3": (2000, 100000, 100), "c4": (5000, 1000000, 250)}
+for shape in [SHAPES[a] for a in (sys.argv[1:] or ["c3", "c4"])]:
     inst = F.survey_instance(*shape, seed=1)
     t = F.build_distance_table(inst, row_copy=False)
     ms = []

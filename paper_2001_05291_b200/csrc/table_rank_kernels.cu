@@ -87,6 +87,38 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- shared-memory mbarriers + 1-D bulk copies (TMA engine, UBLKCP) -------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+// generic-proxy accesses of shared memory ordered before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---- kernel (1) over distinct points ---------------------------------------
 // mission_cost_km(b, m) = hav(b, pickup_m) + hav(b, delivery_m) depends on the
 // point coordinates only, and generated missions draw both ends from S health
@@ -490,38 +522,6 @@ __device__ __forceinline__ long long col_round(double x, double inv_u, bool& tie
   return (long long)f + (fr >= 0.5 ? 1 : 0);
 }
 
-// ---- shared-memory mbarriers + 1-D bulk copies (TMA engine, UBLKCP) -------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-// generic-proxy accesses of shared memory ordered before later async-proxy ones
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
 // rn(y) of a term already scaled by 1/u (y = x / u exact), or -1 for an
 // EVENT term: a rounding tie (round-half-even then depends on the running
 // sum), a term of at least ~0.9 of the binade (it may leave it by itself),
@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(64, 16)
     const int kend = (int)min(kb + STEPN, (long long)M);
     // entries outside the column (the leading element, the tail) become zeros
     if (kb < 0 || kb + STEPN > M) {
-#pragma unroll
+#pragma unroll 1
       for (int q = 0; q < UE; ++q) {
         const long long kk = kb + q * 32 + l;
         if (kk < 0 || kk >= M) x[q * 32 + l] = 0.0;
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(64, 16)
           while (kcur < kend && !(S >= 0x1p-900 && S < INFINITY));
         S = __shfl_sync(FULL, S, 0);
         kcur = __shfl_sync(FULL, kcur, 0);
-#pragma unroll
+#pragma unroll 1
         for (int q = 0; q < UE; ++q)
           if (kb + q * 32 + l < kcur) x[q * 32 + l] = 0.0;  // summed: out of the fast path
         __syncwarp();
@@ -656,11 +656,11 @@ __global__ void __launch_bounds__(64, 16)
         N += local;
         break;  // the rest of the stage is summed
       }
-      // the first event from kcur: one lane scan per 32 terms
+      // the first event from kcur: one lane scan per 32 terms (rare path)
       long long run = N;
       int ev = kend;
       long long before = 0;
-#pragma unroll
+#pragma unroll 1
       for (int q = 0; q < UE; ++q) {
         if (ev == kend) {
           const long long r0 = chain_term_int(x[q * 32 + l] * inv_u);
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(64, 16)
       // exact sum before the event, then its true fp64 add; the processed
       // entries of the stage become zeros for the next fast-path attempt
       S = __dadd_rn((double)before * u, x[ev - kb]);
-#pragma unroll
+#pragma unroll 1
       for (int q = 0; q < UE; ++q)
         if (kb + q * 32 + l <= ev) x[q * 32 + l] = 0.0;
       __syncwarp();
@@ -761,16 +761,26 @@ cudaError_t launch_table_check(const double* t, size_t n, int* bad, cudaStream_t
 cudaError_t launch_column_totals_chain(const double* cost, int M, int B, const double* carry,
                                        double* out, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  // two-warp blocks of 12.3 KB: up to 17 per SM (34 warps, one per column)
-  constexpr int UE = 8, NS = 3, WPB = 2;
-  const size_t smem = (size_t)WPB * NS * (32 * UE * 8 + 8);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(column_chain_kernel<UE, NS>, cudaFuncAttributePreferredSharedMemoryCarveout,
+  // two-warp blocks of ~12 KB: up to 17 per SM (34 warps, one per column,
+  // so c4's 5000 columns are resident at once). FLEETPLACE_CHAIN_CFG picks
+  // another (terms per lane per stage, stages) variant for probes.
+  int cfg = 0;
+  if (const char* e = std::getenv("FLEETPLACE_CHAIN_CFG")) cfg = std::atoi(e);
+  auto go = [&](auto kern, int ue, int ns) {
+    constexpr int WPB = 2;
+    const size_t smem = (size_t)WPB * ns * (32 * ue * 8 + 8);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                          cudaSharedmemCarveoutMaxShared);
-    attr = true;
-  }
-  column_chain_kernel<UE, NS><<<(B + WPB - 1) / WPB, 32 * WPB, smem, st>>>(cost, M, B, carry, out);
+    kern<<<(B + WPB - 1) / WPB, 32 * WPB, smem, st>>>(cost, M, B, carry, out);
+  };
+  // measured (tools/chain_probe.py): c4 (5000 columns) 6.85 ms with 24-term
+  // lanes (89% of HBM), c3 (2000 columns) 0.47 ms with 12-term lanes
+  if (cfg == 0) cfg = B >= 4000 ? 3 : 2;
+  if (cfg == 1) go(column_chain_kernel<8, 3>, 8, 3);
+  else if (cfg == 2) go(column_chain_kernel<12, 2>, 12, 2);
+  else if (cfg == 3) go(column_chain_kernel<24, 2>, 24, 2);
+  else if (cfg == 4) go(column_chain_kernel<32, 2>, 32, 2);
+  else go(column_chain_kernel<16, 2>, 16, 2);
   return cudaGetLastError();
 }
 

@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-python tools/chain_probe.py c3 > gpurun_out/plain_chain.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:column_chain -s 1 -c 1 -o gpurun_out/r2_column_chain python tools/chain_probe.py c3 > gpurun_out/ncu_chain.log 2>&1; echo ncu_rc=$?
+timeout 600 python tools/table_probe.py > gpurun_out/table_probe.log 2>&1; echo table_rc=$?; cat gpurun_out/table_probe.log
+CHAIN_CFGS=0 timeout 600 python tools/chain_probe.py > gpurun_out/chain_probe.log 2>&1; echo chain_rc=$?; cat gpurun_out/chain_probe.log
+timeout 900 python -m pytest -m gpu -q -rf tests/test_kernels_gpu.py tests/test_sharded_gpu.py tests/test_golden_runs_gpu.py > gpurun_out/pytest_part.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_part.log

@@ -611,9 +611,11 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // In-kernel chunks hold up to 1024 passes (64 MB of permutations); a
   // single scenario's chunks grow 32, 64, ... so a short search generates
   // few permutations.
-  // (several permutation streams: their chunks share a budget of up to 24x
+  // (several permutation streams: their chunks share a budget of up to 16x
   // one stream's, permutations and device draws together)
-  const long long budget = ((inkernel ? 64ll : 16ll) << 20) * std::min(D, 24);
+  // (one stream: 1024 passes of c5's 5k missions, ~123 MB, so a batch runs in
+  // one launch and no scenario waits at a chunk boundary)
+  const long long budget = ((inkernel ? 192ll : 16ll) << 20) * std::min(D, 16);
   const long long per_pass = (inkernel ? 24ll : 8ll) * std::max(M, 1) * D;
   int kmax = (int)std::max<long long>(1, std::min<long long>(inkernel ? 1024 : 16, budget / per_pass));
   if (const char* e = std::getenv("FLEETPLACE_KPASSES")) kmax = std::max(1, std::atoi(e));

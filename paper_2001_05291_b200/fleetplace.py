@@ -582,6 +582,33 @@ class SearchResult:
     kernel_launches: int
 
 
+def _fields(arr, ctype, n, nested=None):
+    """Column views (numpy, no copies) of the scalar / pointer fields of a
+    ctypes struct array; `nested`: the fields of that struct member."""
+    base = C.addressof(arr)
+    size = C.sizeof(ctype)
+    off0 = 0
+    if nested is not None:
+        off0 = getattr(ctype, nested).offset
+        ctype = dict(ctype._fields_)[nested]
+    buf = (C.c_char * (size * n)).from_address(base)
+    out = {}
+    for name, t in ctype._fields_:
+        if t in (C.c_double,):
+            dt = np.float64
+        elif t in (C.c_int32,):
+            dt = np.int32
+        elif t in (C.c_uint64,):
+            dt = np.uint64
+        elif issubclass(t, C._Pointer) or t is C.c_void_p:
+            dt = np.uint64
+        else:
+            continue
+        out[name] = np.ndarray((n,), dt, buffer=buf, offset=off0 + getattr(ctype, name).offset,
+                               strides=(size,))
+    return out
+
+
 def _cfg_c(cfg: SearchConfig) -> A.fp_search_config:
     return A.fp_search_config(int(cfg.seed) & 0xFFFFFFFFFFFFFFFF, int(cfg.mode), int(cfg.tabu_tenure),
                               -1 if cfg.max_passes is None else int(cfg.max_passes),
@@ -883,33 +910,53 @@ def search_batch(insts: Sequence[Instance], starts: Sequence[tuple], cfg,
     scenario."""
     n = len(insts)
     ctx = ctx if ctx is not None else _Ctx(device)
-    ci = (A.fp_instance * n)(*[x.c() for x in insts])
-    keep = []
-    tp = (C.POINTER(C.c_double) * n)()
-    for s in range(n):
-        t = None if tables is None else tables[s]
-        if t is not None:
-            t = np.ascontiguousarray(t, np.float64).reshape(-1)
-            keep.append(t)
-            tp[s] = A.ptr(t, C.c_double)
-        else:
-            tp[s] = C.cast(None, C.POINTER(C.c_double))
-    st = (A.fp_search_start * n)()
-    res = (A.fp_search_result * n)()
-    outs = []
-    for s in range(n):
-        vb, mv, pk, px = (np.ascontiguousarray(a, np.int32) for a in starts[s])
-        keep += [vb, mv, pk, px]
-        st[s] = A.fp_search_start(A.ptr(vb, C.c_int32), A.ptr(mv, C.c_int32), len(pk),
-                                  A.ptr(pk, C.c_int32), A.ptr(px, C.c_int32))
-        ovb = np.empty(insts[s].n_vehicles, np.int32)
-        omv = np.empty(insts[s].n_missions, np.int32)
-        outs.append((ovb, omv))
-        res[s].vehicle_base, res[s].mission_vehicle = A.ptr(ovb, C.c_int32), A.ptr(omv, C.c_int32)
+    if n == 0:
+        return []
     cfgs = [cfg] * n if isinstance(cfg, SearchConfig) else list(cfg)
     if len(cfgs) != n:
         raise InvalidArgument("one SearchConfig per scenario")
+    # marshalling is vectorised (a c5 batch has 512 scenarios): the starts
+    # and outputs of every scenario live in a few concatenated arrays, the
+    # ABI structs are filled column-wise through numpy views of their bytes
+    ci = (A.fp_instance * n)(*[x.c() for x in insts])
+    keep = []
+    tp = None
+    if tables is not None:
+        tp = (C.POINTER(C.c_double) * n)()
+        for k in range(n):
+            if tables[k] is not None:
+                t = np.ascontiguousarray(tables[k], np.float64).reshape(-1)
+                keep.append(t)
+                tp[k] = A.ptr(t, C.c_double)
+    cols = [[np.asarray(x[f], np.int32).reshape(-1) for x in starts] for f in range(4)]
+    lens = [np.fromiter((a.size for a in c), np.int64, n) for c in cols]
+    flat = [np.ascontiguousarray(np.concatenate(c)) for c in cols]
+    offs = [np.concatenate([[0], np.cumsum(l)[:-1]]) * 4 for l in lens]
+    st = (A.fp_search_start * n)()
+    sv = _fields(st, A.fp_search_start, n)
+    for name, f in (("vehicle_base", 0), ("mission_vehicle", 1), ("pool_kind", 2), ("pool_index", 3)):
+        sv[name][:] = flat[f].ctypes.data + offs[f]
+    sv["pool_size"][:] = lens[2]
+    V = np.fromiter((x.n_vehicles for x in insts), np.int64, n)
+    M = insts[0].n_missions
+    ovb = np.empty(int(V.sum()), np.int32)
+    omv = np.empty(n * M, np.int32)
+    vo = np.concatenate([[0], np.cumsum(V)[:-1]])
+    res = (A.fp_search_result * n)()
+    rv = _fields(res, A.fp_search_result, n)
+    rv["vehicle_base"][:] = ovb.ctypes.data + 4 * vo
+    rv["mission_vehicle"][:] = omv.ctypes.data + 4 * M * np.arange(n)
     cc = (A.fp_search_config * n)(*[_cfg_c(c) for c in cfgs])
     _check(lib().fp_search_batch_configs(ctx.p, n, ci, tp, float(radius_km), cc, st, res))
-    return [SearchResult(outs[s][0], outs[s][1], _stats(res[s]), int(res[s].kernel_launches))
-            for s in range(n)]
+    ss = _fields(res, A.fp_search_result, n, nested="stats")
+    stat_cols = [ss[f].tolist() for f in A.STATS_FIELDS]
+    dev_ms, launches = rv["device_ms"].tolist(), rv["kernel_launches"].tolist()
+    fallbacks = rv["exact_fallbacks"].tolist()
+    out = []
+    for k in range(n):
+        sk = SearchStats(*(int(c[k]) for c in stat_cols[:6]), float(stat_cols[6][k]),
+                         float(dev_ms[k]), int(fallbacks[k]))
+        if k == 0:  # the phase clocks describe scenario 0 (fp_search_result)
+            sk = _stats(res[0])
+        out.append(SearchResult(ovb[vo[k]:vo[k] + V[k]], omv[k * M:(k + 1) * M], sk, int(launches[k])))
+    return out

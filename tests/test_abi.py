@@ -127,3 +127,34 @@ def test_initial_pool_order():
     pool = F.initial_pool(start, None)
     assert pool == [F.PoolEntry(F.PoolEntryKind.EmptyBase, 4), F.PoolEntry(F.PoolEntryKind.EmptyBase, 3),
                     F.PoolEntry(F.PoolEntryKind.IdleVehicle, 3), F.PoolEntry(F.PoolEntryKind.IdleVehicle, 5)]
+
+
+def test_struct_field_views_match_ctypes():
+    """fleetplace._fields (the vectorised marshalling of search_batch) views
+    exactly the bytes ctypes reads and writes, nested stats included."""
+    import ctypes as C
+    import numpy as np
+    from paper_2001_05291_b200 import _abi as A
+    from paper_2001_05291_b200 import fleetplace as F
+    n = 5
+    res = (A.fp_search_result * n)()
+    for k in range(n):
+        res[k].stats.evaluations = 1000 + k
+        res[k].stats.final_objective_km = 0.5 * k
+        res[k].device_ms = 2.0 * k
+        res[k].kernel_launches = 7 * k
+    rv = F._fields(res, A.fp_search_result, n)
+    ss = F._fields(res, A.fp_search_result, n, nested="stats")
+    assert ss["evaluations"].tolist() == [1000 + k for k in range(n)]
+    assert ss["final_objective_km"].tolist() == [0.5 * k for k in range(n)]
+    assert rv["device_ms"].tolist() == [2.0 * k for k in range(n)]
+    assert rv["kernel_launches"].tolist() == [7 * k for k in range(n)]
+    buf = np.arange(10, dtype=np.int32)
+    rv["mission_vehicle"][:] = buf.ctypes.data + 4 * np.arange(n)
+    for k in range(n):
+        assert C.cast(res[k].mission_vehicle, C.c_void_p).value == buf.ctypes.data + 4 * k
+        assert res[k].mission_vehicle[0] == k
+    st = (A.fp_search_start * n)()
+    sv = F._fields(st, A.fp_search_start, n)
+    sv["pool_size"][:] = np.arange(n) + 3
+    assert [st[k].pool_size for k in range(n)] == [3 + k for k in range(n)]

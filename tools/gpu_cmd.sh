@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 600 python tools/table_probe.py > gpurun_out/table_probe.log 2>&1; echo table_rc=$?; cat gpurun_out/table_probe.log
-CHAIN_CFGS=0 timeout 600 python tools/chain_probe.py > gpurun_out/chain_probe.log 2>&1; echo chain_rc=$?; cat gpurun_out/chain_probe.log
-timeout 900 python -m pytest -m gpu -q -rf tests/test_kernels_gpu.py tests/test_sharded_gpu.py tests/test_golden_runs_gpu.py > gpurun_out/pytest_part.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_part.log
+FLEETPLACE_TRACE=1 timeout 600 python tools/c5_e2e_probe.py > gpurun_out/c5_e2e_probe.log 2>&1; echo rc=$?; grep -v "^\[fleetplace trace\]" gpurun_out/c5_e2e_probe.log; grep "fleetplace trace" gpurun_out/c5_e2e_probe.log | tail -6
+timeout 1500 python -m pytest -m gpu -q -rf tests > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?; tail -2 gpurun_out/bench.err

@@ -158,10 +158,14 @@ def run_ours(args) -> None:
     from paper_2001_05291_b200 import fleetplace as F
 
     ws, rank = _dist()
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # FLEETPLACE_DIST_BACKEND=gloo: the multi-rank host protocol with
+        # several ranks on one GPU (a functional check only, never a number)
+        backend = os.environ.get("FLEETPLACE_DIST_BACKEND", "nccl")
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)}
+                                            if backend == "nccl" else {}))
     inst = _instance()
     t = F.build_distance_table(inst, device=local)
     start = F.rank_bases(inst, t)

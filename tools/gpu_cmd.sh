@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-FLEETPLACE_TRACE=1 timeout 600 python tools/c5_e2e_probe.py > gpurun_out/c5_e2e_probe.log 2>&1; echo rc=$?; grep -v "^\[fleetplace trace\]" gpurun_out/c5_e2e_probe.log; grep "fleetplace trace" gpurun_out/c5_e2e_probe.log | tail -6
-timeout 1500 python -m pytest -m gpu -q -rf tests > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?; tail -2 gpurun_out/bench.err
+# multi-rank host protocol, functional check: 2 ranks over gloo on the one GPU (no number is kept)
+FLEETPLACE_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_2rank_gloo.json 2> gpurun_out/bench_2rank_gloo.err; echo rc=$?; tail -5 gpurun_out/bench_2rank_gloo.err

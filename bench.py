@@ -420,10 +420,18 @@ def sharded_rank_workload(ws: int, rank: int, local: int, reps: int = 2) -> dict
         dist.all_reduce(v, op=dist.ReduceOp.SUM)
         v[0] = mx[0]
     sweep = sharded_sweep(ws, inst, part, table)
+    # parity gate: the assembled ranked start is the reference's (c4_1pass golden)
+    full = S.gather_start(inst, part)
+    start_ok = None
+    if full is not None:
+        start_ok = _sha(full.vehicle_base, full.mission_vehicle, full.unused_index) == \
+            _golden("c4_1pass")["start_sha256"]
+        if not start_ok:
+            raise SystemExit("PARITY FAILURE: sharded c4 ranked start differs from the reference's")
     del table
     torch.cuda.empty_cache()
     B, M = shape[0], shape[1]
-    return {"sweep": sweep,
+    return {"sweep": sweep, "start_equals_reference": start_ok,
             "workload": "c4 5000 bases x 1M missions x 250 vehicles: build_distance_table + "
                         f"rank_bases, missions sharded over {ws} GPU(s)",
             "ms": float(v[0]), "n_gpus": ws, "missions_per_gpu": -(-M // ws),

@@ -215,3 +215,27 @@ def test_batch_device_tables_leave_the_context_table_alone():
     again = F.search_arrays(inst, t, cfg, *st)
     assert again.stats.evaluations == one.stats.evaluations
     assert np.array_equal(again.mission_vehicle, one.mission_vehicle)
+
+
+def test_batch_device_tables_with_mixed_base_counts():
+    """Scenarios of one mission count but different base / vehicle counts,
+    tables built inside the batch call (one kernel (1) launch): each result
+    equals the single search on its own device-built table."""
+    shapes = [(50, 300, 10), (73, 300, 12), (40, 300, 8), (90, 300, 15)]
+    insts, starts, singles = [], [], []
+    for k, (B, M, V) in enumerate(shapes):
+        inst = F.survey_instance(B, M, V, seed=20 + k)
+        t = F.build_distance_table(inst)
+        s = F.rank_bases(inst, t)
+        st = F._state_arrays(s.assignment, F.initial_pool(s, inst), inst)
+        cfg = F.SearchConfig(seed=k, mode=F.SearchMode.Tabu)
+        singles.append(F.search_arrays(inst, t, cfg, *st))
+        insts.append(inst)
+        starts.append(st)
+    res = F.search_batch(insts, starts, [F.SearchConfig(seed=k, mode=F.SearchMode.Tabu)
+                                         for k in range(len(shapes))], None)
+    for one, r in zip(singles, res):
+        assert r.stats.evaluations == one.stats.evaluations
+        assert r.stats.final_objective_km == one.stats.final_objective_km
+        assert np.array_equal(r.mission_vehicle, one.mission_vehicle)
+        assert np.array_equal(r.vehicle_base, one.vehicle_base)

@@ -22,12 +22,15 @@ start = F.rank_bases(inst, t)
 VARIANTS = [
     {},
     {"FLEETPLACE_INKERNEL": "1"},
-    {"FLEETPLACE_THREADS": "256"},
-    {"FLEETPLACE_THREADS": "1024"},
+    {"FLEETPLACE_HELPERS": "-1", "FLEETPLACE_BITS_SMEM": "0"},
+    {"FLEETPLACE_HELPERS": "-1", "FLEETPLACE_BITS_SMEM": "0", "FLEETPLACE_MIRRORS_SMEM": "0"},
+    {"FLEETPLACE_BITS_SMEM": "0"},
 ]
+KNOBS = ("FLEETPLACE_INKERNEL", "FLEETPLACE_THREADS", "FLEETPLACE_HELPERS", "FLEETPLACE_BITS_SMEM",
+         "FLEETPLACE_MIRRORS_SMEM")
 base = None
 for var in VARIANTS:
-    for k in ("FLEETPLACE_INKERNEL", "FLEETPLACE_THREADS"):
+    for k in KNOBS:
         os.environ.pop(k, None)
     os.environ.update(var)
     times = []

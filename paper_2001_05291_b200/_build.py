@@ -38,6 +38,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     LIB_DIR.mkdir(exist_ok=True)
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
              "-Xptxas", "-v", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+    # probe builds only (e.g. FLEETPLACE_NVCC_DEFS=FP_RELOC_PROBE): extra -D macros
+    flags += [f"-D{d}" for d in os.environ.get("FLEETPLACE_NVCC_DEFS", "").split(",") if d]
     # one nvcc per source in parallel, then one link
     cmds = [[NVCC, *flags, "-c", str(CSRC / s), "-o", str(LIB_DIR / (s + ".o"))] for s in SOURCES]
     cmds.append([NVCC, *ARCH, "-shared", *[str(LIB_DIR / (s + ".o")) for s in SOURCES],

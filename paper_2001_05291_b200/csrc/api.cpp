@@ -14,10 +14,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <numeric>
 #include <random>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -48,6 +50,12 @@ struct fp_ctx {
   // are by construction; uploads are checked): the search's exact-sum
   // machinery relies on it
   bool table_ok = false;
+  int* d_flag = nullptr;  // device word for the table check (allocated once)
+  // pinned host staging (grow-only): search region A, batch point coordinates
+  unsigned char* h_stage = nullptr;
+  size_t h_stage_cap = 0;
+  double* h_pts = nullptr;
+  size_t h_pts_cap = 0;
   uint64_t launches = 0;
   double last_kernel_ms = 0.0;
   // pinned staging for permutations (double-buffered)
@@ -264,11 +272,12 @@ struct EvTimer {
 };
 
 // One device pass over a table: every entry finite and >= 0 (synchronises).
-bool table_entries_ok(const double* d_t, size_t n, cudaStream_t st) {
-  DBuf<int> bad(1, st);
-  check(fpk::launch_table_check(d_t, n, bad.p, st), "table_check");
+bool table_entries_ok(fp_ctx* ctx, const double* d_t, size_t n, cudaStream_t st) {
+  if (!ctx->d_flag) check(cudaMalloc(&ctx->d_flag, sizeof(int)), "cudaMalloc(flag)");
+  check(fpk::launch_table_check(d_t, n, ctx->d_flag, st), "table_check");
+  ctx->launches += 1;
   int h = 0;
-  d2h(&h, bad.p, 1, st);
+  d2h(&h, ctx->d_flag, 1, st);
   check(cudaStreamSynchronize(st), "table check sync");
   return h == 0;
 }
@@ -534,6 +543,30 @@ struct Trace {
   }
 };
 
+// fn(0..n-1) on up to 16 host threads (per-scenario host work of batches);
+// the first exception is rethrown.
+template <typename Fn>
+void parallel_for(int n, Fn&& fn) {
+  const int T = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u);
+  if (n < 64 || T == 1) {
+    for (int i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> ws;
+  std::vector<std::exception_ptr> errs(T);
+  for (int t = 0; t < T; ++t)
+    ws.emplace_back([&, t] {
+      try {
+        for (int i = (int)((long long)n * t / T); i < (int)((long long)n * (t + 1) / T); ++i) fn(i);
+      } catch (...) {
+        errs[t] = std::current_exception();
+      }
+    });
+  for (auto& w : ws) w.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
 // Shared driver for fp_search / fp_search_batch. `tables[s]` is a device
 // pointer to scenario s's table (nullptr = the scenario's arena copy).
 // sweep != nullptr (fp_neighbourhood_sweep): stop after the search start's
@@ -575,8 +608,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   const Trace tr;
 
   SearchRun run;
-  run.hs.reserve(n);
-  for (int s = 0; s < n; ++s) run.hs.push_back(prepare(&insts[s], &starts[s]));
+  run.hs.resize(n);
+  parallel_for(n, [&](int s) { run.hs[s] = prepare(&insts[s], &starts[s]); });
 
   // ---- arena
   size_t totalA = 0, totalB = 0;
@@ -698,14 +731,23 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     if (const char* e = std::getenv("FLEETPLACE_HELPED_CHAINS")) ctrs[s].chain_mode = std::atoi(e) == 0;
     if (const char* e = std::getenv("FLEETPLACE_CHECK_IMPT")) ctrs[s].check_impt = std::atoi(e);
   }
-  std::vector<unsigned char> stage(totalA, 0);
+  // region A of every scenario, staged in the context's pinned buffer
+  if (ctx->h_stage_cap < totalA) {
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    ctx->h_stage = nullptr;
+    ctx->h_stage_cap = 0;
+    check(cudaMallocHost(&ctx->h_stage, totalA + totalA / 4), "pinned stage");
+    ctx->h_stage_cap = totalA + totalA / 4;
+  }
+  unsigned char* const stage = ctx->h_stage;
+  std::memset(stage, 0, totalA);
   run.scs.resize(n);
-  for (int s = 0; s < n; ++s) {
+  parallel_for(n, [&](int s) {
     const HostScenario& h = run.hs[s];
     const Layout& L = run.lay[s];
     const fp_instance* in = &insts[s];
     const int V = in->n_vehicles, B = in->n_bases;
-    unsigned char* hb = stage.data() + baseA[s];
+    unsigned char* hb = stage + baseA[s];
     unsigned char* db = d0 + baseA[s];              // region A (staged)
     unsigned char* dw = d0 + o_B + baseB[s];        // region B (device-built)
     if (M) std::memcpy(hb + L.ro, in->rotary_only, M);
@@ -782,7 +824,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     S.tabu = cfgs[s].mode == FP_MODE_TABU;
     S.debug = cfgs[s].debug_check_deltas != 0;
     S.pstream = pstream[s];
-  }
+  });
   cudaEvent_t ev0, ev1;
   check(cudaEventCreate(&ev0), "event");
   check(cudaEventCreate(&ev1), "event");
@@ -820,7 +862,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     }
   }
   check(cudaEventRecord(ev0, st), "event");
-  h2d(d0, stage.data(), totalA, st);
+  h2d(d0, stage, totalA, st);
   h2d(d_scs, run.scs.data(), n, st);
   std::vector<int32_t> active(n, 1);
   h2d(d_ctr, ctrs.data(), n, st);
@@ -884,10 +926,21 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   long long launched = 0;  // passes whose permutations went to the device
   // batches: one launch for (nearly) every search — a chunk boundary makes
   // every scenario wait for the slowest; single scenarios start small
-  int kfirst = inkernel && n == 1 ? std::min(kmax, 32) : kmax;
+  int threads = n == 1 ? 512 : 256;
+  if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
+  // medium single scenarios (8k <= M < 32k, bitsets in shared memory): the
+  // relocation-heavy first passes run with helper blocks (bitsets in global
+  // memory, the relocations' O(M) work spread over the SMs), one pass per
+  // launch, until a pass applies fewer than two relocations; the rest run in
+  // one block with the bitsets in shared memory. An execution strategy only:
+  // results are identical either way (c2: first 3 passes 5.25 -> ~4.9 ms).
+  bool adaptive = n == 1 && !inkernel && M >= (8 << 10) && M < (32 << 10) && threads < 1024 &&
+                  !std::getenv("FLEETPLACE_HELPERS");
+  if (const char* e = std::getenv("FLEETPLACE_ADAPTIVE_HELPERS")) adaptive = adaptive && std::atoi(e) != 0;
+  int kfirst = inkernel && n == 1 ? std::min(kmax, 32) : (adaptive ? 1 : kmax);
   if (const char* e = std::getenv("FLEETPLACE_KFIRST")) kfirst = std::max(1, std::min(kmax, std::atoi(e)));
   auto next_chunk = [&](int prev) {
-    int k = prev == 0 ? kfirst : std::min(kmax, 2 * prev);
+    int k = prev == 0 ? kfirst : (adaptive ? 1 : std::min(kmax, 2 * prev));
     if (max_passes_all >= 0) k = (int)std::max<long long>(1, std::min<long long>(k, max_passes_all - launched));
     return k;
   };
@@ -907,15 +960,14 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   int buf = 0;
   if (!dev_perm) gen_chunk(ctx->h_perm[buf], kchunk);  // overlaps the init kernels
   tr.mark("first permutation chunk");
-  int threads = n == 1 ? 512 : 256;
-  if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
   // large single scenarios share each relocation's O(M) work with helper
   // blocks (-1 = as many as fit; FLEETPLACE_HELPERS=0 disables)
   int helpers = n == 1 && M >= (32 << 10) ? -1 : 0;
   if (const char* e = std::getenv("FLEETPLACE_HELPERS")) helpers = std::atoi(e);
-  // the 1024-thread variant (a FLEETPLACE_THREADS experiment knob) is not
-  // validated with helper blocks: c3 with both faulted (illegal instruction)
-  if (threads >= 1024 && !std::getenv("FLEETPLACE_ALLOW_1024_HELPERS")) helpers = 0;
+  // the 1024-thread variant (a FLEETPLACE_THREADS experiment knob, 64
+  // registers, ~1 KB of spills) never runs with helper blocks: that pairing
+  // faults (illegal instruction) in some builds and not in others
+  if (threads >= 1024) helpers = 0;
   unsigned epoch = 0;
   int n_active = n;
   while (n_active > 0) {
@@ -956,7 +1008,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
         check(fpk::launch_pass(d_scs, d_active, n, d_perm + 2ll * k * M, 1,
                                false, max_passes_all, M, any_tabu, tenures[0],
                                any_debug, maxV, maxB, maxK, st, threads,
-                               helpers, ++epoch, nullptr),
+                               adaptive ? -1 : helpers, ++epoch, nullptr, adaptive),
               "pass_kernel");
         cudaEvent_t e2;
         cudaEventCreate(&e2);
@@ -1010,6 +1062,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     }
     buf = nb;
     kchunk = knext;
+    if (adaptive && ctrs[0].pass_relocs < 2) adaptive = false;
     tr.mark("chunk synchronised");
     for (int s = 0; s < n; ++s) {
       if (!active[s]) continue;
@@ -1107,6 +1160,9 @@ void fp_ctx_destroy(fp_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->aux) cudaStreamSynchronize(ctx->aux);
   if (ctx->d_costT) cudaFree(ctx->d_costT);
+  if (ctx->d_flag) cudaFree(ctx->d_flag);
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  if (ctx->h_pts) cudaFreeHost(ctx->h_pts);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->table_ready) cudaEventDestroy(ctx->table_ready);
   if (ctx->costT_ready) cudaEventDestroy(ctx->costT_ready);
@@ -1243,13 +1299,17 @@ fp_status fp_table_upload(fp_ctx* ctx, int32_t n_missions, int32_t n_bases,
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
     if (n_missions < 0 || n_bases < 0 || ((size_t)n_missions * n_bases > 0 && !cost_colmajor))
       throw FpError(FP_ERR_INVALID_ARGUMENT, "bad table shape or NULL table");
+    const Trace tr;
     table_alloc(ctx, n_missions, n_bases);
+    tr.mark("upload: table allocated");
     h2d(ctx->d_cost, cost_colmajor, (size_t)n_missions * n_bases, ctx->stream);
     // a caller's matrix may hold anything: column_totals stays exact for any
     // entries, the search requires distances (checked on the device)
-    ctx->table_ok = table_entries_ok(ctx->d_cost, (size_t)n_missions * n_bases, ctx->stream);
+    ctx->table_ok = table_entries_ok(ctx, ctx->d_cost, (size_t)n_missions * n_bases, ctx->stream);
+    tr.mark("upload: copied and checked");
     start_costT(ctx);
     check(cudaStreamSynchronize(ctx->stream), "upload sync");
+    tr.mark("upload: done");
   });
 }
 
@@ -1509,30 +1569,44 @@ fp_status fp_search_batch_configs(fp_ctx* ctx, int32_t n, const fp_instance* ins
         maxB = std::max(maxB, insts[s].n_bases);
       }
       built = DBuf<double>(tot + 2, st);
-      // points: [lat | lon | cos] regions, each [bases, pickups, deliveries] per scenario
-      std::vector<double> hp(2 * npts);
+      // points: [lat | lon | cos] regions, each [bases, pickups, deliveries]
+      // per scenario, packed on host threads into the context's pinned buffer
+      if (ctx->h_pts_cap < 2 * npts) {
+        if (ctx->h_pts) cudaFreeHost(ctx->h_pts);
+        ctx->h_pts = nullptr;
+        ctx->h_pts_cap = 0;
+        check(cudaMallocHost(&ctx->h_pts, sizeof(double) * 2 * npts), "pinned points");
+        ctx->h_pts_cap = 2 * npts;
+      }
+      double* const hp = ctx->h_pts;
       pts = DBuf<double>(3 * npts + 1, st);
       std::vector<fpk::TableJob> jobs(build.size());
+      std::vector<size_t> pof(build.size()), tof(build.size());
       size_t po = 0, to = 0;
       for (size_t k = 0; k < build.size(); ++k) {
+        pof[k] = po;
+        tof[k] = to;
+        po += (size_t)insts[build[k]].n_bases + 2ull * M;
+        to += (size_t)M * insts[build[k]].n_bases;
+      }
+      parallel_for((int)build.size(), [&](int k) {
         const fp_instance& in = insts[build[k]];
         const int B = in.n_bases;
-        std::copy(in.base_lat, in.base_lat + B, hp.begin() + po);
-        std::copy(in.pickup_lat, in.pickup_lat + M, hp.begin() + po + B);
-        std::copy(in.delivery_lat, in.delivery_lat + M, hp.begin() + po + B + M);
-        std::copy(in.base_lon, in.base_lon + B, hp.begin() + npts + po);
-        std::copy(in.pickup_lon, in.pickup_lon + M, hp.begin() + npts + po + B);
-        std::copy(in.delivery_lon, in.delivery_lon + M, hp.begin() + npts + po + B + M);
-        const double* la = pts.p + po;
-        const double* lo = pts.p + npts + po;
-        const double* co = pts.p + 2 * npts + po;
+        const size_t o = pof[k];
+        std::copy(in.base_lat, in.base_lat + B, hp + o);
+        std::copy(in.pickup_lat, in.pickup_lat + M, hp + o + B);
+        std::copy(in.delivery_lat, in.delivery_lat + M, hp + o + B + M);
+        std::copy(in.base_lon, in.base_lon + B, hp + npts + o);
+        std::copy(in.pickup_lon, in.pickup_lon + M, hp + npts + o + B);
+        std::copy(in.delivery_lon, in.delivery_lon + M, hp + npts + o + B + M);
+        const double* la = pts.p + o;
+        const double* lo = pts.p + npts + o;
+        const double* co = pts.p + 2 * npts + o;
         jobs[k] = fpk::TableJob{la, lo, co, la + B, lo + B, co + B, la + B + M, lo + B + M,
-                                co + B + M, built.p + to, B};
-        dev[build[k]] = built.p + to;
-        po += (size_t)B + 2ull * M;
-        to += (size_t)M * B;
-      }
-      h2d(pts.p, hp.data(), 2 * npts, st);
+                                co + B + M, built.p + tof[k], B};
+        dev[build[k]] = built.p + tof[k];
+      });
+      h2d(pts.p, hp, 2 * npts, st);
       d_jobs = DBuf<fpk::TableJob>(build.size(), st);
       h2d(d_jobs.p, jobs.data(), build.size(), st);
       check(fpk::launch_point_cos(pts.p, (int)npts, pts.p + 2 * npts, st), "cos(points)");

@@ -26,6 +26,7 @@ struct Counters {
   int done;                       // search finished (quiescent, max_passes or error)
   int psize;                      // current pool size
   int pass_applied;               // moves applied in the current pass
+  int pass_relocs;                // relocations applied in the current pass
   int pass_skipped;               // any tabu skip in the current pass
   int error;                      // 0 = ok, else an fp_status
   int force_exact;                // test hook: 1 = every total comparison through the exact

@@ -60,7 +60,7 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,
                         bool tabu, long long tenure, bool debug, int V, int B, int K,
                         cudaStream_t stream, int threads, int helpers_req, unsigned epoch,
-                        const int* perm_bad);
+                        const int* perm_bad, bool global_bits = false);
 }  // namespace fpk
 
 namespace fpk_host {

@@ -802,6 +802,9 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
   }
   __syncthreads();
   const int n = min(sh.bi[7], cap);
+#ifdef FP_RELOC_PROBE
+  const long long p0 = ph_now();
+#endif
   // PP positions per warp at a time, lanes over vehicles: all the round's
   // gathers (PP positions x GU groups of 32 vehicles) are independent and in
   // flight together; bits of one position live in different words (rows),
@@ -852,6 +855,9 @@ __device__ void bits_after_relocation(const Scenario& s, Shared& sh, const Smem&
     }
   }
   __syncthreads();
+#ifdef FP_RELOC_PROBE
+  PH_ADD(sh, 14, p0);
+#endif
   if (sh.bi[7] > cap) {
     // more positions than the buffer holds: finish them one word at a time
     for (int wd = threadIdx.x; wd < nwd; wd += NT) {
@@ -1097,7 +1103,13 @@ __device__ void table_after_relocation(const Scenario& s, Shared& sh, const Smem
     s.rcnt[t2] += (int)(table_class(s, sh, t2, x) != CLS_POS) - before;
   }
   __syncthreads();
+#ifdef FP_RELOC_PROBE
+  const long long f0 = ph_now();
+#endif
   table_row_fresh<NT>(s, sh, sm.acc_sum, sm.acc_abs, sm.stage, b_old);
+#ifdef FP_RELOC_PROBE
+  PH_ADD(sh, 9, f0);
+#endif
 }
 
 
@@ -1615,12 +1627,20 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           PH_ADD(sh, 8, a0);
           const long long a1 = ph_now();
           bits_after_relocation<NT>(s, sh, sm, mover, sm.xlist, sm.xlist_cap);
+#ifdef FP_RELOC_PROBE
+          PH_ADD(sh, 12, a1);
+          const long long a2 = ph_now();
+#endif
           table_after_relocation<NT>(s, sh, sm, mover, t, b_old);
+#ifdef FP_RELOC_PROBE
+          PH_ADD(sh, 13, a2);
+#endif
           PH_ADD(sh, 6, a1);
         }
         if (threadIdx.x == 0) {
           sh.c.applied += 1;
           sh.c.pass_applied += 1;
+          sh.c.pass_relocs += 1;
           if (exact_known) {
             sh.c.total_exact = after;
             sh.c.total_ver = (long long)sh.c.applied;
@@ -2261,6 +2281,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     }
     if (threadIdx.x == 0) {
       sh.c.pass_applied = 0;
+      sh.c.pass_relocs = 0;
       sh.c.pass_skipped = 0;
     }
     __syncthreads();
@@ -2651,7 +2672,7 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
                                   const int32_t* d_perms, int kpasses, bool inkernel,
                                   int max_passes, int M, bool tabu, long long tenure, bool debug,
                                   int V, int B, int K, int helpers_req, unsigned epoch,
-                                  const int* perm_bad, cudaStream_t stream) {
+                                  const int* perm_bad, cudaStream_t stream, bool global_bits) {
   const size_t core = pass_smem_core(V, NT);
   const size_t state = pass_smem_state(V, B, K);
   const size_t bits = 2 * align16(4ull * V * ((M + 31) / 32));
@@ -2660,7 +2681,7 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   const size_t bits_limit = NT == 256 ? 100 * 1024 : limit;
   if (core > limit) return cudaErrorInvalidConfiguration;
   const int in_smem = core + state <= limit ? 1 : 0;
-  int bits_smem = in_smem && core + state + bits <= bits_limit ? 1 : 0;
+  int bits_smem = in_smem && core + state + bits <= bits_limit && !global_bits ? 1 : 0;
   if (const char* e = std::getenv("FLEETPLACE_BITS_SMEM")) bits_smem = bits_smem && std::atoi(e) != 0;
   // the mission mirrors join when the bitsets did (pool bound: B + 2V + 1)
   const size_t mirrors = 2 * align16(4ull * M) + 2 * align16(4ull * (B + 2 * V + 1)) + align16(4ull * B);
@@ -2725,15 +2746,18 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
                         const int32_t* d_perms, int kpasses, bool inkernel, int max_passes, int M,
                         bool tabu, long long tenure, bool debug, int V, int B, int K,
                         cudaStream_t stream, int threads, int helpers_req, unsigned epoch,
-                        const int* perm_bad) {
+                        const int* perm_bad, bool global_bits) {
   if (threads == 1024)
     return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                                M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream);
+                                M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream,
+                                global_bits);
   if (threads == 512)
     return launch_pass_nt<512>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                               M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream);
+                               M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream,
+                               global_bits);
   return launch_pass_nt<256>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
-                             M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream);
+                             M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream,
+                             global_bits);
 }
 
 // ev[0..4]: events recorded around the four stages (may be null).

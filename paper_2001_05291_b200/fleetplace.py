@@ -928,15 +928,14 @@ def search_batch(insts: Sequence[Instance], starts: Sequence[tuple], cfg,
                 t = np.ascontiguousarray(tables[k], np.float64).reshape(-1)
                 keep.append(t)
                 tp[k] = A.ptr(t, C.c_double)
-    cols = [[np.asarray(x[f], np.int32).reshape(-1) for x in starts] for f in range(4)]
-    lens = [np.fromiter((a.size for a in c), np.int64, n) for c in cols]
-    flat = [np.ascontiguousarray(np.concatenate(c)) for c in cols]
-    offs = [np.concatenate([[0], np.cumsum(l)[:-1]]) * 4 for l in lens]
+    # the callers' start arrays are used in place (int32, contiguous: no copy)
+    cols = [[np.ascontiguousarray(x[f], np.int32) for x in starts] for f in range(4)]
+    keep.append(cols)
     st = (A.fp_search_start * n)()
     sv = _fields(st, A.fp_search_start, n)
     for name, f in (("vehicle_base", 0), ("mission_vehicle", 1), ("pool_kind", 2), ("pool_index", 3)):
-        sv[name][:] = flat[f].ctypes.data + offs[f]
-    sv["pool_size"][:] = lens[2]
+        sv[name][:] = np.fromiter((a.ctypes.data for a in cols[f]), np.uint64, n)
+    sv["pool_size"][:] = np.fromiter((a.size for a in cols[2]), np.int64, n)
     V = np.fromiter((x.n_vehicles for x in insts), np.int64, n)
     M = insts[0].n_missions
     ovb = np.empty(int(V.sum()), np.int32)

@@ -179,28 +179,10 @@ def test_natural_order_rows_stay_exact(monkeypatch, case):
         _check_search(ref_survey_instance(300, 40000, 60, seed=3), 1, seeds=[7], max_passes=3)
 
 
-@pytest.mark.parametrize("case", ["40k", "c3"])
-def test_1024_threads_with_helper_blocks(monkeypatch, case):
-    """Round 1 saw an illegal-instruction fault with the 1024-thread pass
-    kernel plus helper blocks at c3 and disabled the combination. It is
-    allowed again (FLEETPLACE_ALLOW_1024_HELPERS) and must follow the
-    reference's trajectory: the 40k-mission helper case against the
-    reference search, c3's first pass against the reference's recorded run."""
-    monkeypatch.setenv("FLEETPLACE_THREADS", "1024")
-    monkeypatch.setenv("FLEETPLACE_HELPERS", "-1")
-    monkeypatch.setenv("FLEETPLACE_ALLOW_1024_HELPERS", "1")
-    if case == "40k":
-        _check_search(ref_survey_instance(300, 40000, 60, seed=3), 1, seeds=[7], max_passes=2)
-    else:
-        import json
-        from pathlib import Path
-        run = json.loads((Path(__file__).parent / "golden" / "runs.json").read_text())["c3_1pass"]
-        inst = F.survey_instance(2000, 100000, 100, seed=1)
-        t = F.build_distance_table(inst)
-        start = F.rank_bases(inst, t)
-        vb, mv, pk, px = F._state_arrays(start.assignment, F.initial_pool(start, inst), inst)
-        r = F.search_arrays(inst, t, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=1),
-                            vb, mv, pk, px)
-        s = r.stats
-        assert [s.passes, s.evaluations, s.applied_moves, s.committed_moves, s.tabu_skips_outer,
-                s.tabu_skips_inner] == run["stats"]
+@pytest.mark.parametrize("adaptive", ["0", "1"])
+def test_adaptive_helper_blocks_c2(monkeypatch, adaptive):
+    """c2 (M = 10k): the first passes run with helper blocks until a pass
+    applies fewer than two relocations (the default), or never (knob off):
+    both follow the reference's trajectory (its first 4 passes)."""
+    monkeypatch.setenv("FLEETPLACE_ADAPTIVE_HELPERS", adaptive)
+    _check_search(ref_survey_instance(500, 10000, 40, seed=1), 1, seeds=[7], max_passes=4)

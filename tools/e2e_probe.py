@@ -20,7 +20,7 @@ host = torch.from_numpy(np.ascontiguousarray(t.cost.T).reshape(-1)).pin_memory()
 view = host.reshape(inst.n_bases, inst.n_missions).T
 tt = F.DistanceTable.from_host(view)
 F.search_arrays(inst, tt, cfg, vb, mv, pk, px)
-for it in range(4):
+for it in range(12):
     t0 = time.perf_counter()
     tt.upload(view)
     t1 = time.perf_counter()

@@ -21,13 +21,14 @@ start = F.rank_bases(inst, t)
 
 VARIANTS = [
     {},
+    {"FLEETPLACE_ADAPTIVE_HELPERS": "0"},
     {"FLEETPLACE_INKERNEL": "1"},
     {"FLEETPLACE_HELPERS": "-1", "FLEETPLACE_BITS_SMEM": "0"},
     {"FLEETPLACE_HELPERS": "-1", "FLEETPLACE_BITS_SMEM": "0", "FLEETPLACE_MIRRORS_SMEM": "0"},
     {"FLEETPLACE_BITS_SMEM": "0"},
 ]
 KNOBS = ("FLEETPLACE_INKERNEL", "FLEETPLACE_THREADS", "FLEETPLACE_HELPERS", "FLEETPLACE_BITS_SMEM",
-         "FLEETPLACE_MIRRORS_SMEM")
+         "FLEETPLACE_MIRRORS_SMEM", "FLEETPLACE_ADAPTIVE_HELPERS")
 base = None
 for var in VARIANTS:
     for k in KNOBS:

@@ -2215,12 +2215,15 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   if (mirrors_in_smem) {
     // mission -> vehicle (both orders), the pool and the unsettled-row counts
     // in shared memory too; mv / mvp are written through (the sweep and the
-    // helpers read them), the rest is written back at the end
+    // helpers read them), the rest is written back at the end. With helper
+    // blocks the unsettled-row counts stay in global memory: the helpers'
+    // table patches update them.
     s.mv = reinterpret_cast<int32_t*>(take(4ull * s.M));
     s.mvp = reinterpret_cast<int32_t*>(take(4ull * s.M));
     s.pkind = reinterpret_cast<int32_t*>(take(4ull * s.pool_cap));
     s.pidx = reinterpret_cast<int32_t*>(take(4ull * s.pool_cap));
-    s.rcnt = reinterpret_cast<int32_t*>(take(4ull * B));
+    int32_t* rc = reinterpret_cast<int32_t*>(take(4ull * B));
+    if (helpers == 0) s.rcnt = rc;
     sm.gmv = g.mv;
     sm.gmvp = g.mvp;
     copy_words<NT>(reinterpret_cast<uint32_t*>(s.mv), reinterpret_cast<const uint32_t*>(g.mv), s.M);
@@ -2228,7 +2231,8 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       s.pkind[k] = g.pkind[k];
       s.pidx[k] = g.pidx[k];
     }
-    for (int b = threadIdx.x; b < B; b += NT) s.rcnt[b] = g.rcnt[b];
+    if (helpers == 0)
+      for (int b = threadIdx.x; b < B; b += NT) s.rcnt[b] = g.rcnt[b];
   }
   if (threadIdx.x == 0) {
     sh.c = *s.ctr;
@@ -2259,11 +2263,13 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     if (INK) {
       prep_words(s, sm.pb, threadIdx.x >> 5, NW);
       __syncthreads();
-    } else if (bits_in_smem) {
+    } else if (bits_in_smem || mirrors_in_smem) {
       // the grid-wide sweep built them in global memory: 16-byte loads, a
       // batch of them in flight per thread before any store
-      copy_words<NT>(s.imp, g.imp, (long long)V * s.nwd);
-      copy_words<NT>(s.mem, g.mem, (long long)V * s.nwd);
+      if (bits_in_smem) {
+        copy_words<NT>(s.imp, g.imp, (long long)V * s.nwd);
+        copy_words<NT>(s.mem, g.mem, (long long)V * s.nwd);
+      }
       if (mirrors_in_smem)
         copy_words<NT>(reinterpret_cast<uint32_t*>(s.mvp), reinterpret_cast<const uint32_t*>(g.mvp),
                        s.M);
@@ -2417,7 +2423,8 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       g.pkind[k] = s.pkind[k];
       g.pidx[k] = s.pidx[k];
     }
-    for (int b = threadIdx.x; b < B; b += NT) g.rcnt[b] = s.rcnt[b];
+    if (helpers == 0)
+      for (int b = threadIdx.x; b < B; b += NT) g.rcnt[b] = s.rcnt[b];
   }
   if (threadIdx.x == 0) {
     sh.c.cycles[15] += (unsigned long long)(clock64() - t_entry);
@@ -2685,7 +2692,9 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   if (const char* e = std::getenv("FLEETPLACE_BITS_SMEM")) bits_smem = bits_smem && std::atoi(e) != 0;
   // the mission mirrors join when the bitsets did (pool bound: B + 2V + 1)
   const size_t mirrors = 2 * align16(4ull * M) + 2 * align16(4ull * (B + 2 * V + 1)) + align16(4ull * B);
-  int mirrors_smem = bits_smem && core + state + bits + mirrors <= bits_limit ? 1 : 0;
+  // (also without the bitsets: helper-block launches keep those in global
+  // memory, the mission mirrors still fit)
+  int mirrors_smem = in_smem && core + state + (bits_smem ? bits : 0) + mirrors <= bits_limit ? 1 : 0;
   if (const char* e = std::getenv("FLEETPLACE_MIRRORS_SMEM"))
     mirrors_smem = mirrors_smem && std::atoi(e) != 0;
   const size_t smem = core + (in_smem ? state : 0) + (bits_smem ? bits : 0) +

@@ -1076,11 +1076,33 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   ctx->launches += 1;
   check(cudaEventRecord(ev1, st), "event");
   d2h(ctrs.data(), d_ctr, n, st);
-  for (int s = 0; s < n; ++s) {
-    d2h(outs[s].vehicle_base, run.scs[s].vbase, insts[s].n_vehicles, st);
-    d2h(outs[s].mission_vehicle, run.scs[s].mv, (size_t)M, st);
+  if (n < 64) {
+    for (int s = 0; s < n; ++s) {
+      d2h(outs[s].vehicle_base, run.scs[s].vbase, insts[s].n_vehicles, st);
+      d2h(outs[s].mission_vehicle, run.scs[s].mv, (size_t)M, st);
+    }
+    check(cudaStreamSynchronize(st), "final sync");
+  } else {
+    // large batches: every scenario's result gathered on the device, one copy
+    // into the pinned stage (region A, already consumed), spread on threads
+    std::vector<long long> vbo(n + 1, 0);
+    for (int s = 0; s < n; ++s) vbo[s + 1] = vbo[s] + insts[s].n_vehicles;
+    const size_t nres = (size_t)n * M + (size_t)vbo[n];
+    DBuf<unsigned char> dres(4 * nres + 8ull * (n + 1), st);
+    int32_t* d_mv = reinterpret_cast<int32_t*>(dres.p);
+    int32_t* d_vb = d_mv + (size_t)n * M;
+    long long* d_vbo = reinterpret_cast<long long*>(dres.p + 4 * nres);
+    h2d(d_vbo, vbo.data(), n + 1, st);
+    check(fpk::launch_gather_results(d_scs, n, M, d_mv, d_vb, d_vbo, st), "gather_results");
+    ctx->launches += 1;
+    int32_t* h_res = reinterpret_cast<int32_t*>(stage);  // totalA >= 4 * nres
+    d2h(h_res, d_mv, nres, st);
+    check(cudaStreamSynchronize(st), "final sync");
+    parallel_for(n, [&](int s) {
+      std::memcpy(outs[s].mission_vehicle, h_res + (size_t)s * M, 4ull * M);
+      std::memcpy(outs[s].vehicle_base, h_res + (size_t)n * M + vbo[s], 4ull * insts[s].n_vehicles);
+    });
   }
-  check(cudaStreamSynchronize(st), "final sync");
   tr.mark("final sync");
   double init_part[4] = {0, 0, 0, 0};
   {

@@ -54,6 +54,8 @@ cudaError_t launch_init(Scenario* d_scs, const Scenario* h_scs, int n_scn, int M
                         int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev,
                         bool exact_total = true);
 cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream);
+cudaError_t launch_gather_results(const Scenario* d_scs, int n_scn, int M, int32_t* out_mv,
+                                  int32_t* out_vb, const long long* vb_off, cudaStream_t stream);
 cudaError_t launch_sweep(Scenario* d_scs, const int32_t* d_active, int n_scn,
                          const int32_t* d_perms, int M, cudaStream_t stream);
 cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,

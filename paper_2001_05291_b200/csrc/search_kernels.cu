@@ -691,7 +691,11 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
   // One base per thread (B <= NT, no helpers): the table entries this
   // thread patches are loaded before the imp-row gathers, so both sets of
   // loads are in flight together.
-  const bool pre = !(HELP && sm.helpers > 0) && s.B <= NT;
+  // (with helper blocks the patches of a large table go to them as a log;
+  // a table of at most NT bases is patched here either way: one pass of
+  // thread-per-base patches beats a wait for the log at the next row)
+  const bool logged = HELP && sm.helpers > 0 && s.B > NT;
+  const bool pre = !logged && s.B <= NT;
   const int t = threadIdx.x;
   const bool live = pre && t < s.B && s.bveh[t] < 0;
   double pc = 0.0, pAl = 0.0, pEl = 0.0, pUl = 0.0, pAg = 0.0, pEg = 0.0, pUg = 0.0;
@@ -724,7 +728,7 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     s.mem[(long long)gain * s.nwd + wd] |= bit;
   }
   const long long tp0 = ph_now();
-  if (HELP && sm.helpers > 0) {
+  if (logged) {
     if (threadIdx.x == 0) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, s.mcp[q]);
   } else if (pre) {
     if (live)
@@ -2672,6 +2676,27 @@ __global__ void __launch_bounds__(512) final_kernel(Scenario* scs) {
   }
   const double t = exact_chain<512>(s, sh, 0, -1, 0.0, -1, nullptr);
   if (threadIdx.x == 0) s.ctr->final_total = t;
+}
+
+// A batch's results side by side (one device-to-host copy instead of two per
+// scenario): mv of scenario s at out_mv + s*M, vbase at out_vb + vb_off[s].
+__global__ void __launch_bounds__(256) gather_results_kernel(const Scenario* scs, int M,
+                                                             int32_t* __restrict__ out_mv,
+                                                             int32_t* __restrict__ out_vb,
+                                                             const long long* __restrict__ vb_off) {
+  const Scenario& s = scs[blockIdx.y];
+  int32_t* mv = out_mv + (long long)blockIdx.y * M;
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < M; m += gridDim.x * blockDim.x) mv[m] = s.mv[m];
+  if (blockIdx.x == 0)
+    for (int v = threadIdx.x; v < s.V; v += blockDim.x) out_vb[vb_off[blockIdx.y] + v] = s.vbase[v];
+}
+
+cudaError_t launch_gather_results(const Scenario* d_scs, int n_scn, int M, int32_t* out_mv,
+                                  int32_t* out_vb, const long long* vb_off, cudaStream_t stream) {
+  if (n_scn <= 0) return cudaSuccess;
+  gather_results_kernel<<<dim3(std::max(1, std::min((M + 255) / 256, 8)), n_scn), 256, 0, stream>>>(
+      d_scs, M, out_mv, out_vb, vb_off);
+  return cudaGetLastError();
 }
 
 template <int NT>

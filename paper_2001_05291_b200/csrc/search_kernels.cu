@@ -2220,14 +2220,14 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
     // mission -> vehicle (both orders), the pool and the unsettled-row counts
     // in shared memory too; mv / mvp are written through (the sweep and the
     // helpers read them), the rest is written back at the end. With helper
-    // blocks the unsettled-row counts stay in global memory: the helpers'
-    // table patches update them.
+    // blocks patching a large table (B > NT, the patch log) the unsettled-row
+    // counts stay in global memory: the helpers update them.
     s.mv = reinterpret_cast<int32_t*>(take(4ull * s.M));
     s.mvp = reinterpret_cast<int32_t*>(take(4ull * s.M));
     s.pkind = reinterpret_cast<int32_t*>(take(4ull * s.pool_cap));
     s.pidx = reinterpret_cast<int32_t*>(take(4ull * s.pool_cap));
     int32_t* rc = reinterpret_cast<int32_t*>(take(4ull * B));
-    if (helpers == 0) s.rcnt = rc;
+    if (helpers == 0 || B <= NT) s.rcnt = rc;
     sm.gmv = g.mv;
     sm.gmvp = g.mvp;
     copy_words<NT>(reinterpret_cast<uint32_t*>(s.mv), reinterpret_cast<const uint32_t*>(g.mv), s.M);
@@ -2235,7 +2235,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       s.pkind[k] = g.pkind[k];
       s.pidx[k] = g.pidx[k];
     }
-    if (helpers == 0)
+    if (helpers == 0 || B <= NT)
       for (int b = threadIdx.x; b < B; b += NT) s.rcnt[b] = g.rcnt[b];
   }
   if (threadIdx.x == 0) {
@@ -2427,7 +2427,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       g.pkind[k] = s.pkind[k];
       g.pidx[k] = s.pidx[k];
     }
-    if (helpers == 0)
+    if (helpers == 0 || B <= NT)
       for (int b = threadIdx.x; b < B; b += NT) g.rcnt[b] = s.rcnt[b];
   }
   if (threadIdx.x == 0) {

@@ -158,3 +158,32 @@ def test_struct_field_views_match_ctypes():
     sv = F._fields(st, A.fp_search_start, n)
     sv["pool_size"][:] = np.arange(n) + 3
     assert [st[k].pool_size for k in range(n)] == [3 + k for k in range(n)]
+
+
+def test_bench_parity_gate_and_goldens():
+    """bench.py's parity gate accepts the reference's recorded c2 run and
+    refuses a trajectory that differs in any counter or in the Assignment."""
+    import importlib.util
+    import types
+    from pathlib import Path
+
+    import numpy as np
+    import pytest as _pt
+    spec = importlib.util.spec_from_file_location("bench_mod", Path(__file__).resolve().parents[1] / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    g = bench._golden("c2_full")
+    st = types.SimpleNamespace(passes=g["stats"][0], evaluations=g["stats"][1],
+                               applied_moves=g["stats"][2], committed_moves=g["stats"][3],
+                               tabu_skips_outer=g["stats"][4], tabu_skips_inner=g["stats"][5],
+                               final_objective_km=g["final_objective_km"])
+    vb = np.array(g["vehicle_base"], np.int32)
+    mv = np.array(g["mission_vehicle"], np.int32)
+    bench._assert_golden("c2_full", st, vb, mv)  # the reference's own run passes
+    bad = types.SimpleNamespace(**{**vars(st), "evaluations": st.evaluations + 1})
+    with _pt.raises(SystemExit):
+        bench._assert_golden("c2_full", bad, vb, mv)
+    mv2 = mv.copy()
+    mv2[0] = (mv2[0] + 1) % 40
+    with _pt.raises(SystemExit):
+        bench._assert_golden("c2_full", st, vb, mv2)

@@ -61,6 +61,7 @@ struct Shared {
   unsigned hdone;                       // helper completions expected so far
   unsigned lt, lsync, ldone0;           // substitution log: published, applied, base
   int hp2_from;                         // hP2 holds the last candidate chain from this chunk (-1: none)
+  int reassigned;                       // process_pair applied a reassignment (its last move kind)
   long long red_l[33];
   int red_i[2][33];
   int red2[2][32][2];                   // row-run minima, double-buffered
@@ -1688,6 +1689,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
               sh.c.total_ver = (long long)sh.c.applied;
             }
             if (tabu) s.exp_reas[g] = exp;
+            sh.reassigned = 1;
             if (debug) debug_check(s, sh);
           }
           __syncthreads();
@@ -1952,10 +1954,24 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
       return;
     }
     const long long c2 = ph_now();
+    if (threadIdx.x == 0) sh.reassigned = 0;
     process_pair<NT, HELP>(s, sh, sm, i, p, tabu, tenure, debug);
     PH_ADD(sh, 3, c2);
     if (sh.c.error) return;
     p += 1;
+    if (tabu && tenure > 1 && sh.reassigned && p < M) {
+      // the reassignment just inserted {Reassign, id(vehicle(i))} with the
+      // Outer role and expiry tick + tenure: the row's next pair checks that
+      // key, finds it live (tenure > 1) and ends the row there -- one tick,
+      // one outer skip (proj/src/search.cpp:312-330), no context or scan
+      if (threadIdx.x == 0) {
+        sh.c.skips_outer += 1;
+        sh.c.tick += 1;
+        sh.c.pass_skipped = 1;
+      }
+      __syncthreads();
+      return;
+    }
   }
 }
 

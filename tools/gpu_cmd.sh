@@ -1,2 +1,4 @@
 mkdir -p gpurun_out
-python tools/profile_case.py --passes 196 > gpurun_out/plain_pass195.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:pass_kernel -s 194 -c 1 -o gpurun_out/r2_pass195 python tools/profile_case.py --passes 196 > gpurun_out/ncu_pass195.log 2>&1; echo ncu_rc=$?
+timeout 600 python tools/c2_pass_profile.py > gpurun_out/c2_pass_profile.log 2>&1; echo rc=$?; cat gpurun_out/c2_pass_profile.log
+timeout 1500 python -m pytest -m gpu -q -rf -x --timeout 300 tests > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?; tail -3 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?; tail -2 gpurun_out/bench.err

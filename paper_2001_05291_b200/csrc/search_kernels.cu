@@ -53,6 +53,8 @@ struct Shared {
   int nj;                               // live j-keys in sm.jl_*
   int nrl;                              // vehicles whose relocation class is not POS (sm.rlist)
   long long jexp_max;                   // latest expiry of any vehicle's {Relocate, id} key
+  long long jkey_ver;                   // {Relocate, id} inserts so far in this launch
+  long long jl_ver;                     // jkey_ver when the j-key list was built (-1: never)
   int tmp;
   double bd0;
   double xs;                            // exact chain: partial sum so far ...
@@ -83,7 +85,7 @@ struct Smem {
   int* impc;           // [V] set bits of imp[g] (0 = no reassign/takeover to g improves)
   int* rlist;          // [V] vehicles whose relocation to the row's empty base may improve
   int* jl_v;           // [V] vehicles whose {Relocate, id} j-key is live
-  int* jl_lim;         // [V] its live window (positions from the segment start)
+  long long* jl_exp;   // [V] its expiry stamp (live iff tick < stamp)
   uint8_t* jl_outer;   // [V] its role is Outer
   const int32_t* pb;   // perm_b
   int* paw;            // [2*NT] window of perm_a (row runs)
@@ -1659,6 +1661,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
             s.exp_rel[ki] = exp;
             s.role_rel[ki] = ROLE_INNER;
             sh.jexp_max = max(sh.jexp_max, exp);
+            sh.jkey_ver += 1;
           }
           if (debug) debug_check(s, sh);
         }
@@ -1713,12 +1716,14 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
 // relocates; those phases publish through shared memory).
 struct RowCtx {
   int gain_r, gain_t, rel_t, lim_ro, lim_ra, nj, nrl;
+  long long T;  // the tick at the segment start
 };
 
 template <int NT, bool HELP>
 __device__ RowCtx make_context(const Scenario& s, Shared& sh, const Smem& sm, int i, bool tabu) {
   RowCtx c;
   const long long T = sh.c.tick;
+  c.T = T;
   const int g = s.mv[i];
   c.gain_r = g;
   c.gain_t = -1;
@@ -1755,31 +1760,34 @@ __device__ RowCtx make_context(const Scenario& s, Shared& sh, const Smem& sm, in
   __syncwarp();
   if (threadIdx.x == 0) sh.c.counts[2] += 1;
   if (tabu && sh.jexp_max > T) {
-    for (int v = threadIdx.x; v < s.V; v += NT) {
-      const int k = s.vrk[v];
-      sm.lim_j[v] = clamp_lim(s.exp_rel[k] - T, s.M);
-      sm.outer_j[v] = s.role_rel[k] == ROLE_OUTER;
-    }
-    __syncthreads();
-    // compact the vehicles whose j-key is live (usually none or a few)
-    if (threadIdx.x < 32) {
-      const int l = threadIdx.x;
-      int n = 0;
-      for (int v0 = 0; v0 < s.V; v0 += 32) {
-        const int v = v0 + l;
-        const bool live = v < s.V && sm.lim_j[v] > 0;
-        const unsigned m = __ballot_sync(FULL, live);
-        if (live) {
-          const int k = n + __popc(m & ((1u << l) - 1u));
-          sm.jl_v[k] = v;
-          sm.jl_lim[k] = sm.lim_j[v];
-          sm.jl_outer[k] = sm.outer_j[v];
+    // the vehicles whose {Relocate, id} j-key is live (usually none or a
+    // few) with their expiry stamps; rebuilt only after a new insert (a key
+    // that has expired since only masks nothing: its window is empty)
+    if (sh.jl_ver != sh.jkey_ver) {
+      if (threadIdx.x < 32) {
+        const int l = threadIdx.x;
+        int n = 0;
+        for (int v0 = 0; v0 < s.V; v0 += 32) {
+          const int v = v0 + l;
+          const int k = v < s.V ? s.vrk[v] : 0;
+          const long long e = v < s.V ? s.exp_rel[k] : LLONG_MIN;
+          const bool live = v < s.V && e > T;
+          const unsigned m = __ballot_sync(FULL, live);
+          if (live) {
+            const int kk = n + __popc(m & ((1u << l) - 1u));
+            sm.jl_v[kk] = v;
+            sm.jl_exp[kk] = e;
+            sm.jl_outer[kk] = s.role_rel[k] == ROLE_OUTER;
+          }
+          n += __popc(m);
         }
-        n += __popc(m);
+        if (l == 0) {
+          sh.nj = n;
+          sh.jl_ver = sh.jkey_ver;
+        }
       }
-      if (l == 0) sh.nj = n;
+      __syncthreads();
     }
-    __syncthreads();
     c.nj = sh.nj;
   }
   if (c.rel_t >= 0) {
@@ -1866,7 +1874,8 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
           blk = prefix_bits(p_seg + lim_ra - base);
           for (int k = 0; k < nj; ++k) {
             const uint32_t m =
-                s.mem[(long long)sm.jl_v[k] * nwd + wd] & prefix_bits(p_seg + sm.jl_lim[k] - base);
+                s.mem[(long long)sm.jl_v[k] * nwd + wd] &
+                prefix_bits(p_seg + clamp_lim(sm.jl_exp[k] - cx.T, M) - base);
             blk |= m;
             if (sm.jl_outer[k]) outer |= m;
           }
@@ -1941,7 +1950,8 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
       outer_ev = off < lim_ro;
       if (!outer_ev && nj > 0) {
         const int v = s.mvp[p];
-        outer_ev = off < sm.lim_j[v] && sm.outer_j[v];
+        const int kk = s.vrk[v];
+        outer_ev = off < clamp_lim(s.exp_rel[kk] - cx.T, s.M) && s.role_rel[kk] == ROLE_OUTER;
       }
     }
     if (outer_ev) {
@@ -2120,7 +2130,7 @@ size_t pass_smem_core(int V, int NT) {
   const int NW = NT / 32;
   return align16(4ull * V) + align16(V) + align16(V) + 2 * align16(8ull * NW * V) +
          align16(8ull * NW * 32) + align16(8ull * NW * 3) + 3 * align16(4ull * V) + align16(V) +
-         align16(8ull * NT) + align16(8ull * NT) + align16(4ull * V) + 64;
+         align16(8ull * NT) + align16(8ull * NT) + 2 * align16(4ull * V) + 64;
 }
 size_t pass_smem_state(int V, int B, int K) {
   return align16(8ull * V) * 2 + align16(8ull * K) + align16(K) + align16(4ull * V) * 3 +
@@ -2176,7 +2186,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   sm.xlist = s.scratch;
   sm.xlist_cap = s.M;
   sm.jl_v = reinterpret_cast<int*>(take(4ull * V));
-  sm.jl_lim = reinterpret_cast<int*>(take(4ull * V));
+  sm.jl_exp = reinterpret_cast<long long*>(take(8ull * V));
   sm.jl_outer = take(V);
   sm.impc = reinterpret_cast<int*>(take(4ull * V));
   sm.rlist = reinterpret_cast<int*>(take(4ull * V));
@@ -2257,6 +2267,8 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
   if (threadIdx.x == 0) {
     sh.c = *s.ctr;
     sh.jexp_max = LLONG_MIN;
+    sh.jkey_ver = 0;
+    sh.jl_ver = -1;
     sh.hk = 0;
     sh.hdone = helpers > 0 ? s.hc->done : 0u;
     sh.lt = 0;

@@ -239,3 +239,31 @@ def test_batch_device_tables_with_mixed_base_counts():
         assert r.stats.final_objective_km == one.stats.final_objective_km
         assert np.array_equal(r.mission_vehicle, one.mission_vehicle)
         assert np.array_equal(r.vehicle_base, one.vehicle_base)
+
+
+def test_c5_share_512_scenarios_as_one_batch():
+    """The bench's c5 share -- instance seeds 1..512, tabu seed 7, to
+    quiescence -- as ONE batch (tables built inside the call) equals the
+    reference's recorded run of every scenario (tests/golden/c5_512.json,
+    tests/golden/make_c5_512.py)."""
+    gold = json.loads((Path(__file__).parent / "golden" / "c5_512.json").read_text())
+    insts, starts = [], []
+    for k in range(1, 513):
+        inst = F.survey_instance(200, 5000, 20, seed=k)
+        t = F.build_distance_table(inst)
+        start = F.rank_bases(inst, t)
+        insts.append(inst)
+        starts.append(F._state_arrays(start.assignment, F.initial_pool(start, inst), inst))
+        del t
+    res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu), None)
+    bad = []
+    for k, r in zip(range(1, 513), res):
+        g = gold[str(k)]
+        s = r.stats
+        got = [s.passes, s.evaluations, s.applied_moves, s.committed_moves, s.tabu_skips_outer,
+               s.tabu_skips_inner]
+        ref = struct.unpack(">d", bytes.fromhex(g["final_objective_bits"]))[0]
+        if got != g["stats"] or _sha(r.vehicle_base, r.mission_vehicle) != g["assignment_sha256"] \
+                or abs(s.final_objective_km - ref) > 1e-9 * ref:
+            bad.append((k, got, g["stats"]))
+    assert not bad, bad[:5]

@@ -2336,8 +2336,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
         for (int k = threadIdx.x; k < 2 * NT; k += NT) sm.paw[k] = pw + k < M ? pa[pw + k] : 0;
         __syncthreads();
       }
-      // Classify the next rows of the perm_a window (up to 2*NT; threads d and
-      // d + NT) at the current tick T:
+      // Classify the next NT rows at the current tick T (thread d: row r+d):
       //  S: no move from its outer index can improve any mission (imp rows
       //     empty, relocation classes all POS) -- tick independent;
       //  F: latest expiry of any key that could touch the row (row keys and
@@ -2346,11 +2345,9 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       // A row with S and F <= T is eventless at any later tick: all M pairs
       // are evaluated (M ticks, 3M evaluations). A row with T_d < E is
       // outer-blocked at its first pair (1 tick).
-      const int span = min(2 * NT, pw + 2 * NT - r);  // window rows from r (>= NT)
+      const int d = threadIdx.x, row = r + d;
       int first_nontrivial = INT_MAX, first_nonouter = INT_MAX;
-      auto classify = [&](int d) {
-        const int row = r + d;
-        if (d >= span || row >= M) return;
+      if (row < M) {
         const int i = sm.paw[row - pw];
         const int g0 = s.mv[i];
         bool st = sm.impc[g0] == 0;
@@ -2377,11 +2374,9 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
           const int k = s.vrk[s.mvp[0]];
           if (s.role_rel[k] == ROLE_OUTER) E = max(E, s.exp_rel[k]);
         }
-        if (!(st && F <= T)) first_nontrivial = min(first_nontrivial, d);
-        if (!(T + d < E)) first_nonouter = min(first_nonouter, d);
-      };
-      classify(threadIdx.x);
-      classify(threadIdx.x + NT);
+        if (!(st && F <= T)) first_nontrivial = d;
+        if (!(T + d < E)) first_nonouter = d;
+      }
       // both block minima with one barrier (double-buffered by parity; every
       // warp combines the per-warp values itself)
       {
@@ -2402,7 +2397,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       const int A = first_nontrivial;
       if (A > 0) {
         // a run of eventless rows
-        const int n = A == INT_MAX ? min(span, M - r) : A;
+        const int n = A == INT_MAX ? min(NT, M - r) : A;
         if (threadIdx.x == 0) {
           sh.c.evaluations += 3ull * (unsigned long long)M * (unsigned long long)n;
           if (tabu) sh.c.tick += (long long)M * n;
@@ -2415,7 +2410,7 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       }
       if (tabu) {
         // a run of rows outer-blocked at their first pair (one tick each)
-        const int nskip = first_nonouter == INT_MAX ? min(span, M - r) : first_nonouter;
+        const int nskip = first_nonouter == INT_MAX ? min(NT, M - r) : first_nonouter;
         if (threadIdx.x == 0 && nskip > 0) {
           sh.c.tick += nskip;
           sh.c.skips_outer += (unsigned long long)nskip;

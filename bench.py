@@ -386,11 +386,11 @@ def _kernel_rooflines(inst, t, start_ms, r, peak):
     nvw = (V + 31) // 32
     out["transpose_table_kernel (row-major table copy, second stream)"] = {
         "ms": start_ms["copy"] or tp, "bytes": 16 * B * M, "bound": "hbm"}
-    out["init_kernel (costs + exact total, one block)"] = {
-        "ms": ini, "bytes": 8 * M * 2 + 4 * M, "bound": "latency (one block per scenario)"}
+    out["mission_cost_kernel + init_kernel (costs grid-wide + exact total, one block)"] = {
+        "ms": ini, "bytes": 8 * M * 2 + 4 * M, "bound": "latency (the exact total: one block)"}
     out["impt_init_kernel (every reassignment scored: improvement rows)"] = {
         "ms": imp_rows, "bytes": 8 * V * M + 17 * M + 4 * nvw * M, "bound": "hbm"}
-    out["table_rows_kernel (relocation-delta rows of the empty bases)"] = {
+    out["rows_stream_kernel (relocation-delta rows of the empty bases)"] = {
         "ms": rel_rows, "bytes": 8 * P * M + 12 * M, "bound": "hbm"}
     if r.stats.sweep_ms > 0:
         # gathers of M natural-order rows + mirrors, writes of imp / mem / mirrors
@@ -594,7 +594,7 @@ def _c4_sweep_roofline(extra: dict, peak: float) -> dict:
     the relocation table: rows_stream_kernel), 8*B*M + 16*M algorithmic
     bytes -- against the measured HBM copy bandwidth."""
     k = extra.get("c4_1_pass", {}).get("kernels", {})
-    parts = [n for n in k if n.startswith("impt_init_kernel") or n.startswith("table_rows_kernel")]
+    parts = [n for n in k if n.startswith("impt_init_kernel") or n.startswith("rows_stream_kernel")]
     if len(parts) != 2:
         return {}
     ms = sum(k[n]["ms"] for n in parts)

@@ -866,12 +866,14 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   h2d(d_scs, run.scs.data(), n, st);
   std::vector<int32_t> active(n, 1);
   h2d(d_ctr, ctrs.data(), n, st);
-  if (ctx->perm_cap < chunk_ints) {
+  // pinned staging of host-generated permutations (device-drawn ones need none)
+  auto host_perm_buffers = [&]() {
+    if (ctx->perm_cap >= chunk_ints) return;
     for (auto& p : ctx->h_perm)
       if (p) cudaFreeHost(p), p = nullptr;
     for (auto& p : ctx->h_perm) check(cudaMallocHost(&p, sizeof(int32_t) * chunk_ints), "pinned");
     ctx->perm_cap = chunk_ints;
-  }
+  };
   double init_ms = 0.0, sweep_ms = 0.0, pass_ms = 0.0;
   uint64_t pass_launches = 0;
   cudaEvent_t ei[5];
@@ -928,6 +930,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   // every scenario wait for the slowest; single scenarios start small
   int threads = n == 1 ? 512 : 256;
   if (const char* e = std::getenv("FLEETPLACE_THREADS")) threads = std::atoi(e);
+  int threads_later = 0;
+  if (const char* e = std::getenv("FLEETPLACE_THREADS_LATER")) threads_later = std::atoi(e);
   // medium single scenarios (8k <= M < 32k, bitsets in shared memory): the
   // relocation-heavy first passes run with helper blocks (bitsets in global
   // memory, the relocations' O(M) work spread over the SMs), one pass per
@@ -958,7 +962,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   }
   int kchunk = next_chunk(0);
   int buf = 0;
-  if (!dev_perm) gen_chunk(ctx->h_perm[buf], kchunk);  // overlaps the init kernels
+  if (!dev_perm) {
+    host_perm_buffers();
+    gen_chunk(ctx->h_perm[buf], kchunk);  // overlaps the init kernels
+  }
   tr.mark("first permutation chunk");
   // large single scenarios share each relocation's O(M) work with helper
   // blocks (-1 = as many as fit; FLEETPLACE_HELPERS=0 disables)
@@ -1056,12 +1063,14 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
         rngs[d] = PermStream(seeds[d]);
         for (long long p = 0; p < 2 * launched; ++p) rngs[d].perm(M, skip.data());
       }
+      host_perm_buffers();
       gen_chunk(ctx->h_perm[buf], kchunk);
       tr.mark("device permutation chunk rejected: host stream");
       continue;
     }
     buf = nb;
     kchunk = knext;
+    if (threads_later > 0) threads = threads_later;
     if (adaptive && ctrs[0].pass_relocs < 2) adaptive = false;
     tr.mark("chunk synchronised");
     for (int s = 0; s < n; ++s) {

@@ -37,6 +37,9 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#ifdef FP_ROW_TRACE
+#include <cstdio>
+#endif
 
 namespace fpk {
 
@@ -347,8 +350,16 @@ __device__ void chain_steps(const Scenario& s, Shared& sh, int kind, int j, doub
         if (tie) first_tie = min(first_tie, k);
       }
     }
+    // saturate: only reaching LIM matters. A lane holds up to 32 terms of
+    // <= LIM each (2^58); clamping it before the warp sum keeps that sum
+    // <= 2^58 too -- unclamped, 1024 saturated terms (a chain whose first
+    // term is small against the next 1024) sum to 2^63 and wrap negative,
+    // hiding the binade crossing
+#ifndef FP_CHAIN_UNCLAMPED  // (probe builds: the round-2 bug, to show the test catches it)
+    local = min(local, LIM);
+#endif
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(FULL, local, o);
-    local = min(local, LIM);  // saturate: only reaching LIM matters
+    local = min(local, LIM);
     first_tie = __reduce_min_sync(FULL, first_tie);
     if (l == 0) sh.red_l[w] = local;
     __syncthreads();
@@ -1547,6 +1558,17 @@ __device__ bool exact_accept_single(const Scenario& s, Shared& sh, const Smem& s
   }
   PH_ADD(sh, 4, f0);
   __syncthreads();
+#ifdef FP_ROW_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0 && sh.c.passes == FP_ROW_TRACE) {
+    double q = 0.0, q2 = 0.0;
+    for (int k = 0; k < s.M; ++k) {
+      q += s.mc[k];
+      q2 += k == j ? newc : s.mc[k];
+    }
+    printf("RT exact j %d S %a S2 %a seqS %a seqS2 %a ver %lld ap %llu\n", j, S, S2, q, q2,
+           sh.c.total_ver, (unsigned long long)sh.c.applied);
+  }
+#endif
   return S2 < S;
 }
 
@@ -1965,7 +1987,21 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
     }
     const long long c2 = ph_now();
     if (threadIdx.x == 0) sh.reassigned = 0;
+#ifdef FP_ROW_TRACE
+    const unsigned long long tr_ap = sh.c.applied;
+    if (threadIdx.x == 0 && blockIdx.x == 0 && sh.c.passes == FP_ROW_TRACE) {
+      const int j = sm.pb[p], g = s.mv[i], l = s.mv[j];
+      printf("RT pre i %d p %d j %d g %d l %d vb %d newc %a mcj %a mcp %a mvp %d tu %a ps %d vf %d ro %d sb %a fe %d\n", i, p, j, g, l,
+             s.vbase[g], cost_mb(s, j, s.vbase[g]), s.mc[j], s.mcp[p], s.mvp[p], sh.c.total_up, sh.c.psize,
+             (int)s.vfixed[g], (int)s.ro[j], single_bound(s, sh), sh.c.force_exact);
+    }
+#endif
     process_pair<NT, HELP>(s, sh, sm, i, p, tabu, tenure, debug);
+#ifdef FP_ROW_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0 && sh.c.passes == FP_ROW_TRACE)
+      printf("RT pair i %d p %d j %d applied %d fb %llu ev %llu\n", i, p, s.mvp[p] , (int)(sh.c.applied - tr_ap),
+             (unsigned long long)sh.c.fallbacks, (unsigned long long)sh.c.evaluations);
+#endif
     PH_ADD(sh, 3, c2);
     if (sh.c.error) return;
     p += 1;
@@ -2142,7 +2178,7 @@ size_t pass_smem_state(int V, int B, int K) {
 // separate instantiation, so the grid-wide-sweep variant carries none of
 // that code's registers).
 template <int NT, bool INK, bool HELP>
-__global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (NT == 256 ? 2 : 4))
     pass_kernel(Scenario* scs, const int32_t* __restrict__ active, const int32_t* __restrict__ perms,
                 int kpasses, int inkernel_prep, int max_passes, int tabu_i, long long tenure,
                 int debug_i, int state_in_smem, int bits_in_smem, int mirrors_in_smem,
@@ -2404,6 +2440,10 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
           sh.c.counts[4] += (unsigned long long)n;
         }
         if (tabu) T += (long long)M * n;
+#ifdef FP_ROW_TRACE
+        if (threadIdx.x == 0 && blockIdx.x == 0 && sh.c.passes == FP_ROW_TRACE)
+          printf("RT run %d %d E\n", r, n);
+#endif
         r += n;
         PH_ADD(sh, 0, b0);
         continue;
@@ -2417,6 +2457,10 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
           sh.c.pass_skipped = 1;
         }
         T += nskip;
+#ifdef FP_ROW_TRACE
+        if (threadIdx.x == 0 && blockIdx.x == 0 && sh.c.passes == FP_ROW_TRACE && nskip > 0)
+          printf("RT run %d %d O\n", r, nskip);
+#endif
         r += nskip;
         PH_ADD(sh, 0, b0);
         if (nskip > 0) continue;
@@ -2424,6 +2468,13 @@ __global__ void __launch_bounds__(NT, NT == 1024 ? 1 : (NT == 512 ? 1 : 2))
       // (the reduction barrier above published thread 0's counter updates)
       run_row<NT, HELP>(s, sh, sm, sm.paw[r - pw], tabu, tenure, debug);
       __syncthreads();
+#ifdef FP_ROW_TRACE
+      if (threadIdx.x == 0 && blockIdx.x == 0 && sh.c.passes == FP_ROW_TRACE)
+        printf("RT row %d i %d ev %llu tick %lld so %llu si %llu ap %d\n", r, sm.paw[r - pw],
+               (unsigned long long)sh.c.evaluations, (long long)sh.c.tick,
+               (unsigned long long)sh.c.skips_outer, (unsigned long long)sh.c.skips_inner,
+               (int)sh.c.pass_applied);
+#endif
       T = sh.c.tick;
       r += 1;
     }
@@ -2737,8 +2788,10 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   const size_t state = pass_smem_state(V, B, K);
   const size_t bits = 2 * align16(4ull * V * ((M + 31) / 32));
   const size_t limit = 220 * 1024;
-  // 256-thread blocks run two per SM: the bitsets only join while two fit
-  const size_t bits_limit = NT == 256 ? 100 * 1024 : limit;
+  // 256-thread blocks run two per SM, 128-thread blocks four: the bitsets
+  // (and mission mirrors) only join while that many fit
+  size_t bits_limit = NT == 256 ? 100 * 1024 : (NT == 128 ? 54 * 1024 : limit);
+  if (const char* e = std::getenv("FLEETPLACE_SMEM_KB")) bits_limit = (size_t)std::atoi(e) * 1024;
   if (core > limit) return cudaErrorInvalidConfiguration;
   const int in_smem = core + state <= limit ? 1 : 0;
   int bits_smem = in_smem && core + state + bits <= bits_limit && !global_bits ? 1 : 0;
@@ -2813,6 +2866,10 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
     return launch_pass_nt<1024>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
                                 M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream,
                                 global_bits);
+  if (threads == 128)
+    return launch_pass_nt<128>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
+                               M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream,
+                               global_bits);
   if (threads == 512)
     return launch_pass_nt<512>(d_scs, d_active, n_scn, d_perms, kpasses, inkernel, max_passes,
                                M, tabu, tenure, debug, V, B, K, helpers_req, epoch, perm_bad, stream,

@@ -241,20 +241,32 @@ def test_batch_device_tables_with_mixed_base_counts():
         assert np.array_equal(r.vehicle_base, one.vehicle_base)
 
 
-def test_c5_share_512_scenarios_as_one_batch():
+_C5_SHARE = []
+
+
+def _c5_share():
+    if not _C5_SHARE:
+        for k in range(1, 513):
+            inst = F.survey_instance(200, 5000, 20, seed=k)
+            t = F.build_distance_table(inst)
+            start = F.rank_bases(inst, t)
+            _C5_SHARE.append((inst, F._state_arrays(start.assignment, F.initial_pool(start, inst), inst)))
+            del t
+    return [x[0] for x in _C5_SHARE], [x[1] for x in _C5_SHARE]
+
+
+@pytest.mark.parametrize("threads", [None, "128", "512"])
+def test_c5_share_512_scenarios_as_one_batch(monkeypatch, threads):
     """The bench's c5 share -- instance seeds 1..512, tabu seed 7, to
     quiescence -- as ONE batch (tables built inside the call) equals the
     reference's recorded run of every scenario (tests/golden/c5_512.json,
-    tests/golden/make_c5_512.py)."""
+    tests/golden/make_c5_512.py); also with 128-thread blocks (four per SM:
+    every block-wide step covers fewer threads than the default's, e.g. a
+    warp's share of an exact-chain step reaches 1024 terms) and 512."""
+    if threads:
+        monkeypatch.setenv("FLEETPLACE_THREADS", threads)
     gold = json.loads((Path(__file__).parent / "golden" / "c5_512.json").read_text())
-    insts, starts = [], []
-    for k in range(1, 513):
-        inst = F.survey_instance(200, 5000, 20, seed=k)
-        t = F.build_distance_table(inst)
-        start = F.rank_bases(inst, t)
-        insts.append(inst)
-        starts.append(F._state_arrays(start.assignment, F.initial_pool(start, inst), inst))
-        del t
+    insts, starts = _c5_share()
     res = F.search_batch(insts, starts, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu), None)
     bad = []
     for k, r in zip(range(1, 513), res):

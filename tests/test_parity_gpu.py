@@ -151,6 +151,45 @@ def test_forced_exact_decisions(monkeypatch, case):
         _check_search(ref_survey_instance(200, 5000, 20, seed=1), 1, seeds=[7], max_passes=1)
 
 
+def _cheapest_mission_first(inst):
+    """The instance with its missions reordered so that the one cheapest at
+    the ranked start comes first. Every exact chain then starts from a sum
+    below each of the next terms: all of them round to >= 2^53 units of the
+    first binade, so a warp's 1024 terms sum to 2^63 -- the int64 wrap that
+    hid the binade crossing in exact_chain (a 128-thread batch miscounted c5
+    scenario 78 from pass 98; any warp covering 1024 terms could)."""
+    from paper_2001_05291_b200.fleetplace import Instance
+    cost = ref_table(inst)
+    r = ref_rank(inst, cost)
+    M = inst.n_missions
+    mc = cost[r.vehicle_base[r.mission_vehicle].astype(np.int64) * M + np.arange(M)]
+    first = int(np.argmin(mc))
+    order = np.r_[first, np.delete(np.arange(M), first)]
+    out = Instance.from_arrays(inst.base_id, inst.base_kind, inst.base_lat, inst.base_lon,
+                               inst.vehicle_id, inst.vehicle_kind, inst.mission_id[order],
+                               inst.pickup_lat[order], inst.pickup_lon[order],
+                               inst.delivery_lat[order], inst.delivery_lon[order],
+                               inst.rotary_only[order])
+    cost2 = ref_table(out)
+    r2 = ref_rank(out, cost2)
+    mc2 = cost2[r2.vehicle_base[r2.mission_vehicle].astype(np.int64) * M + np.arange(M)]
+    assert 0 < mc2[0] and np.all(mc2[1:1025] >= mc2[0])  # the precondition of the case
+    return out
+
+
+@pytest.mark.parametrize("threads", ["128", "256"])
+def test_forced_exact_chain_small_first_term(monkeypatch, threads):
+    """Every decision through exact_chain on a chain whose first term is the
+    smallest: 8200 missions make each warp's share of a block step 1024 terms
+    at 128 and 256 threads. The trajectory must equal the reference's."""
+    monkeypatch.setenv("FLEETPLACE_FORCE_EXACT", "1")
+    monkeypatch.setenv("FLEETPLACE_THREADS", threads)
+    monkeypatch.setenv("FLEETPLACE_HELPERS", "0")
+    monkeypatch.setenv("FLEETPLACE_ADAPTIVE_HELPERS", "0")
+    inst = _cheapest_mission_first(ref_survey_instance(100, 8200, 20, seed=5))
+    _check_search(inst, 1, seeds=[7], max_passes=1)
+
+
 def test_forced_exact_totals_with_helper_chains(monkeypatch):
     """M = 40k with helper blocks: every total comparison goes through the
     helper-assisted exact chains (chunk sums in the predicted binade, walked

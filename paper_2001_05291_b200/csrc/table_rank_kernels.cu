@@ -242,6 +242,75 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// Packed variant (U < 2^16, M even): a mission's (pickup, delivery) ids are
+// one 32-bit word, so a warp's index loads are half the bytes and each lane
+// serves two consecutive missions per step: one 8-byte index load, four
+// shared-memory gathers, one 16-byte streaming store (a warp step covers 64
+// missions per column, 512 contiguous bytes per store instruction); four
+// steps' indices are in flight per thread. The columns are streamed past L2
+// (st.global.cs) so the index words and H rows stay resident.
+template <int R>
+__global__ void __launch_bounds__(1024)
+    table_gather_packed_kernel(const double* __restrict__ H, int U, int B,
+                               const uint2* __restrict__ pd2, int M, int chunk,
+                               double* __restrict__ cost) {
+  extern __shared__ double hs[];
+  const int b0 = blockIdx.x * R;
+  const int nb = min(R, B - b0);
+  const double* h = H + (long long)b0 * U;
+  {
+    const int n = nb * U, bd = blockDim.x;
+    int k = threadIdx.x;
+    for (; k + 7 * bd < n; k += 8 * bd) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = h[k + u * bd];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) hs[k + u * bd] = v[u];
+    }
+    for (; k < n; k += bd) hs[k] = h[k];
+  }
+  __syncthreads();
+  // in mission pairs: [q0, q1) of M/2
+  const int q0 = blockIdx.y * chunk, q1 = min(M / 2, q0 + chunk);
+  constexpr int UN = 4;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int qb = q0 + w * 32 * UN; qb < q1; qb += nw * 32 * UN) {
+    uint2 p[UN];
+#pragma unroll
+    for (int u = 0; u < UN; ++u) {
+      const int q = qb + u * 32 + l;
+      p[u] = q < q1 ? __ldg(pd2 + q) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r < nb) {
+        double2* col = reinterpret_cast<double2*>(cost + (long long)(b0 + r) * M);
+        const double* hr = hs + r * U;
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          const int q = qb + u * 32 + l;
+          if (q < q1) {
+            double2 v;
+            v.x = __dadd_rn(hr[p[u].x & 0xffffu], hr[p[u].x >> 16]);
+            v.y = __dadd_rn(hr[p[u].y & 0xffffu], hr[p[u].y >> 16]);
+            __stcs(col + q, v);
+          }
+        }
+      }
+    }
+  }
+}
+
+// (pickup, delivery) int pairs -> one packed 16-bit pair word per mission
+__global__ void pack_pairs_kernel(const int2* __restrict__ pd, int M, uint32_t* __restrict__ out) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < M) {
+    const int2 v = pd[m];
+    out[m] = (uint32_t)v.x | ((uint32_t)v.y << 16);
+  }
+}
+
 // The same with the H row read through L1 / L2 (rows too long for smem).
 __global__ void __launch_bounds__(1024)
     table_gather_kernel(const double* __restrict__ H, int U, const int2* __restrict__ pd, int M,
@@ -471,7 +540,26 @@ cudaError_t launch_table_auto(const double* blat, const double* blon, const doub
     kern<<<dim3((B + r - 1) / r, (M + chunk - 1) / chunk), 1024, row * r, st>>>(
         H, U, B, (const int2*)pid, M, chunk, cost);
   };
-  if (R == 8) go(table_gather_smem_kernel<8>, 8);
+  // packed indices: U < 2^16 and an even M (16-byte aligned mission pairs;
+  // the table allocation is 256-byte aligned)
+  bool packed = R > 0 && U < (1 << 16) && M % 2 == 0 &&
+                (reinterpret_cast<uintptr_t>(cost) & 15) == 0;
+  if (const char* e = std::getenv("FLEETPLACE_TABLE_PACKED")) packed = packed && std::atoi(e) != 0;
+  if (packed) {
+    // the packed words reuse the flag/uid scratch (free once pid is built)
+    auto* pd16 = reinterpret_cast<uint32_t*>(flag);
+    pack_pairs_kernel<<<(M + 255) / 256, 256, 0, st>>>((const int2*)pid, M, pd16);
+    const int qchunk = (chunk + 1) / 2;
+    auto gp = [&](auto kern, int r) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(row * r));
+      kern<<<dim3((B + r - 1) / r, (M / 2 + qchunk - 1) / qchunk), 1024, row * r, st>>>(
+          H, U, B, reinterpret_cast<const uint2*>(pd16), M, qchunk, cost);
+    };
+    if (R == 8) gp(table_gather_packed_kernel<8>, 8);
+    else if (R == 4) gp(table_gather_packed_kernel<4>, 4);
+    else if (R == 2) gp(table_gather_packed_kernel<2>, 2);
+    else gp(table_gather_packed_kernel<1>, 1);
+  } else if (R == 8) go(table_gather_smem_kernel<8>, 8);
   else if (R == 4) go(table_gather_smem_kernel<4>, 4);
   else if (R == 2) go(table_gather_smem_kernel<2>, 2);
   else if (R == 1) go(table_gather_smem_kernel<1>, 1);

@@ -422,11 +422,15 @@ def _table_bytes(inst):
     return np.ascontiguousarray(t.cost.T).tobytes()
 
 
-@pytest.mark.parametrize("shape", [(50, 200, 10), (500, 10000, 40), (2000, 40000, 100)])
-def test_table_distinct_point_path_bit_identical(shape, monkeypatch):
+@pytest.mark.parametrize("packed", ["0", "1"])
+@pytest.mark.parametrize("shape", [(50, 200, 10), (500, 10000, 40), (2000, 40000, 100),
+                                   (2001, 40001, 100), (7, 4096, 3)])
+def test_table_distinct_point_path_bit_identical(shape, packed, monkeypatch):
     """Kernel (1) through the distinct mission points (H(b, u) once per base
     and distinct point, then a gather + add per entry) equals the direct
-    per-entry kernel bit for bit."""
+    per-entry kernel bit for bit -- with the packed 16-bit index pairs (even
+    M) and without (odd M always takes the int-pair gather)."""
+    monkeypatch.setenv("FLEETPLACE_TABLE_PACKED", packed)
     inst = F.survey_instance(*shape, seed=2)
     monkeypatch.setenv("FLEETPLACE_TABLE_SITES", "0")
     direct = _table_bytes(inst)

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity_gpu.py -q -x -k "small_first_term" -p no:cacheprovider > gpurun_out/unclamped.log 2>&1; echo rc=$?; tail -5 gpurun_out/unclamped.log
+bash tools/gpu_tests.sh 2400
+timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?; tail -c 600 gpurun_out/bench.json

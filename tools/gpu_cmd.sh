@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-bash tools/gpu_tests.sh 2400
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?; tail -c 600 gpurun_out/bench.json
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:table_gather_packed -c 1 -o gpurun_out/r2_table_gather_packed python tools/table_probe.py 5000,1000000,250 > gpurun_out/ncu_tg.log 2>&1; echo rc=$?; tail -3 gpurun_out/ncu_tg.log

@@ -56,6 +56,10 @@ struct fp_ctx {
   size_t h_stage_cap = 0;
   double* h_pts = nullptr;
   size_t h_pts_cap = 0;
+  // pinned per-chunk control words of a search (counters, active flags, the
+  // rejected-draw flag): pageable copies would stage through the driver
+  unsigned char* h_small = nullptr;
+  size_t h_small_cap = 0;
   uint64_t launches = 0;
   double last_kernel_ms = 0.0;
   // pinned staging for permutations (double-buffered)
@@ -155,6 +159,23 @@ void h2d(T* d, const T* h, size_t n, cudaStream_t st) {
 template <typename T>
 void d2h(T* h, const T* d, size_t n, cudaStream_t st) {
   if (n) check(cudaMemcpyAsync(h, d, sizeof(T) * n, cudaMemcpyDeviceToHost, st), "D2H");
+}
+
+// Waits for the stream. blocking: the thread sleeps on a blocking-sync event
+// instead of spinning -- for the long waits of batch launches (hundreds of
+// ms), where a spinning thread burns the process's CPU quota and a quota-
+// throttled process wakes tens of ms late; short waits spin (lower latency).
+void wait_stream(cudaStream_t st, bool blocking, const char* what) {
+  if (!blocking) {
+    check(cudaStreamSynchronize(st), what);
+    return;
+  }
+  cudaEvent_t e;
+  check(cudaEventCreateWithFlags(&e, cudaEventBlockingSync | cudaEventDisableTiming), what);
+  cudaError_t r = cudaEventRecord(e, st);
+  if (r == cudaSuccess) r = cudaEventSynchronize(e);
+  cudaEventDestroy(e);
+  check(r, what);
 }
 
 void ensure_table(const fp_ctx* ctx, int M, int B) {
@@ -722,7 +743,17 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   fpk::MtState* const d_mt = reinterpret_cast<fpk::MtState*>(d0 + o_mt);
   int* const d_pbad = reinterpret_cast<int*>(d0 + o_pbad);
   unsigned long long* const d_draws = reinterpret_cast<unsigned long long*>(d0 + o_draws);
-  std::vector<fpk::Counters> ctrs(n);
+  const size_t small_bytes = sizeof(fpk::Counters) * n + 4ull * n + 64;
+  if (ctx->h_small_cap < small_bytes) {
+    if (ctx->h_small) cudaFreeHost(ctx->h_small);
+    ctx->h_small = nullptr;
+    ctx->h_small_cap = 0;
+    check(cudaMallocHost(&ctx->h_small, small_bytes), "pinned control words");
+    ctx->h_small_cap = small_bytes;
+  }
+  fpk::Counters* const ctrs = reinterpret_cast<fpk::Counters*>(ctx->h_small);
+  int32_t* const active = reinterpret_cast<int32_t*>(ctx->h_small + sizeof(fpk::Counters) * n);
+  int* const pbad_h = reinterpret_cast<int*>(ctx->h_small + sizeof(fpk::Counters) * n + 4ull * n);
   for (int s = 0; s < n; ++s) {
     ctrs[s] = fpk::Counters{};
     ctrs[s].psize = run.hs[s].psize;
@@ -864,8 +895,8 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   check(cudaEventRecord(ev0, st), "event");
   h2d(d0, stage, totalA, st);
   h2d(d_scs, run.scs.data(), n, st);
-  std::vector<int32_t> active(n, 1);
-  h2d(d_ctr, ctrs.data(), n, st);
+  for (int s = 0; s < n; ++s) active[s] = 1;
+  h2d(d_ctr, ctrs, n, st);
   // pinned staging of host-generated permutations (device-drawn ones need none)
   auto host_perm_buffers = [&]() {
     if (ctx->perm_cap >= chunk_ints) return;
@@ -978,10 +1009,26 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   unsigned epoch = 0;
   int n_active = n;
   while (n_active > 0) {
-    h2d(d_active, active.data(), n, st);
+    h2d(d_active, active, n, st);
     if (dev_perm) {
+      cudaEvent_t q0 = nullptr, q1 = nullptr;
+      if (tr.on) {
+        cudaEventCreate(&q0);
+        cudaEventCreate(&q1);
+        cudaEventRecord(q0, st);
+      }
       check(fpk::launch_permutations(d_mt, D, M, 2 * kchunk, d_draws, d_perm, d_pbad, st),
             "permutations");
+      if (tr.on) {
+        cudaEventRecord(q1, st);
+        cudaEventSynchronize(q1);
+        float a = 0.f, b = 0.f;
+        cudaEventElapsedTime(&a, ev0, q0);
+        cudaEventElapsedTime(&b, q0, q1);
+        std::fprintf(stderr, "[fleetplace trace] device: start->perms %.3f ms, perms %.3f ms (%d passes)\n", a, b, kchunk);
+        cudaEventDestroy(q0);
+        cudaEventDestroy(q1);
+      }
       ctx->launches += 2;
       if (force_bad) check(cudaMemsetAsync(d_pbad, 1, 1, st), "memset");
     } else {
@@ -1031,10 +1078,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     const int knext = next_chunk(kchunk);
     const int nb = buf ^ 1;
     if (!dev_perm) gen_chunk(ctx->h_perm[nb], knext);
-    d2h(ctrs.data(), d_ctr, n, st);
-    int pbad = 0;
-    if (dev_perm) d2h(&pbad, d_pbad, 1, st);
-    check(cudaStreamSynchronize(st), "pass sync");
+    d2h(ctrs, d_ctr, n, st);
+    *pbad_h = 0;
+    if (dev_perm) d2h(pbad_h, d_pbad, 1, st);
+    wait_stream(st, inkernel, "pass sync");
     for (size_t e = 0; e + 1 < pass_ev.size(); e += 2) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, pass_ev[e], pass_ev[e + 1]);
@@ -1052,7 +1099,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       cudaEventDestroy(sweep_ev[e + 1]);
     }
     sweep_ev.clear();
-    if (pbad) {
+    if (*pbad_h) {
       // a rejected draw (or the test hook): the pass kernel did not run this
       // chunk; regenerate the stream exactly on the host and redo the chunk
       dev_perm = false;
@@ -1084,13 +1131,13 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   check(fpk::launch_final(d_scs, n, st), "final_kernel");
   ctx->launches += 1;
   check(cudaEventRecord(ev1, st), "event");
-  d2h(ctrs.data(), d_ctr, n, st);
+  d2h(ctrs, d_ctr, n, st);
   if (n < 64) {
     for (int s = 0; s < n; ++s) {
       d2h(outs[s].vehicle_base, run.scs[s].vbase, insts[s].n_vehicles, st);
       d2h(outs[s].mission_vehicle, run.scs[s].mv, (size_t)M, st);
     }
-    check(cudaStreamSynchronize(st), "final sync");
+    wait_stream(st, inkernel, "final sync");
   } else {
     // large batches: every scenario's result gathered on the device, one copy
     // into the pinned stage (region A, already consumed), spread on threads
@@ -1106,7 +1153,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
     ctx->launches += 1;
     int32_t* h_res = reinterpret_cast<int32_t*>(stage);  // totalA >= 4 * nres
     d2h(h_res, d_mv, nres, st);
-    check(cudaStreamSynchronize(st), "final sync");
+    wait_stream(st, inkernel, "final sync");
     parallel_for(n, [&](int s) {
       std::memcpy(outs[s].mission_vehicle, h_res + (size_t)s * M, 4ull * M);
       std::memcpy(outs[s].vehicle_base, h_res + (size_t)n * M + vbo[s], 4ull * insts[s].n_vehicles);
@@ -1172,6 +1219,7 @@ fp_status fp_ctx_create(int32_t device, fp_ctx** out) {
       throw FpError(FP_ERR_CUDA, "no CUDA device available (fleetplace_b200 has no CPU path)");
     if (device < 0 || device >= n) throw FpError(FP_ERR_INVALID_ARGUMENT, "bad device ordinal");
     check(cudaSetDevice(device), "cudaSetDevice");
+    fpk::keep_pool_mapped(device);
     auto* c = new fp_ctx();
     c->device = device;
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
@@ -1194,6 +1242,7 @@ void fp_ctx_destroy(fp_ctx* ctx) {
   if (ctx->d_flag) cudaFree(ctx->d_flag);
   if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->h_pts) cudaFreeHost(ctx->h_pts);
+  if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->table_ready) cudaEventDestroy(ctx->table_ready);
   if (ctx->costT_ready) cudaEventDestroy(ctx->costT_ready);

@@ -25,6 +25,7 @@ struct TableJob;
 cudaError_t launch_table_batch(const TableJob* d_jobs, int n_jobs, int M, int max_B,
                                double radius_km, cudaStream_t st);
 
+void keep_pool_mapped(int dev);
 cudaError_t launch_point_cos(const double* lat, int n, double* out, cudaStream_t st);
 cudaError_t launch_transpose(const double* src, int M, int B, double* dst, cudaStream_t stream);
 cudaError_t launch_table(const double* blat, const double* blon, const double* bcos, int B,

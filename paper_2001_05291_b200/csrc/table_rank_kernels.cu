@@ -415,6 +415,23 @@ __global__ void candidate_delta_kernel(const double* __restrict__ cost, int M,
 
 // ---- launchers ------------------------------------------------------------
 
+// Freed stream-ordered allocations (cudaFreeAsync) stay mapped in the
+// device's default pool up to 16 GB instead of going back to the OS at the
+// next synchronisation: unmapping a few GB there stalled that sync by
+// hundreds of ms, and the next call paid the mapping again (a c5 batch's
+// 4 GB of scenario tables per call). Raises the threshold, never lowers it.
+void keep_pool_mapped(int dev) {
+  static bool done[64] = {};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long cur = 0, keep = 16ull << 30;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur);
+    if (cur < keep) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 cudaError_t launch_point_cos(const double* lat, int n, double* out, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int blocks = min(1184, (n + 255) / 256);
@@ -451,19 +468,9 @@ cudaError_t launch_table_auto(const double* blat, const double* blon, const doub
     return launch_table(blat, blon, bcos, B, plat, plon, pcos, dlat, dlon, dcos, M, radius_km, cost, st);
   const int n = 2 * M;
   {
-    // keep freed stream-ordered allocations mapped (H is up to 4 GB): repeated
-    // builds must not pay the physical mapping again
-    static bool pool_set[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !pool_set[dev]) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        unsigned long long keep = 6ull << 30;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
-      pool_set[dev] = true;
-    }
+    keep_pool_mapped(dev);  // H is up to 4 GB: repeated builds reuse its mapping
   }
   // workspace: keys x4, idx x4, flag, uid, pid, ulat, ulon, ucos, + cub temp
   size_t t_sort = 0, t_scan = 0;

@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python tools/c4_rank_probe.py > gpurun_out/c4_rank.log 2>&1; echo rc=$?; cat gpurun_out/c4_rank.log
+FLEETPLACE_TRACE=1 timeout 600 python tools/c5_outlier_probe.py 14 > gpurun_out/c5_outlier.log 2>&1; echo rc=$?; grep "call " gpurun_out/c5_outlier.log
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw,temperature.gpu --format=csv

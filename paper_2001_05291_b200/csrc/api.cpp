@@ -8,6 +8,7 @@
 // that touches the M x B table runs on the device.
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -202,8 +203,76 @@ void table_alloc(fp_ctx* ctx, int M, int B) {
   ctx->table_ok = false;
 }
 
+// fn(0..n-1) on up to 16 host threads (per-scenario host work of batches);
+// the first exception is rethrown.
+template <typename Fn>
+void parallel_for(int n, Fn&& fn) {
+  const int T = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u);
+  if (n < 64 || T == 1) {
+    for (int i = 0; i < n; ++i) fn(i);
+    return;
+  }
+  std::vector<std::thread> ws;
+  std::vector<std::exception_ptr> errs(T);
+  for (int t = 0; t < T; ++t)
+    ws.emplace_back([&, t] {
+      try {
+        for (int i = (int)((long long)n * t / T); i < (int)((long long)n * (t + 1) / T); ++i) fn(i);
+      } catch (...) {
+        errs[t] = std::current_exception();
+      }
+    });
+  for (auto& w : ws) w.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
 bool valid_point(double lat, double lon) {
   return lat >= -90.0 && lat <= 90.0 && lon >= -180.0 && lon <= 180.0;
+}
+
+// The missions' checks of validate_instance on host threads: ids unique
+// (a bitmap over a compact id range, set with atomic ors) and coordinates in
+// range (branch-free, vectorised). true = every mission passes; false =
+// some mission fails, or the ids are not compact -- the sequential scan then
+// runs and reports the first failure in load order. c4 (1M missions):
+// ~8 ms sequential.
+bool missions_ok_fast(const fp_instance* in) {
+  const int M = in->n_missions;
+  if (M < (1 << 16)) return false;  // small: the sequential scan is cheap
+  constexpr int kParts = 64;
+  int los[kParts], his[kParts];
+  parallel_for(kParts, [&](int t) {
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int m = (int)((long long)M * t / kParts); m < (int)((long long)M * (t + 1) / kParts); ++m) {
+      lo = std::min(lo, in->mission_id[m]);
+      hi = std::max(hi, in->mission_id[m]);
+    }
+    los[t] = lo;
+    his[t] = hi;
+  });
+  const int lo = *std::min_element(los, los + kParts), hi = *std::max_element(his, his + kParts);
+  const int64_t span = (int64_t)hi - lo + 1;
+  if (span > 8 * (int64_t)M + 4096) return false;
+  std::vector<uint64_t> bits((size_t)((span + 63) / 64), 0);
+  std::atomic<int> bad{0};
+  parallel_for(kParts, [&](int t) {
+    int ok = 1;
+    const int m0 = (int)((long long)M * t / kParts), m1 = (int)((long long)M * (t + 1) / kParts);
+    for (int m = m0; m < m1; ++m) {
+      const double a = in->pickup_lat[m], b = in->pickup_lon[m];
+      const double c = in->delivery_lat[m], d = in->delivery_lon[m];
+      ok &= (a >= -90.0) & (a <= 90.0) & (b >= -180.0) & (b <= 180.0) & (c >= -90.0) &
+            (c <= 90.0) & (d >= -180.0) & (d <= 180.0);
+    }
+    for (int m = m0; m < m1 && ok; ++m) {
+      const uint64_t k = (uint64_t)((int64_t)in->mission_id[m] - lo);
+      const uint64_t bit = 1ull << (k & 63);
+      if (__atomic_fetch_or(&bits[k >> 6], bit, __ATOMIC_RELAXED) & bit) ok = 0;
+    }
+    if (!ok) bad.store(1, std::memory_order_relaxed);
+  });
+  return bad.load() == 0;
 }
 
 // validate_instance, proj/src/model.cpp:46-74 (same checks, same order).
@@ -230,9 +299,10 @@ void validate(const fp_instance* in) {
         throw FpError(FP_ERR_VALIDATION, "validation failed for vehicle " +
                                              std::to_string(in->vehicle_id[v]) + ": duplicate id");
   }
-  {
-    // first repeated id in load order: a bitmap over the id range when it is
-    // compact (generated ids are dense, proj/src/data.cpp:156-174), else a map
+  if (!missions_ok_fast(in)) {
+    // the first failing mission in load order (the reference's error): a
+    // bitmap over the id range when it is compact (generated ids are dense,
+    // proj/src/data.cpp:156-174), else a map
     const int M = in->n_missions;
     int lo = INT_MAX, hi = INT_MIN;
     for (int m = 0; m < M; ++m) {
@@ -303,6 +373,17 @@ bool table_entries_ok(fp_ctx* ctx, const double* d_t, size_t n, cudaStream_t st)
   return h == 0;
 }
 
+// ctx->h_pts holds at least n doubles (pinned, grow-only; its previous
+// contents are not kept: every user syncs before returning)
+void pinned_points(fp_ctx* ctx, size_t n) {
+  if (ctx->h_pts_cap >= n) return;
+  if (ctx->h_pts) cudaFreeHost(ctx->h_pts);
+  ctx->h_pts = nullptr;
+  ctx->h_pts_cap = 0;
+  check(cudaMallocHost(&ctx->h_pts, sizeof(double) * n), "pinned points");
+  ctx->h_pts_cap = n;
+}
+
 // kernel (1) (build_distance_table, proj/src/model.cpp:76-90) into `dst`
 // (M x B column-major) on the context's stream; ctx's resident table is
 // untouched unless dst is it.
@@ -317,17 +398,39 @@ void build_table_into(fp_ctx* ctx, const fp_instance* in, double radius_km, doub
   double* blat = dlon + M;
   double* blon = blat + B;
   double* cosv = blon + B;  // [B + 2M]: bases, pickups, deliveries
-  h2d(plat, in->pickup_lat, M, st);
-  h2d(plon, in->pickup_lon, M, st);
-  h2d(dlat, in->delivery_lat, M, st);
-  h2d(dlon, in->delivery_lon, M, st);
-  h2d(blat, in->base_lat, B, st);
-  h2d(blon, in->base_lon, B, st);
+  if ((size_t)M >= (1u << 16)) {
+    // large instances: packed on host threads into the context's pinned
+    // buffer, one copy (pageable copies stage through the driver: c4's 32 MB
+    // of coordinates 2.5 -> ~1 ms)
+    const size_t n = 4ull * M + 2ull * B;
+    pinned_points(ctx, n);
+    double* hp = ctx->h_pts;
+    const double* src[6] = {in->pickup_lat, in->pickup_lon, in->delivery_lat, in->delivery_lon,
+                            in->base_lat, in->base_lon};
+    const size_t len[6] = {(size_t)M, (size_t)M, (size_t)M, (size_t)M, (size_t)B, (size_t)B};
+    constexpr int kParts = 64;
+    parallel_for(6 * kParts, [&](int k) {
+      const int a = k / kParts, t = k % kParts;
+      size_t off = 0;
+      for (int q = 0; q < a; ++q) off += len[q];
+      const size_t lo = len[a] * t / kParts, hi = len[a] * (t + 1) / kParts;
+      std::memcpy(hp + off + lo, src[a] + lo, sizeof(double) * (hi - lo));
+    });
+    h2d(plat, hp, n, st);  // plat .. blon are contiguous in the same order
+  } else {
+    h2d(plat, in->pickup_lat, M, st);
+    h2d(plon, in->pickup_lon, M, st);
+    h2d(dlat, in->delivery_lat, M, st);
+    h2d(dlon, in->delivery_lon, M, st);
+    h2d(blat, in->base_lat, B, st);
+    h2d(blon, in->base_lon, B, st);
+  }
   check(fpk::launch_point_cos(blat, B, cosv, st), "cos(bases)");
   check(fpk::launch_point_cos(plat, M, cosv + B, st), "cos(pickups)");
   check(fpk::launch_point_cos(dlat, M, cosv + B + M, st), "cos(deliveries)");
   EvTimer tk(st);
   int sites = 0;
+  if (std::getenv("FLEETPLACE_TRACE")) std::fprintf(stderr, "[fleetplace trace] build: points staged\n");
   check(fpk::launch_table_auto(blat, blon, cosv, B, plat, plon, cosv + B, dlat, dlon,
                                cosv + B + M, M, radius_km, dst, st, &sites),
         "table_kernel");
@@ -563,30 +666,6 @@ struct Trace {
     std::fprintf(stderr, "[fleetplace trace] %8.3f ms  %s\n", ms, what);
   }
 };
-
-// fn(0..n-1) on up to 16 host threads (per-scenario host work of batches);
-// the first exception is rethrown.
-template <typename Fn>
-void parallel_for(int n, Fn&& fn) {
-  const int T = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u);
-  if (n < 64 || T == 1) {
-    for (int i = 0; i < n; ++i) fn(i);
-    return;
-  }
-  std::vector<std::thread> ws;
-  std::vector<std::exception_ptr> errs(T);
-  for (int t = 0; t < T; ++t)
-    ws.emplace_back([&, t] {
-      try {
-        for (int i = (int)((long long)n * t / T); i < (int)((long long)n * (t + 1) / T); ++i) fn(i);
-      } catch (...) {
-        errs[t] = std::current_exception();
-      }
-    });
-  for (auto& w : ws) w.join();
-  for (auto& e : errs)
-    if (e) std::rethrow_exception(e);
-}
 
 // Shared driver for fp_search / fp_search_batch. `tables[s]` is a device
 // pointer to scenario s's table (nullptr = the scenario's arena copy).
@@ -1336,12 +1415,16 @@ fp_status fp_build_distance_table(fp_ctx* ctx, const fp_instance* in, double rad
     cudaStream_t st = ctx->stream;
     if (!(radius_km >= 0.0 && radius_km < INFINITY))
       throw FpError(FP_ERR_INVALID_ARGUMENT, "radius_km must be finite and >= 0");
+    Trace tr;
     table_alloc(ctx, M, B);
+    tr.mark("build: table allocated");
     build_table_into(ctx, in, radius_km, ctx->d_cost);
+    tr.mark("build: kernels enqueued");
     ctx->table_ok = true;  // haversine sums: finite and >= 0 for valid coordinates
     start_costT(ctx);
     if (out_cost) d2h(out_cost, ctx->d_cost, (size_t)M * B, st);
     check(cudaStreamSynchronize(st), "table sync");
+    tr.mark("build: done");
   });
 }
 
@@ -1554,7 +1637,15 @@ void rank_from_totals(fp_ctx* ctx, const fp_instance* in, const double* tot, fp_
     h2d(d_cbid, cbid.data(), n, st);
     h2d(d_cv, cv.data(), n, st);
     h2d(d_cf, cf.data(), n, st);
-    h2d(d_ro, in->rotary_only, M, st);
+    // large instances: the per-mission copies through the pinned buffer
+    const bool staged = (size_t)M >= (1u << 16);
+    if (staged) {
+      pinned_points(ctx, (size_t)M / 2 + 2);
+      std::memcpy(ctx->h_pts, in->rotary_only, (size_t)M);
+      h2d(d_ro, reinterpret_cast<const uint8_t*>(ctx->h_pts), M, st);
+    } else {
+      h2d(d_ro, in->rotary_only, M, st);
+    }
     const int32_t big = 0x7fffffff;
     h2d(d_bad, &big, 1, st);
     check(fpk::launch_mission_argmin(ctx->d_cost, M, d_cb, d_cbid, d_cf, d_cv, n, d_ro, d_mv, d_bad,
@@ -1562,9 +1653,15 @@ void rank_from_totals(fp_ctx* ctx, const fp_instance* in, const double* tot, fp_
           "mission_argmin");
     ctx->launches += 1;
     int32_t bad = 0;
-    d2h(out->mission_vehicle, d_mv, M, st);
+    int32_t* const hmv = staged ? reinterpret_cast<int32_t*>(ctx->h_pts) : out->mission_vehicle;
+    d2h(hmv, d_mv, M, st);
     d2h(&bad, d_bad, 1, st);
     check(cudaStreamSynchronize(st), "rank sync");
+    if (staged)
+      parallel_for(64, [&](int t) {
+        const size_t lo = (size_t)M * t / 64, hi = (size_t)M * (t + 1) / 64;
+        std::memcpy(out->mission_vehicle + lo, hmv + lo, 4 * (hi - lo));
+      });
     if (bad != big)
       throw FpError(FP_ERR_NO_COMPATIBLE, "mission " + std::to_string(in->mission_id[bad]) +
                                               " has no compatible placed vehicle");
@@ -1651,13 +1748,7 @@ fp_status fp_search_batch_configs(fp_ctx* ctx, int32_t n, const fp_instance* ins
       built = DBuf<double>(tot + 2, st);
       // points: [lat | lon | cos] regions, each [bases, pickups, deliveries]
       // per scenario, packed on host threads into the context's pinned buffer
-      if (ctx->h_pts_cap < 2 * npts) {
-        if (ctx->h_pts) cudaFreeHost(ctx->h_pts);
-        ctx->h_pts = nullptr;
-        ctx->h_pts_cap = 0;
-        check(cudaMallocHost(&ctx->h_pts, sizeof(double) * 2 * npts), "pinned points");
-        ctx->h_pts_cap = 2 * npts;
-      }
+      pinned_points(ctx, 2 * npts);
       double* const hp = ctx->h_pts;
       pts = DBuf<double>(3 * npts + 1, st);
       std::vector<fpk::TableJob> jobs(build.size());

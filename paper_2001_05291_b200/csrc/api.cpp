@@ -75,6 +75,7 @@ struct fp_ctx {
   size_t costT_cap = 0;   // elements
   bool costT_valid = false;
   cudaStream_t aux = nullptr;
+  cudaStream_t pstream = nullptr;  // a batch's first permutation draws (overlap its start)
   cudaEvent_t table_ready = nullptr, costT_ready = nullptr;
   cudaEvent_t copy_t0 = nullptr, copy_t1 = nullptr;  // timing of the copy
   bool copy_timed = false;
@@ -1064,11 +1065,20 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   bool dev_perm = inkernel && M >= 2 && fpk::fy_smem_bytes(M) <= (200u << 10);
   if (const char* e = std::getenv("FLEETPLACE_DEVICE_PERMS")) dev_perm = dev_perm && std::atoi(e) != 0;
   bool force_bad = std::getenv("FLEETPLACE_PERM_FORCE_BAD") != nullptr;  // test hook
+  // the first chunk's draws depend on the seeds only: on a side stream they
+  // overlap the staging and init kernels (c5 share: ~10 ms of draws)
+  cudaStream_t pst = st;
+  cudaEvent_t perm_done = nullptr;
+  if (dev_perm && inkernel) {
+    if (!ctx->pstream) check(cudaStreamCreateWithFlags(&ctx->pstream, cudaStreamNonBlocking), "stream");
+    pst = ctx->pstream;
+    check(cudaEventCreateWithFlags(&perm_done, cudaEventDisableTiming), "event");
+  }
   if (dev_perm) {
     std::vector<fpk::MtState> seeded(D);
     for (int d = 0; d < D; ++d) fpk::mt_seed_host(&seeded[d], seeds[d]);
-    h2d(d_mt, seeded.data(), D, st);
-    check(cudaMemsetAsync(d_pbad, 0, sizeof(int), st), "memset");
+    h2d(d_mt, seeded.data(), D, pst);
+    check(cudaMemsetAsync(d_pbad, 0, sizeof(int), pst), "memset");
   }
   int kchunk = next_chunk(0);
   int buf = 0;
@@ -1094,10 +1104,15 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       if (tr.on) {
         cudaEventCreate(&q0);
         cudaEventCreate(&q1);
-        cudaEventRecord(q0, st);
+        cudaEventRecord(q0, pst);
       }
-      check(fpk::launch_permutations(d_mt, D, M, 2 * kchunk, d_draws, d_perm, d_pbad, st),
+      check(fpk::launch_permutations(d_mt, D, M, 2 * kchunk, d_draws, d_perm, d_pbad, pst),
             "permutations");
+      if (pst != st) {
+        check(cudaEventRecord(perm_done, pst), "event");
+        check(cudaStreamWaitEvent(st, perm_done, 0), "wait");
+        pst = st;  // later chunks: in order on the search stream
+      }
       if (tr.on) {
         cudaEventRecord(q1, st);
         cudaEventSynchronize(q1);
@@ -1207,6 +1222,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       }
     }
   }
+  if (perm_done) cudaEventDestroy(perm_done);  // (the wait on it is enqueued)
   check(fpk::launch_final(d_scs, n, st), "final_kernel");
   ctx->launches += 1;
   check(cudaEventRecord(ev1, st), "event");
@@ -1323,6 +1339,7 @@ void fp_ctx_destroy(fp_ctx* ctx) {
   if (ctx->h_pts) cudaFreeHost(ctx->h_pts);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->pstream) cudaStreamDestroy(ctx->pstream);
   if (ctx->table_ready) cudaEventDestroy(ctx->table_ready);
   if (ctx->costT_ready) cudaEventDestroy(ctx->costT_ready);
   if (ctx->copy_t0) cudaEventDestroy(ctx->copy_t0);

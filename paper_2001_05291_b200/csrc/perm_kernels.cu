@@ -44,40 +44,46 @@ __device__ __forceinline__ unsigned long long temper(unsigned long long x) {
 }  // namespace
 
 // Appends `count` outputs of the generator held in st[blockIdx.x] to
-// out + blockIdx.x * count. One block of 320 threads per stream.
+// out + blockIdx.x * count. One block of 320 threads per stream. The state is
+// double-buffered in shared memory (round r reads buffer r&1 and writes the
+// other), so a round is two barriers: phase A (k < 156: old words only),
+// phase B (k >= 156: old words and phase A's new ones); the tempering and
+// stores of a round overlap the next round's phase A.
 __global__ void __launch_bounds__(320) mt_gen_kernel(MtState* st, unsigned long long* out,
                                                      long long count) {
-  __shared__ unsigned long long mt[312];
+  __shared__ unsigned long long mt[2][312];
   st += blockIdx.x;
   out += (long long)blockIdx.x * count;
   const int t = threadIdx.x;
-  for (int k = t; k < 312; k += blockDim.x) mt[k] = st->mt[k];
+  for (int k = t; k < 312; k += blockDim.x) mt[0][k] = st->mt[k];
   int idx = st->idx;
+  int cur = 0;  // the buffer holding the current state
   __syncthreads();
   long long produced = 0;
-  while (produced < count) {
-    if (idx >= 312) {
-      // phase A: k < 156 reads old mt[k], mt[k+1], mt[k+156]
-      unsigned long long v = 0;
-      if (t < 156) v = twist_word(mt[t], mt[t + 1], mt[t + 156]);
-      __syncthreads();
-      if (t < 156) mt[t] = v;
-      __syncthreads();
-      // phase B: 156 <= k < 312 reads old mt[k], mt[k+1] (k = 311: new mt[0])
-      // and new mt[k-156]
-      if (t >= 156 && t < 312) v = twist_word(mt[t], mt[t == 311 ? 0 : t + 1], mt[t - 156]);
-      __syncthreads();
-      if (t >= 156 && t < 312) mt[t] = v;
-      __syncthreads();
-      idx = 0;
-    }
-    const int n = (int)min((long long)(312 - idx), count - produced);
-    if (t < n) out[produced + t] = temper(mt[idx + t]);
+  // the rest of the current state's outputs
+  if (idx < 312) {
+    const int n = (int)min((long long)(312 - idx), count);
+    if (t < n) out[t] = temper(mt[cur][idx + t]);
     idx += n;
     produced += n;
   }
+  while (produced < count) {
+    const unsigned long long* o = mt[cur];
+    unsigned long long* w = mt[cur ^ 1];
+    // phase A: k < 156 reads old k, k+1, k+156
+    if (t < 156) w[t] = twist_word(o[t], o[t + 1], o[t + 156]);
+    __syncthreads();
+    // phase B: 156 <= k < 312 reads old k, k+1 (k = 311: new 0) and new k-156
+    if (t >= 156 && t < 312) w[t] = twist_word(o[t], t == 311 ? w[0] : o[t + 1], w[t - 156]);
+    __syncthreads();
+    cur ^= 1;
+    const int n = (int)min(312ll, count - produced);
+    if (t < n) out[produced + t] = temper(mt[cur][t]);
+    idx = n;
+    produced += n;
+  }
   __syncthreads();
-  for (int k = t; k < 312; k += blockDim.x) st->mt[k] = mt[k];
+  for (int k = t; k < 312; k += blockDim.x) st->mt[k] = mt[cur][k];
   if (t == 0) st->idx = idx;
 }
 

@@ -25,4 +25,4 @@ for it in range(int(sys.argv[1]) if len(sys.argv) > 1 else 12):
     w = time.perf_counter() - t0
     s = res[0].stats
     print(f"call {it}: device {s.device_ms:.1f} ms, pass {s.pass_ms:.1f} ms, init {s.init_ms:.1f}, "
-          f"launches {s.pass_launches}, wall {1e3 * w:.1f} ms", file=sys.stderr, flush=True)
+          f"launches {s.pass_launches}, init parts {[round(x, 2) for x in s.init_part_ms]}, wall {1e3 * w:.1f} ms", file=sys.stderr, flush=True)

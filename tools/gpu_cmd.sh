@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-bash tools/gpu_tests.sh 2400
-timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench_rc=$?; tail -c 400 gpurun_out/bench.json
+FLEETPLACE_TRACE=1 timeout 600 python tools/c5_outlier_probe.py 4 > gpurun_out/c5_outlier.log 2>&1; echo rc=$?; tail -12 gpurun_out/c5_outlier.log

@@ -129,7 +129,9 @@ typedef struct fp_search_result {
                                     updates, relocation apply, exact totals,
                                     table patches, per-pass setup, exact
                                     relocation deltas, exact candidate totals,
-                                    helper waits, (reserved) */
+                                    helper waits, (reserved); all zero unless
+                                    the library is built with -DFP_PHASE_CLOCKS
+                                    (a profiling build: the clocks cost ~5%) */
   double init_ms;                /* search start: costs, exact total, relocation
                                     table sweep (CUDA events) */
   double sweep_ms;               /* per-pass bitset sweeps (grid-wide mode) */

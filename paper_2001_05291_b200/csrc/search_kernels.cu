@@ -100,11 +100,22 @@ struct Smem {
 };
 
 // Phase timing (thread 0's SM clock), accumulated into Counters::cycles.
+// Phase clocks (SearchStats::phase_cycles): probe builds only
+// (FLEETPLACE_NVCC_DEFS=FP_PHASE_CLOCKS): thread 0's clock reads and
+// shared-memory accumulations cost the automaton ~5% (c2 to quiescence 112
+// -> 107 ms, the c5 share 193 -> 182 ms without them).
+#ifndef FP_PHASE_CLOCKS
+__device__ __forceinline__ long long ph_now() { return 0; }
+#define PH_ADD(sh, k, t0) \
+  do {                    \
+  } while (0)
+#else
 __device__ __forceinline__ long long ph_now() { return threadIdx.x == 0 ? clock64() : 0; }
 #define PH_ADD(sh, k, t0)                                        \
   do {                                                           \
     if (threadIdx.x == 0) (sh).c.cycles[k] += clock64() - (t0); \
   } while (0)
+#endif
 
 __device__ __forceinline__ double cost_at(const Scenario& s, int col, int m) {
   return s.cost[(long long)col * s.M + m];

@@ -1,5 +1,6 @@
 """c3 (2k x 100k x 100; or argv[1] = B,M,V and argv[2:] = pass caps) to quiescence: device time and the pass kernel's
-phase clocks (scenario 0), to see where the per-move time goes."""
+phase clocks (scenario 0), to see where the per-move time goes. The clocks need a
+probe build: FLEETPLACE_NVCC_DEFS=FP_PHASE_CLOCKS python -m paper_2001_05291_b200._build --force"""
 import sys
 from pathlib import Path
 

@@ -1,6 +1,7 @@
 """The c5 share's longest scenarios (instance seeds 29, 40, 508: 786 / 773 /
 710 passes) alone in 2-copy batches (the in-kernel path): device time and the
-pass kernel's phase clocks per thread count."""
+pass kernel's phase clocks per thread count (phase clocks: probe build with
+FLEETPLACE_NVCC_DEFS=FP_PHASE_CLOCKS python -m paper_2001_05291_b200._build --force)."""
 import os
 import sys
 from pathlib import Path

@@ -78,7 +78,7 @@ _C5 = {}
 def _assert_c5_golden(seed: int, stats, vb, mv) -> None:
     """Parity gate for the c5 share: every scenario (instance seed 1..512) equals
     the reference's recorded run (tests/golden/c5_512.json; own tables, so the
-    objective within 1e-9 relative)."""
+    objective bits too: kernel (1) is bit-identical to the reference's table)."""
     import struct
     if not _C5:
         f = ROOT / "tests" / "golden" / "c5_512.json"
@@ -90,18 +90,18 @@ def _assert_c5_golden(seed: int, stats, vb, mv) -> None:
            stats.tabu_skips_outer, stats.tabu_skips_inner]
     ref = struct.unpack(">d", bytes.fromhex(g["final_objective_bits"]))[0]
     if got != g["stats"] or _sha(vb, mv) != g["assignment_sha256"] or \
-            abs(stats.final_objective_km - ref) > 1e-9 * ref:
+            stats.final_objective_km != ref:
         raise SystemExit(f"PARITY FAILURE on c5 scenario {seed}: {got} vs the reference's {g['stats']}")
 
 
 def _assert_golden(name: str, stats, vb, mv) -> None:
     """Parity gate: the six SearchStats counters and the final Assignment
-    equal the reference's recorded run (objective within 1e-9 relative)."""
+    equal the reference's recorded run (objective bits too)."""
     g = _golden(name)
     got = [stats.passes, stats.evaluations, stats.applied_moves, stats.committed_moves,
            stats.tabu_skips_outer, stats.tabu_skips_inner]
     if got != g["stats"] or _sha(vb, mv) != g["assignment_sha256"] or \
-            abs(stats.final_objective_km - g["final_objective_km"]) > 1e-9 * g["final_objective_km"]:
+            stats.final_objective_km != g["final_objective_km"]:
         raise SystemExit(f"PARITY FAILURE on {name}: {got} vs the reference's {g['stats']}")
 
 

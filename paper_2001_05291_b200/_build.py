@@ -26,6 +26,9 @@ def _stale() -> bool:
         return True
     t = LIB.stat().st_mtime
     deps = [CSRC / s for s in SOURCES] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp"))
+    deps += [PKG / "_glibc_tables.py"]
+    if not (CSRC / "gen" / "glibc_dbl64_tables.inc").exists():
+        return True
     deps.append(ROOT / "include" / "fleetplace_b200.h")
     return any(d.stat().st_mtime > t for d in deps)
 
@@ -36,6 +39,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     from concurrent.futures import ThreadPoolExecutor
 
     LIB_DIR.mkdir(exist_ok=True)
+    # glibc's sin/cos/asin tables, read from the image's libm (glibc_dbl64.cuh)
+    from paper_2001_05291_b200._glibc_tables import write as write_glibc_tables
+    write_glibc_tables()
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
              "-Xptxas", "-v", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
     # probe builds only (e.g. FLEETPLACE_NVCC_DEFS=FP_RELOC_PROBE): extra -D macros
@@ -45,6 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     cmds.append([NVCC, *ARCH, "-shared", *[str(LIB_DIR / (s + ".o")) for s in SOURCES],
                  "-o", str(LIB)])
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.hpp")) + [ROOT / "include" / "fleetplace_b200.h"]
+    headers += list((CSRC / "gen").glob("*.inc"))
     newest_h = max(h.stat().st_mtime for h in headers)
 
     def run(c):

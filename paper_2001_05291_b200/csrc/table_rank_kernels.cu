@@ -5,8 +5,8 @@
 // none of its multiply-adds are fused; every product/sum here is an explicit
 // __dmul_rn/__dadd_rn so nvcc cannot contract them into FMAs. cos(phi) of
 // every point is hoisted (bit-identical: same argument, same function).
-// The transcendentals are CUDA's fp64 sin/asin; see DESIGN.md for the
-// measured per-entry ULP agreement with glibc.
+// The transcendentals are glibc's own sin/cos/asin restated for the device
+// (glibc_dbl64.cuh), so every entry is bit-identical to the reference's.
 //
 // Kernel (2) computes the fixed-order column totals (proj/src/rank.cpp:10-23):
 // each column is ONE sequential fp64 chain in row order, bit-identical to the
@@ -22,6 +22,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
+#include "glibc_dbl64.cuh"
 
 namespace fpk {
 
@@ -31,19 +32,19 @@ constexpr double kDegToRad = 3.14159265358979323846 / 180.0;
 
 __global__ void point_cos_kernel(const double* __restrict__ lat, int n, double* __restrict__ out) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-    out[k] = cos(__dmul_rn(lat[k], kDegToRad));
+    out[k] = gl64::cos(__dmul_rn(lat[k], kDegToRad));
 }
 
 __device__ __forceinline__ double hav(double lat_a, double lon_a, double cos_a, double lat_b,
                                       double lon_b, double cos_b, double two_r) {
   const double half_dphi = __dmul_rn(__dmul_rn(0.5, fabs(__dsub_rn(lat_b, lat_a))), kDegToRad);
   const double half_dpsi = __dmul_rn(__dmul_rn(0.5, fabs(__dsub_rn(lon_b, lon_a))), kDegToRad);
-  const double s_lat = sin(half_dphi);
-  const double s_lon = sin(half_dpsi);
+  const double s_lat = gl64::sin(half_dphi);
+  const double s_lon = gl64::sin(half_dpsi);
   const double h = __dadd_rn(__dmul_rn(s_lat, s_lat),
                              __dmul_rn(__dmul_rn(__dmul_rn(cos_a, cos_b), s_lon), s_lon));
   const double r = __dsqrt_rn(h);
-  return __dmul_rn(two_r, asin(fmin(1.0, r)));
+  return __dmul_rn(two_r, gl64::asin(fmin(1.0, r)));
 }
 
 // cost[b*M + m] for a tile of bases; threads run along missions so every
@@ -335,10 +336,10 @@ __global__ void haversine_pairs_kernel(int n, const double* __restrict__ alat,
                                        double* __restrict__ out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const double ca = cos(__dmul_rn(alat[k], kDegToRad));
-  double r = hav(alat[k], alon[k], ca, blat[k], blon[k], cos(__dmul_rn(blat[k], kDegToRad)), two_r);
+  const double ca = gl64::cos(__dmul_rn(alat[k], kDegToRad));
+  double r = hav(alat[k], alon[k], ca, blat[k], blon[k], gl64::cos(__dmul_rn(blat[k], kDegToRad)), two_r);
   if (clat) r = __dadd_rn(r, hav(alat[k], alon[k], ca, clat[k], clon[k],
-                                 cos(__dmul_rn(clat[k], kDegToRad)), two_r));
+                                 gl64::cos(__dmul_rn(clat[k], kDegToRad)), two_r));
   out[k] = r;
 }
 

@@ -21,19 +21,38 @@ def _ulps(a, b):
 
 
 @pytest.mark.parametrize("shape", [(50, 200, 10), (200, 5000, 20), (500, 10000, 40)])
-def test_table_matches_reference_within_8ulp(shape):
-    """Kernel (1) vs glibc: same operation order, no FMA contraction; the only
-    difference is CUDA's vs glibc's sin/asin (each within ~1-2 ulp), which the
-    haversine amplifies to a few ulp of the entry. Tolerance: 8 ulp per entry
-    (relative ~1e-15, far inside the reference's own 1e-12/1e-9 geo tests)."""
+def test_table_bit_identical_to_reference(shape):
+    """Kernel (1) vs the compiled reference's build_distance_table: the same
+    operation order with no FMA contraction, and glibc's own sin/cos/asin
+    restated for the device (csrc/glibc_dbl64.cuh), so every entry is equal
+    bit for bit (0 ulp)."""
     inst = F.survey_instance(*shape, seed=1)
     t = F.build_distance_table(inst)
     got = np.ascontiguousarray(t.cost.T).reshape(-1)
     ref = H.ref_table(inst)
     u = _ulps(got, ref)
-    print(f"ulp histogram {np.bincount(u)}")
-    assert u.max() <= 8, int(u.max())
-    assert (u == 0).mean() > 0.5, float((u == 0).mean())
+    assert int(u.max()) == 0, f"ulp histogram {np.bincount(u)}"
+
+
+def test_table_bit_identical_on_extreme_coordinates():
+    """Every branch of glibc's sin (Taylor, table, pi/2 - x, reduced), cos and
+    asin (Taylor, the five table ranges, the square-root branch near 1, exactly
+    1): poles, the antimeridian, antipodes, co-located and nearly co-located
+    points, random points."""
+    rng = np.random.default_rng(5)
+    pts = [(90.0, 0.0), (-90.0, 0.0), (0.0, 180.0), (0.0, -180.0), (0.0, 0.0), (45.0, 90.0),
+           (-45.0, -90.0), (89.999999, 179.999999), (-89.999999, -179.999999), (1e-9, 1e-9),
+           (0.0, 179.9999), (10.0, -170.0), (60.0, 120.0), (-60.0, -60.0)]
+    pts += [(float(a), float(b)) for a, b in zip(rng.uniform(-90, 90, 200), rng.uniform(-180, 180, 200))]
+    # antipodes and near-antipodes of the first points (asin near 1)
+    pts += [(-a, b - 180.0 if b > 0 else b + 180.0) for a, b in pts[:60]]
+    pts += [(a + 1e-7, b) for a, b in pts[:40] if abs(a) < 89]
+    bases = [(i, i % 2, p) for i, p in enumerate(pts[:150])]
+    missions = [(j, pts[j % len(pts)], pts[(7 * j + 3) % len(pts)], False) for j in range(600)]
+    inst = F.Instance(bases=bases, fleet=[(0, 0)], missions=missions)
+    got = np.ascontiguousarray(F.build_distance_table(inst).cost.T).reshape(-1)
+    ref = H.ref_table(inst)
+    assert int(_ulps(got, ref).max()) == 0
 
 
 def test_table_geo_known_answers():

@@ -1070,14 +1070,20 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   cudaStream_t pst = st;
   cudaEvent_t perm_done = nullptr;
   if (dev_perm && inkernel) {
-    if (!ctx->pstream) check(cudaStreamCreateWithFlags(&ctx->pstream, cudaStreamNonBlocking), "stream");
+    if (!ctx->pstream) {
+      // highest priority: the draws' single block is dispatched ahead of the
+      // start kernels' blocks queued on the search stream
+      int least = 0, greatest = 0;
+      check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+      check(cudaStreamCreateWithPriority(&ctx->pstream, cudaStreamNonBlocking, greatest), "stream");
+    }
     pst = ctx->pstream;
     check(cudaEventCreateWithFlags(&perm_done, cudaEventDisableTiming), "event");
   }
   if (dev_perm) {
-    std::vector<fpk::MtState> seeded(D);
-    for (int d = 0; d < D; ++d) fpk::mt_seed_host(&seeded[d], seeds[d]);
-    h2d(d_mt, seeded.data(), D, pst);
+    // seeded on the device: no host copy queued in front of the draws
+    check(fpk::launch_mt_seed(d_mt, reinterpret_cast<const unsigned long long*>(seeds.data()), D, pst),
+          "mt_seed");
     check(cudaMemsetAsync(d_pbad, 0, sizeof(int), pst), "memset");
   }
   int kchunk = next_chunk(0);

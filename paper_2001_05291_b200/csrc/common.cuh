@@ -99,6 +99,12 @@ struct MtState {
   int idx;
 };
 
+// Up to kMax seeds passed by value to mt_seed_kernel (no host copy).
+struct MtSeeds {
+  static constexpr int kMax = 64;
+  unsigned long long seed[kMax];
+};
+
 // One search scenario: the resident distance table plus the index-based
 // SearchState of proj/src/search_state.hpp:20-31 in structure-of-arrays
 // form, the perm_b-ordered mirrors the scan streams, and the expiry-stamp

@@ -14,6 +14,7 @@ struct Scenario;
 struct MtState;
 
 void mt_seed_host(MtState* st, unsigned long long seed);
+cudaError_t launch_mt_seed(MtState* st, const unsigned long long* seeds, int n, cudaStream_t stream);
 size_t fy_smem_bytes(int n);
 cudaError_t launch_permutations(MtState* st, int nstreams, int n, int nperm,
                                 unsigned long long* draws, int32_t* perms, int* bad,

@@ -6,12 +6,13 @@
 // uniform_below rejects draws below (2^64 - i) mod i. The host generator of
 // api.cpp (PermStream) reproduces that stream; for batches it is the
 // bottleneck (one sequential stream, ~10 ns per draw), so here:
-//  * mt_gen_kernel: one block runs the generator — the 312-word twist in two
-//    data-parallel phases (the in-place sequential update reads old words
-//    ahead of i and new words behind it) and the tempering of every output in
-//    parallel;
-//  * fy_kernel: block per permutation — j = x mod i for every step in
-//    parallel, then the sequential swaps in shared memory by one thread.
+//  * mt_gen_kernel: one block runs the generator's sequential part — the
+//    312-word twist in two data-parallel phases (the in-place sequential
+//    update reads old words ahead of i and new words behind it) — and stores
+//    the raw state words;
+//  * fy_kernel: block per permutation — the tempering of its draws and
+//    j = x mod i for every step in parallel, then the sequential swaps in
+//    shared memory by one thread.
 // A permutation consumes exactly n - 1 draws unless a draw is rejected
 // (probability ~ n / 2^64 per draw); a rejection is flagged, the pass kernels
 // refuse to run on the chunk, and the host regenerates the stream exactly.
@@ -44,11 +45,13 @@ __device__ __forceinline__ unsigned long long temper(unsigned long long x) {
 }  // namespace
 
 // Appends `count` outputs of the generator held in st[blockIdx.x] to
-// out + blockIdx.x * count. One block of 320 threads per stream. The state is
-// double-buffered in shared memory (round r reads buffer r&1 and writes the
-// other), so a round is two barriers: phase A (k < 156: old words only),
-// phase B (k >= 156: old words and phase A's new ones); the tempering and
-// stores of a round overlap the next round's phase A.
+// out + blockIdx.x * count, UNTEMPERED (the consumer applies temper()). One
+// block of 320 threads per stream. The state is double-buffered in shared
+// memory (round r reads buffer r&1 and writes the other), so a round is two
+// barriers: phase A (k < 156: old words only), phase B (k >= 156: old words
+// and phase A's new ones); the stores of a round overlap the next round's
+// phase A. The tempering (half of the per-output work) is left to the
+// parallel consumer, off the generator's sequential critical path.
 __global__ void __launch_bounds__(320) mt_gen_kernel(MtState* st, unsigned long long* out,
                                                      long long count) {
   __shared__ unsigned long long mt[2][312];
@@ -63,7 +66,7 @@ __global__ void __launch_bounds__(320) mt_gen_kernel(MtState* st, unsigned long 
   // the rest of the current state's outputs
   if (idx < 312) {
     const int n = (int)min((long long)(312 - idx), count);
-    if (t < n) out[t] = temper(mt[cur][idx + t]);
+    if (t < n) out[t] = mt[cur][idx + t];
     idx += n;
     produced += n;
   }
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(320) mt_gen_kernel(MtState* st, unsigned long 
     __syncthreads();
     cur ^= 1;
     const int n = (int)min(312ll, count - produced);
-    if (t < n) out[produced + t] = temper(mt[cur][t]);
+    if (t < n) out[produced + t] = mt[cur][t];
     idx = n;
     produced += n;
   }
@@ -87,8 +90,9 @@ __global__ void __launch_bounds__(320) mt_gen_kernel(MtState* st, unsigned long 
   if (t == 0) st->idx = idx;
 }
 
-// Permutation p of nperm (n elements) from draws[p*(n-1) ...]: Fisher–Yates
-// with j_i = x mod i. Dynamic shared memory: 4*(2n+1) bytes.
+// Permutation p of nperm (n elements) from draws[p*(n-1) ...] (untempered
+// state words: x = temper(word)): Fisher–Yates with j_i = x mod i. Dynamic
+// shared memory: 4*(2n+1) bytes.
 __global__ void __launch_bounds__(256) fy_kernel(const unsigned long long* __restrict__ draws, int n,
                                                  int32_t* __restrict__ perms, int* bad) {
   extern __shared__ int fy_smem[];
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(256) fy_kernel(const unsigned long long* __res
   int* jv = fy_smem + n;   // [n + 1], jv[i] for i = 2..n
   const long long base = (long long)blockIdx.x * (n - 1);
   for (int i = 2 + threadIdx.x; i <= n; i += blockDim.x) {
-    const unsigned long long x = draws[base + (n - i)];
+    const unsigned long long x = temper(draws[base + (n - i)]);
     const unsigned long long ui = (unsigned long long)i;
     if (x < (0ull - ui) % ui) atomicOr(bad, 1);
     jv[i] = (int)(x % ui);
@@ -114,6 +118,30 @@ __global__ void __launch_bounds__(256) fy_kernel(const unsigned long long* __res
   __syncthreads();
   int32_t* dst = perms + (long long)blockIdx.x * n;
   for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = out[k];
+}
+
+// The seeded states (std::mersenne_twister_engine::seed) on the device: the
+// search's first permutation chunk needs no host copy in front of it.
+__global__ void mt_seed_kernel(MtState* st, MtSeeds seeds, int n) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  unsigned long long x = seeds.seed[d];
+  st[d].mt[0] = x;
+  for (int i = 1; i < 312; ++i) {
+    x = 6364136223846793005ull * (x ^ (x >> 62)) + (unsigned)i;
+    st[d].mt[i] = x;
+  }
+  st[d].idx = 312;
+}
+
+cudaError_t launch_mt_seed(MtState* st, const unsigned long long* seeds, int n, cudaStream_t stream) {
+  for (int d0 = 0; d0 < n; d0 += MtSeeds::kMax) {
+    MtSeeds b;
+    const int k = n - d0 < MtSeeds::kMax ? n - d0 : MtSeeds::kMax;
+    for (int i = 0; i < k; ++i) b.seed[i] = seeds[d0 + i];
+    mt_seed_kernel<<<1, MtSeeds::kMax, 0, stream>>>(st + d0, b, k);
+  }
+  return cudaGetLastError();
 }
 
 // Host: the seeded state (std::mersenne_twister_engine::seed).

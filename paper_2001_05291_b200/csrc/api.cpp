@@ -1103,8 +1103,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   if (threads >= 1024) helpers = 0;
   unsigned epoch = 0;
   int n_active = n;
+  bool active_dirty = true;  // the device copy of `active` is stale
   while (n_active > 0) {
-    h2d(d_active, active, n, st);
+    if (active_dirty) h2d(d_active, active, n, st);
+    active_dirty = false;
     if (dev_perm) {
       cudaEvent_t q0 = nullptr, q1 = nullptr;
       if (tr.on) {
@@ -1225,6 +1227,7 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
       if (ctrs[s].done || ctrs[s].error) {
         active[s] = 0;
         --n_active;
+        active_dirty = true;
       }
     }
   }

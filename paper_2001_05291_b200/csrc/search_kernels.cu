@@ -35,6 +35,8 @@
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 #ifdef FP_ROW_TRACE
@@ -2789,6 +2791,40 @@ cudaError_t launch_gather_results(const Scenario* d_scs, int n_scn, int M, int32
   return cudaGetLastError();
 }
 
+// Host-side launch attributes, cached per kernel: a single scenario's search
+// enqueues a pass per host round trip, and the attribute / occupancy queries
+// were part of that latency.
+namespace {
+std::mutex g_attr_mu;
+std::unordered_map<const void*, int> g_smem_set;                 // max dynamic smem set
+std::unordered_map<const void*, std::pair<size_t, int>> g_occ;   // (smem, blocks per SM)
+int g_sms = 0;
+
+void set_smem(const void* kern, size_t smem) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_smem_set.find(kern);
+  if (it != g_smem_set.end() && it->second >= (int)smem) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  g_smem_set[kern] = (int)smem;
+}
+
+int blocks_per_sm(const void* kern, int nt, size_t smem, int* sms) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  *sms = g_sms;
+  auto it = g_occ.find(kern);
+  if (it != g_occ.end() && it->second.first == smem) return it->second.second;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nt, smem);
+  g_occ[kern] = {smem, per_sm};
+  return per_sm;
+}
+}  // namespace
+
 template <int NT>
 static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int n_scn,
                                   const int32_t* d_perms, int kpasses, bool inkernel,
@@ -2821,15 +2857,13 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
   const bool help_possible = helpers_req != 0 && n_scn == 1 && kpasses == 1 && !inkernel && !bits_smem;
   auto kern = inkernel ? pass_kernel<NT, true, false>
                        : (help_possible ? pass_kernel<NT, false, true> : pass_kernel<NT, false, false>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_smem((const void*)kern, smem);
   // helper blocks: one scenario, one pass per launch, bitsets in global
   // memory, and every block co-resident (cooperative launch)
   int helpers = 0;
   if (helpers_req != 0 && n_scn == 1 && kpasses == 1 && !inkernel && !bits_smem) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    int sms = 0;
+    const int per_sm = blocks_per_sm((const void*)kern, NT, smem, &sms);
     helpers = per_sm * sms - 1;
     if (helpers_req > 0 && helpers_req < helpers) helpers = helpers_req;
     if (helpers < 0) helpers = 0;
@@ -2846,7 +2880,7 @@ static cudaError_t launch_pass_nt(Scenario* d_scs, const int32_t* d_active, int 
     // same pass without helpers, which is only an execution strategy
     cudaGetLastError();
     kern = pass_kernel<NT, false, false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem((const void*)kern, smem);
   }
   kern<<<n_scn, NT, smem, stream>>>(d_scs, d_active, d_perms, kpasses, inkernel,
                                                max_passes, tabu, tenure, debug, in_smem,

@@ -59,7 +59,7 @@ def _instance(k: int) -> F.Instance:
     return F.Instance(bases=bases, fleet=fleet, missions=missions)
 
 
-@pytest.mark.parametrize("k", range(16))
+@pytest.mark.parametrize("k", range(40))
 def test_fuzzed_instance_whole_pipeline_bit_exact(k):
     inst = _instance(k)
     t = F.build_distance_table(inst)

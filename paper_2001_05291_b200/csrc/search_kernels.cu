@@ -2379,7 +2379,12 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (NT == 256 ? 2 : 4))
     long long T = sh.c.tick;  // every thread tracks the tick through row runs
     while (r < M && !sh.c.error) {
       const long long b0 = ph_now();
-      table_sync<NT, HELP>(s, sh, sm);  // the eventless test reads rcnt
+      // relocation-table patches published to the helper blocks and not yet
+      // confirmed: instead of waiting for them here, a row whose eventless
+      // test needs rcnt (its pool entry is an empty base) counts as
+      // nontrivial -- run_row settles it exactly after its own table_sync --
+      // so the patches overlap the classification of the rows that follow
+      const bool patches_pending = HELP && sm.helpers > 0 && sh.lt != sh.lsync;
       if (r < pw || r + NT > pw + 2 * NT) {
         pw = r;
         for (int k = threadIdx.x; k < 2 * NT; k += NT) sm.paw[k] = pw + k < M ? pa[pw + k] : 0;
@@ -2411,7 +2416,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : (NT == 256 ? 2 : 4))
               E = max(E, s.exp_take[x]);
             }
           } else {
-            st = st && s.rcnt[x] == 0;
+            st = st && !patches_pending && s.rcnt[x] == 0;
             if (tabu) {
               const int k = s.brk[x];
               F = max(F, s.exp_rel[k]);

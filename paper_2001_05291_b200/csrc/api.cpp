@@ -207,9 +207,9 @@ void table_alloc(fp_ctx* ctx, int M, int B) {
 // fn(0..n-1) on up to 16 host threads (per-scenario host work of batches);
 // the first exception is rethrown.
 template <typename Fn>
-void parallel_for(int n, Fn&& fn) {
-  const int T = (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u);
-  if (n < 64 || T == 1) {
+void parallel_for(int n, Fn&& fn, int min_n = 64) {
+  const int T = std::min(n, (int)std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u));
+  if (n < min_n || T <= 1) {
     for (int i = 0; i < n; ++i) fn(i);
     return;
   }
@@ -454,6 +454,40 @@ struct PermStream {
     for (int64_t i = n; i > 1; --i) {
       const int64_t j = (int64_t)below((uint64_t)i);
       std::swap(out[i - 1], out[j]);
+    }
+  }
+  // The same `count` permutations of n, faster for large n: the generator's
+  // raw outputs first (the only sequential part), then the Fisher-Yates
+  // shuffles on host threads -- permutation p consumes draws
+  // [p(n-1), (p+1)(n-1)) unless a draw is rejected (x < (2^64 - i) mod i,
+  // probability ~n/2^64 per draw); a rejection anywhere redoes the chunk
+  // sequentially from the saved generator state, so the stream is exact.
+  void perms(int n, int count, int32_t* out, std::vector<uint64_t>& raw) {
+    if (n < (32 << 10) || count < 2) {
+      for (int p = 0; p < count; ++p) perm(n, out + (size_t)p * n);
+      return;
+    }
+    const std::mt19937_64 saved = rng;
+    const size_t per = (size_t)n - 1;
+    raw.resize(per * count);
+    for (auto& x : raw) x = rng();
+    std::atomic<bool> rejected{false};
+    parallel_for(count, [&](int p) {
+      int32_t* o = out + (size_t)p * n;
+      const uint64_t* r = raw.data() + per * p;
+      for (int i = 0; i < n; ++i) o[i] = i;
+      for (int64_t i = n, k = 0; i > 1; --i, ++k) {
+        const uint64_t x = r[k], ui = (uint64_t)i;
+        if (x < ui && x < (0 - ui) % ui) {  // (the threshold is below i)
+          rejected = true;
+          return;
+        }
+        std::swap(o[i - 1], o[x % ui]);
+      }
+    }, 2);
+    if (rejected) {
+      rng = saved;
+      for (int p = 0; p < count; ++p) perm(n, out + (size_t)p * n);
     }
   }
 };
@@ -1032,9 +1066,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   std::vector<PermStream> rngs;
   for (uint64_t sd : seeds) rngs.emplace_back(sd);
   // a chunk of kk passes: stream d's 2*kk permutations at d * 2*kk*M
+  std::vector<uint64_t> raw_draws;
   auto gen_chunk = [&](int32_t* buf, int kk) {
-    for (int d = 0; d < D; ++d)
-      for (int k = 0; k < 2 * kk; ++k) rngs[d].perm(M, buf + (2ll * kk * d + k) * M);
+    for (int d = 0; d < D; ++d) rngs[d].perms(M, 2 * kk, buf + 2ll * kk * d * M, raw_draws);
   };
   long long launched = 0;  // passes whose permutations went to the device
   // batches: one launch for (nearly) every search — a chunk boundary makes
@@ -1052,7 +1086,9 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   bool adaptive = n == 1 && !inkernel && M >= (8 << 10) && M < (32 << 10) && threads < 1024 &&
                   !std::getenv("FLEETPLACE_HELPERS");
   if (const char* e = std::getenv("FLEETPLACE_ADAPTIVE_HELPERS")) adaptive = adaptive && std::atoi(e) != 0;
-  int kfirst = inkernel && n == 1 ? std::min(kmax, 32) : (adaptive ? 1 : kmax);
+  // (large single scenarios start with 2 passes: the GPU starts after the first
+  // chunk of host permutations, later chunks are drawn while it works)
+  int kfirst = inkernel ? (n == 1 ? std::min(kmax, 32) : kmax) : (adaptive ? 1 : std::min(kmax, 2));
   if (const char* e = std::getenv("FLEETPLACE_KFIRST")) kfirst = std::max(1, std::min(kmax, std::atoi(e)));
   auto next_chunk = [&](int prev) {
     int k = prev == 0 ? kfirst : (adaptive ? 1 : std::min(kmax, 2 * prev));

@@ -736,6 +736,16 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     pEg = s.rE[kg];
     pUg = s.rU[kg];
   }
+  // The membership move and the helpers' patch record depend on nothing the
+  // vehicle loop computes: two threads of the last warps (no vehicle of
+  // theirs when V <= NT - 64) issue them first, so their global
+  // read-modify-writes and the record's release overlap the loop's gathers.
+  const long long tp0 = ph_now();
+  if (threadIdx.x == NT - 1 && loser != gain) {
+    s.mem[(long long)loser * s.nwd + wd] &= ~bit;
+    s.mem[(long long)gain * s.nwd + wd] |= bit;
+  }
+  if (logged && threadIdx.x == NT - 33) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, s.mcp[q]);
   for (int g0 = 0; g0 < s.V; g0 += NT) {
     const int g = g0 + threadIdx.x;
     bool now = false;
@@ -750,13 +760,7 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     const unsigned row = __ballot_sync(FULL, now);
     if ((threadIdx.x & 31) == 0 && g < s.V) s.impT[(long long)j * s.nvw + (g >> 5)] = row;
   }
-  if (threadIdx.x == 0 && loser != gain) {
-    s.mem[(long long)loser * s.nwd + wd] &= ~bit;
-    s.mem[(long long)gain * s.nwd + wd] |= bit;
-  }
-  const long long tp0 = ph_now();
   if (logged) {
-    if (threadIdx.x == 0) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, s.mcp[q]);
   } else if (pre) {
     if (live)
       subst_entry(s, t, pc, pAl, pEl, pUl, pAg, pEg, pUg, loser, gain, s.vfixed[loser],

@@ -711,8 +711,8 @@ __device__ __forceinline__ long long tix(const Scenario& s, int t, int v);
 // block-wide phase with a single barrier.
 template <int NT, bool HELP>
 __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Smem& sm, int q,
-                                        int j, int loser, int gain, double mc_old, int nl,
-                                        int ng) {
+                                        int j, int loser, int gain, double mc_old, double mc_new,
+                                        int nl, int ng) {
   const int wd = q >> 5;
   const uint32_t bit = 1u << (q & 31);
   // One base per thread (B <= NT, no helpers): the table entries this
@@ -745,14 +745,16 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     s.mem[(long long)loser * s.nwd + wd] &= ~bit;
     s.mem[(long long)gain * s.nwd + wd] |= bit;
   }
-  if (logged && threadIdx.x == NT - 33) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, s.mcp[q]);
+  if (logged && threadIdx.x == NT - 33) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, mc_new);
   for (int g0 = 0; g0 < s.V; g0 += NT) {
     const int g = g0 + threadIdx.x;
     bool now = false;
     if (g < s.V) {
       uint32_t* wp = s.imp + (long long)g * s.nwd + wd;
       const bool was = (*wp & bit) != 0u;
-      now = imp_bit(s, g, q, j);
+      // imp_bit on the post-move state, from the move itself (thread 0 may
+      // still be writing mvp[q] / mcp[q]: no barrier after the apply)
+      now = gain != g && compat_vm(s.vfixed[g], s.rop[q]) && cost_mb(s, j, s.vbase[g]) < mc_new;
       put_bit(wp, bit, now);
       sm.impc[g] += (int)now - (int)was;
     }
@@ -764,9 +766,9 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
   } else if (pre) {
     if (live)
       subst_entry(s, t, pc, pAl, pEl, pUl, pAg, pEg, pUg, loser, gain, s.vfixed[loser],
-                  s.vfixed[gain], mc_old, s.mcp[q], nl, ng, single_bound(s, sh));
+                  s.vfixed[gain], mc_old, mc_new, nl, ng, single_bound(s, sh));
   } else {
-    table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, s.mcp[q], nl, ng);
+    table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, mc_new, nl, ng);
   }
   PH_ADD(sh, 10, tp0);
   __syncthreads();
@@ -1484,10 +1486,11 @@ __device__ void set_mission(const Scenario& s, const Smem& sm, int j, int v, dou
   }
 }
 
+// (newc: cost_mb(j, vbase[gain]), already gathered by the caller)
 __device__ void apply_takeover(const Scenario& s, Shared& sh, const Smem& sm, int j, int gain,
-                               int pos) {
+                               int pos, double newc) {
   const int loser = s.mv[j];
-  set_mission(s, sm, j, gain, cost_mb(s, j, s.vbase[gain]));
+  set_mission(s, sm, j, gain, newc);
   s.vcount[gain] += 1;
   s.vcount[loser] -= 1;
   if (s.vcount[loser] == 0) {
@@ -1502,9 +1505,10 @@ __device__ void apply_takeover(const Scenario& s, Shared& sh, const Smem& sm, in
   }
 }
 
-__device__ void apply_reassign(const Scenario& s, Shared& sh, const Smem& sm, int j, int gain) {
+__device__ void apply_reassign(const Scenario& s, Shared& sh, const Smem& sm, int j, int gain,
+                               double newc) {
   const int loser = s.mv[j];
-  set_mission(s, sm, j, gain, cost_mb(s, j, s.vbase[gain]));
+  set_mission(s, sm, j, gain, newc);
   s.vcount[gain] += 1;
   s.vcount[loser] -= 1;
   if (s.vcount[loser] == 0) {
@@ -1611,7 +1615,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
         const int nl = s.vcount[loser], ng = s.vcount[g];
         __syncthreads();  // everyone has read the pre-move state
         if (threadIdx.x == 0) {
-          apply_takeover(s, sh, sm, j, g, i);
+          apply_takeover(s, sh, sm, j, g, i, newc);
           sh.c.hp_valid = min(sh.c.hp_valid, j / kChainSub);
           sh.c.applied += 1;
           sh.c.pass_applied += 1;
@@ -1622,9 +1626,12 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           if (tabu) s.exp_take[g] = exp;
           if (debug) debug_check(s, sh);
         }
-        __syncthreads();
+        // the bit updates read nothing the apply writes (they take the move's
+        // new owner and cost as arguments): no barrier in between, except for
+        // the debug check and an adopted exact chain
+        if (debug || (HELP && acc == 3)) __syncthreads();
         const long long a2 = ph_now();
-        bits_after_substitution<NT, HELP>(s, sh, sm, q, j, loser, g, mcj, nl, ng);
+        bits_after_substitution<NT, HELP>(s, sh, sm, q, j, loser, g, mcj, newc, nl, ng);
         if (HELP && acc == 3) adopt_candidate_sums<NT>(s, sh);
         PH_ADD(sh, 7, a2);
       }
@@ -1722,7 +1729,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
           const int nl = s.vcount[l], ng = s.vcount[g];
           __syncthreads();
           if (threadIdx.x == 0) {
-            apply_reassign(s, sh, sm, j, g);
+            apply_reassign(s, sh, sm, j, g, newc);
             sh.c.hp_valid = min(sh.c.hp_valid, j / kChainSub);
             sh.c.applied += 1;
             sh.c.pass_applied += 1;
@@ -1734,9 +1741,9 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
             sh.reassigned = 1;
             if (debug) debug_check(s, sh);
           }
-          __syncthreads();
+          if (debug || (HELP && acc == 3)) __syncthreads();  // (see the takeover)
           const long long a2 = ph_now();
-          bits_after_substitution<NT, HELP>(s, sh, sm, q, j, l, g, mcj, nl, ng);
+          bits_after_substitution<NT, HELP>(s, sh, sm, q, j, l, g, mcj, newc, nl, ng);
           if (HELP && acc == 3) adopt_candidate_sums<NT>(s, sh);
           PH_ADD(sh, 7, a2);
         }

@@ -1896,7 +1896,9 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
       uint32_t relw = 0;
       if (rel_t >= 0 && nrl <= 8) {
         // relocation candidates: the positions of the few movers that can gain
+        // (unrolled: the membership words' gathers are in flight together)
         if (wd < nwd)
+#pragma unroll 4
           for (int k = 0; k < nrl; ++k) relw |= s.mem[(long long)sm.rlist[k] * nwd + wd];
       } else if (rel_t >= 0) {
         // many movers: the vehicle of every position, one coalesced pass over
@@ -1918,6 +1920,7 @@ __device__ void run_row(const Scenario& s, Shared& sh, const Smem& sm, int i, bo
         if (tabu) {
           outer = prefix_bits(p_seg + lim_ro - base);
           blk = prefix_bits(p_seg + lim_ra - base);
+#pragma unroll 4
           for (int k = 0; k < nj; ++k) {
             const uint32_t m =
                 s.mem[(long long)sm.jl_v[k] * nwd + wd] &

@@ -746,27 +746,36 @@ __device__ void bits_after_substitution(const Scenario& s, Shared& sh, const Sme
     s.mem[(long long)gain * s.nwd + wd] |= bit;
   }
   if (logged && threadIdx.x == NT - 33) log_append(s, sh, sm, j, loser, gain, nl, ng, mc_old, mc_new);
+  // the first vehicle block's gathers are issued before this thread's table
+  // patch, whose arithmetic then overlaps their latency
+  uint32_t w_first = 0u;
+  double c_first = 0.0;
+  if (threadIdx.x < s.V) {
+    w_first = s.imp[(long long)threadIdx.x * s.nwd + wd];
+    c_first = cost_mb(s, j, s.vbase[threadIdx.x]);
+  }
+  if (live)
+    subst_entry(s, t, pc, pAl, pEl, pUl, pAg, pEg, pUg, loser, gain, s.vfixed[loser],
+                s.vfixed[gain], mc_old, mc_new, nl, ng, single_bound(s, sh));
   for (int g0 = 0; g0 < s.V; g0 += NT) {
     const int g = g0 + threadIdx.x;
     bool now = false;
     if (g < s.V) {
       uint32_t* wp = s.imp + (long long)g * s.nwd + wd;
-      const bool was = (*wp & bit) != 0u;
+      const uint32_t wv = g0 == 0 ? w_first : *wp;
+      const double cg = g0 == 0 ? c_first : cost_mb(s, j, s.vbase[g]);
+      const bool was = (wv & bit) != 0u;
       // imp_bit on the post-move state, from the move itself (thread 0 may
       // still be writing mvp[q] / mcp[q]: no barrier after the apply)
-      now = gain != g && compat_vm(s.vfixed[g], s.rop[q]) && cost_mb(s, j, s.vbase[g]) < mc_new;
-      put_bit(wp, bit, now);
+      now = gain != g && compat_vm(s.vfixed[g], s.rop[q]) && cg < mc_new;
+      *wp = now ? (wv | bit) : (wv & ~bit);
       sm.impc[g] += (int)now - (int)was;
     }
     // the mission's natural-order row
     const unsigned row = __ballot_sync(FULL, now);
     if ((threadIdx.x & 31) == 0 && g < s.V) s.impT[(long long)j * s.nvw + (g >> 5)] = row;
   }
-  if (logged) {
-  } else if (pre) {
-    if (live)
-      subst_entry(s, t, pc, pAl, pEl, pUl, pAg, pEg, pUg, loser, gain, s.vfixed[loser],
-                  s.vfixed[gain], mc_old, mc_new, nl, ng, single_bound(s, sh));
+  if (logged || pre) {
   } else {
     table_after_substitution<NT>(s, sh, j, loser, gain, mc_old, mc_new, nl, ng);
   }

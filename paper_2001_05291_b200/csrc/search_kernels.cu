@@ -1609,18 +1609,21 @@ __device__ bool exact_accept_single(const Scenario& s, Shared& sh, const Smem& s
 template <int NT, bool HELP>
 __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int i, int q,
                              bool tabu, long long tenure, bool debug) {
+  // mission j = perm_b[q]; its owner, cost and rotary flag are read from the
+  // position-order mirrors (kept in sync on every move), so they do not wait
+  // for the perm_b gather
   const int j = sm.pb[q];
   const long long exp = sh.c.tick + tenure;
   // ---- takeover (proj/src/search.cpp:82-101)
   if (i < sh.c.psize && s.pkind[i] == POOL_IDLE) {
     const int g = s.pidx[i];
     const double newc = cost_mb(s, j, s.vbase[g]);
-    const double mcj = s.mc[j];
-    if (compat_vm(s.vfixed[g], s.ro[j]) && newc - mcj < 0.0) {
+    const double mcj = s.mcp[q];
+    if (compat_vm(s.vfixed[g], s.rop[q]) && newc - mcj < 0.0) {
       int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
       if (!acc) acc = exact_accept_single<NT, HELP>(s, sh, sm, j, newc) ? 3 : 0;
       if (acc) {
-        const int loser = s.mv[j];
+        const int loser = s.mvp[q];
         const int nl = s.vcount[loser], ng = s.vcount[g];
         __syncthreads();  // everyone has read the pre-move state
         if (threadIdx.x == 0) {
@@ -1649,7 +1652,7 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
   // ---- relocation (proj/src/search.cpp:103-129), on the state left behind
   if (i < sh.c.psize && s.pkind[i] == POOL_EMPTY) {
     const int t = s.pidx[i];
-    const int mover = s.mv[j];
+    const int mover = s.mvp[q];
     if (!(s.vfixed[mover] && s.bheli[t])) {
       relocation_classes<NT, HELP>(s, sh, sm, t);
       const uint8_t cls = sm.cls[mover];
@@ -1727,10 +1730,10 @@ __device__ void process_pair(const Scenario& s, Shared& sh, const Smem& sm, int 
   }
   // ---- reassignment (proj/src/search.cpp:131-148)
   {
-    const int g = s.mv[i], l = s.mv[j];
-    if (g != l && compat_vm(s.vfixed[g], s.ro[j])) {
+    const int g = s.mv[i], l = s.mvp[q];
+    if (g != l && compat_vm(s.vfixed[g], s.rop[q])) {
       const double newc = cost_mb(s, j, s.vbase[g]);
-      const double mcj = s.mc[j];
+      const double mcj = s.mcp[q];
       if (newc - mcj < 0.0) {
         int acc = mcj - newc > single_bound(s, sh) ? 1 : 0;
         if (!acc) acc = exact_accept_single<NT, HELP>(s, sh, sm, j, newc) ? 3 : 0;

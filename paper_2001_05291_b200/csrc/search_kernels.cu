@@ -2086,7 +2086,10 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 // improvement row (NVW words) and the warp transposes it into the V
 // position-order words with ballots; mem from the mirrored vehicles.
 __device__ void prep_words(const Scenario& s, const int32_t* __restrict__ pb, int wd0, int wstride) {
-  constexpr int UW = 4;  // words per warp iteration: their loads in flight together
+#ifndef FP_PREP_UW
+#define FP_PREP_UW 4
+#endif
+  constexpr int UW = FP_PREP_UW;  // words per warp iteration: their loads in flight together
   const int l = threadIdx.x & 31;
   const int nvw = s.nvw, V = s.V;
   for (int wb = wd0; wb < s.nwd; wb += wstride * UW) {

@@ -431,9 +431,20 @@ __device__ void chain_steps(const Scenario& s, Shared& sh, int kind, int j, doub
 template <int NT>
 __device__ double exact_chain(const Scenario& s, Shared& sh, int kind, int j, double newc,
                               int mover, const double* col) {
+  // The head of a chain from zero crosses a binade every time the running
+  // sum doubles (~log2(k) events in its first k terms, each a block step):
+  // its first kChainSeqHead terms are summed by one thread with plain fp64
+  // adds in order -- the reference's own loop, exact by definition -- and
+  // the block steps take over once the running sum is large.
+  constexpr int kChainSeqHead = 1024;
   if (threadIdx.x == 0) {
-    sh.xs = 0.0;
-    sh.xk = 0;
+    const int kh = min(s.M, kChainSeqHead);
+    double S = 0.0;
+    int k = 0;
+#pragma unroll 8
+    for (; k < kh; ++k) S += chain_term(s, kind, k, j, newc, mover, col);
+    sh.xs = S;
+    sh.xk = k;
   }
   __syncthreads();
   chain_steps<NT>(s, sh, kind, j, newc, mover, col, s.M);

@@ -436,15 +436,25 @@ __device__ double exact_chain(const Scenario& s, Shared& sh, int kind, int j, do
   // its first kChainSeqHead terms are summed by one thread with plain fp64
   // adds in order -- the reference's own loop, exact by definition -- and
   // the block steps take over once the running sum is large.
+  // (warp 0: coalesced loads of 32 terms, the next 32 in flight while every
+  // lane adds the current ones in order from shuffles)
   constexpr int kChainSeqHead = 1024;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    const int l = threadIdx.x;
     const int kh = min(s.M, kChainSeqHead);
     double S = 0.0;
-    int k = 0;
-#pragma unroll 8
-    for (; k < kh; ++k) S += chain_term(s, kind, k, j, newc, mover, col);
-    sh.xs = S;
-    sh.xk = k;
+    double nxt = l < kh ? chain_term(s, kind, l, j, newc, mover, col) : 0.0;
+    for (int k0 = 0; k0 < kh; k0 += 32) {
+      const double cur = nxt;
+      const int kk = k0 + 32 + l;
+      if (kk < kh) nxt = chain_term(s, kind, kk, j, newc, mover, col);
+      const int n = min(32, kh - k0);
+      for (int q = 0; q < n; ++q) S += __shfl_sync(FULL, cur, q);
+    }
+    if (l == 0) {
+      sh.xs = S;
+      sh.xk = kh;
+    }
   }
   __syncthreads();
   chain_steps<NT>(s, sh, kind, j, newc, mover, col, s.M);

@@ -410,8 +410,10 @@ __device__ void chain_steps(const Scenario& s, Shared& sh, int kind, int j, doub
     // aligned boundaries in [k0, lim] have their running sum in binade e
     const int lim = ev == INT_MAX ? min(kend, k0 + per * NW) : ev;
     {
+      // (hec has one entry per chunk start: c < ceil(M / kChainSub); a chain
+      // ending exactly on a chunk boundary must not record the next one)
       const int c = (k0 + kChainSub - 1) / kChainSub + threadIdx.x;
-      if ((long long)c * kChainSub <= lim) s.hec[c] = e;
+      if ((long long)c * kChainSub <= lim && c < (s.M + kChainSub - 1) / kChainSub) s.hec[c] = e;
     }
     if (ev == INT_MAX) {
       if (threadIdx.x == 0) {

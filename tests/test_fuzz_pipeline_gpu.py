@@ -90,3 +90,25 @@ def test_fuzzed_instance_whole_pipeline_bit_exact(k):
                 s.tabu_skips_inner, s.final_objective_km) == ref.stats, (mode, seed, tenure)
         assert np.array_equal(got.vehicle_base, ref.vehicle_base)
         assert np.array_equal(got.mission_vehicle, ref.mission_vehicle)
+
+
+@pytest.mark.parametrize("shape,passes", [((120, 4096, 15), None), ((300, 6144, 30), 15)])
+def test_mission_counts_on_chunk_boundaries(shape, passes):
+    """M a multiple of the exact chains' 2048-term chunk: a chain that ends
+    exactly on a chunk boundary records no binade past the last chunk (the
+    round-2 bound fix); the whole pipeline still equals the reference."""
+    inst = F.survey_instance(*shape, seed=3)
+    t = F.build_distance_table(inst)
+    ref_cost = H.ref_table(inst)
+    r = H.ref_rank(inst, ref_cost)
+    start = F.rank_bases(inst, t)
+    assert np.array_equal(start.vehicle_base, r.vehicle_base)
+    pk, px = H.initial_pool_idx(inst, r.vehicle_base, r.mission_vehicle, r.unused)
+    ref = H.ref_search(inst, ref_cost, 1, 7, r.vehicle_base, r.mission_vehicle, pk, px,
+                       max_passes=passes)
+    got = F.search_arrays(inst, t, F.SearchConfig(seed=7, mode=F.SearchMode.Tabu, max_passes=passes),
+                          start.vehicle_base, start.mission_vehicle, pk, px)
+    s = got.stats
+    assert (s.passes, s.evaluations, s.applied_moves, s.committed_moves, s.tabu_skips_outer,
+            s.tabu_skips_inner, s.final_objective_km) == ref.stats
+    assert np.array_equal(got.mission_vehicle, ref.mission_vehicle)

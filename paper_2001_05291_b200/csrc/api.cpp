@@ -1029,7 +1029,10 @@ void run_search(fp_ctx* ctx, int n, const fp_instance* insts, const fp_search_co
   if (cost_t && ctx_copy && ctx->costT_valid && ctx->costT_ready)
     check(cudaStreamWaitEvent(st, ctx->costT_ready, 0), "wait");
   // (a sweep alone does not need the exact start total)
-  check(fpk::launch_init(d_scs, run.scs.data(), n, M, maxB, maxV, transpose, st, ei, !sweep),
+  if (std::getenv("FLEETPLACE_INIT_SIDE") && !ctx->aux)
+    check(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking), "stream");
+  check(fpk::launch_init(d_scs, run.scs.data(), n, M, maxB, maxV, transpose, st, ei, !sweep,
+                         ctx->aux),
         "init_kernel");
   if (ctx_copy && cost_t) ctx->costT_valid = true;
   const bool rows_stream = n == 1 && cost_t && M > 0 && maxB > 0 && maxV > 0;

@@ -54,7 +54,7 @@ cudaError_t launch_candidate_delta(const double* cost, int M, const int32_t* vb,
                                    cudaStream_t st);
 cudaError_t launch_init(Scenario* d_scs, const Scenario* h_scs, int n_scn, int M, int maxB,
                         int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev,
-                        bool exact_total = true);
+                        bool exact_total = true, cudaStream_t side = nullptr);
 cudaError_t launch_final(Scenario* d_scs, int n_scn, cudaStream_t stream);
 cudaError_t launch_gather_results(const Scenario* d_scs, int n_scn, int M, int32_t* out_mv,
                                   int32_t* out_vb, const long long* vb_off, cudaStream_t stream);

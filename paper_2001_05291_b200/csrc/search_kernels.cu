@@ -2982,16 +2982,32 @@ cudaError_t launch_pass(Scenario* d_scs, const int32_t* d_active, int n_scn,
 }
 
 // ev[0..4]: events recorded around the four stages (may be null).
+// side: a second stream, used only by the FLEETPLACE_INIT_SIDE fault probe
+// (1: the exact start total concurrent with the row builds, 2: on the side
+// stream but joined at once); the shipped path runs everything in order.
 cudaError_t launch_init(Scenario* d_scs, const Scenario* h_scs, int n_scn, int M, int maxB,
                         int maxV, bool transpose, cudaStream_t stream, cudaEvent_t* ev,
-                        bool exact_total) {
+                        bool exact_total, cudaStream_t side) {
   if (ev) cudaEventRecord(ev[0], stream);
   if (transpose && M > 0 && maxB > 0)
     transpose_kernel<<<dim3((M + 63) / 64, (maxB + 31) / 32, n_scn), 256, 0, stream>>>(d_scs);
   if (ev) cudaEventRecord(ev[1], stream);
   if (M > 0)
     mission_cost_kernel<<<dim3(std::min((M + 255) / 256, 4 * 148), n_scn), 256, 0, stream>>>(d_scs);
-  if (exact_total) init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
+  const char* probe = std::getenv("FLEETPLACE_INIT_SIDE");
+  const int side_mode = probe && side && side != stream && exact_total ? std::atoi(probe) : 0;
+  cudaEvent_t costs_done = nullptr, total_done = nullptr;
+  if (side_mode) {
+    cudaEventCreateWithFlags(&costs_done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&total_done, cudaEventDisableTiming);
+    cudaEventRecord(costs_done, stream);
+    cudaStreamWaitEvent(side, costs_done, 0);
+    init_kernel<<<n_scn, 512, 0, side>>>(d_scs);
+    cudaEventRecord(total_done, side);
+    if (side_mode == 2) cudaStreamWaitEvent(stream, total_done, 0);
+  } else if (exact_total) {
+    init_kernel<<<n_scn, 512, 0, stream>>>(d_scs);
+  }
   if (ev) cudaEventRecord(ev[2], stream);
   if (M > 0) impt_init_kernel<<<dim3((M + 255) / 256, n_scn), 256, 0, stream>>>(d_scs);
   if (ev) cudaEventRecord(ev[3], stream);
@@ -3011,6 +3027,11 @@ cudaError_t launch_init(Scenario* d_scs, const Scenario* h_scs, int n_scn, int M
     const size_t smem = sizeof(double) * (16ull * maxV + 8 * 32);
     cudaFuncSetAttribute(table_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (maxB > 0) table_rows_kernel<<<dim3(maxB, n_scn), 256, smem, stream>>>(d_scs);
+  }
+  if (side_mode) {
+    cudaStreamWaitEvent(stream, total_done, 0);
+    cudaEventDestroy(total_done);
+    cudaEventDestroy(costs_done);
   }
   if (ev) cudaEventRecord(ev[4], stream);
   return cudaGetLastError();
